@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py — SA / LLSA fwd+bwd frames/s on B200 (BASELINE.json metric) + roofline + CPU-oracle baseline.
+
+Step (one pass of the hot path over one batch): the attention core of a 12-layer
+wav2vec2/HuBERT-base encoder, forward then backward —
+    for l in 0..11:  sa_forward(Q_l, K_l, V_l) -> O_l, LSE_l
+    for l in 11..0:  sa_backward(Q_l, K_l, V_l, O_l, LSE_l, dO_l) -> dQ_l, dK_l, dV_l
+on synthetic iid N(0,1) bf16 activations, B=8 sequences x T=1750 frames (35 s at
+50 Hz), H=12 heads, D=64, band (L, R) = (32, 8) (Table 3's l32_r8), distinct
+per-layer tensors (2.3 GB working set >> 126 MB L2, so no L2 flush is needed).
+A "frame" is one time step of one sequence carried through all heads and layers,
+forward and backward: frames/step = B*T.  The same step with LLSA (C = R+1 = 9
+channels per frame) is reported under "llsa".
+
+Multi-GPU (torchrun, one rank per GPU): batch x head sharding is embarrassingly
+parallel - every rank runs its own B=8 batch, no data-path
+collective; scaling "weak"; value = frames of all ranks / max-over-ranks time.
+
+--impl reference runs the CPU oracle (oracle/, numpy fp64) on a bounded sample of
+the same workload (the task's reference arm for this paper-only reference).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, H, T, D, L, R, NL = 8, 12, 1750, 64, 32, 8, 12
+METRIC = "SA/LLSA fwd+bwd frames/sec (12L, H=12, D=64) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "frames/s"
+# algorithmic bytes per head*layer*frame: bf16 activations, fp32 LSE
+FWD_BYTES = 8 * D + 4            # read Q,K,V + write O (2 B each) + LSE (4 B)   = 516
+BWD_BYTES = 16 * D + 4           # read Q,K,V,O,dO + LSE, write dQ,dK,dV        = 1028
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), float(j["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------------- GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2302_13451_b200 as sattn
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    bf = torch.bfloat16
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+
+    def rnd(*shape):
+        return torch.randn(*shape, device=dev, generator=g, dtype=torch.float32).to(bf)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    # ---------------- SA workload: distinct per-layer tensors
+    shp = (B, H, T, D)
+    Qs, Ks, Vs, dOs = ([rnd(*shp) for _ in range(NL)] for _ in range(4))
+    Os = [torch.empty(shp, device=dev, dtype=bf) for _ in range(NL)]
+    LSEs = [torch.empty(shp[:-1], device=dev, dtype=torch.float32) for _ in range(NL)]
+    dQs, dKs, dVs = ([torch.empty(shp, device=dev, dtype=bf) for _ in range(NL)] for _ in range(3))
+    ws = torch.empty(sattn.lib().sa_backward_workspace(__import__("ctypes").byref(
+        sattn.make_desc(B, H, T, D, L, R, sattn.BF16))), device=dev, dtype=torch.uint8)
+    lib = sattn.lib()
+    import ctypes
+    desc = sattn.make_desc(B, H, T, D, L, R, sattn.BF16, impl=args.kernels)
+    pd = ctypes.byref(desc)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    nws = ws.numel()
+
+    def check(st, what):
+        if st != 0:
+            raise RuntimeError(f"{what}: {lib.sattn_last_error().decode()}")
+
+    ev = {"fwd": [], "bwd": []}
+
+    def step(record=False):
+        for l in range(NL):
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True); e0.record(stream)
+            check(lib.sa_forward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), sp), "sa_forward")
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True); e1.record(stream); ev["fwd"].append((e0, e1))
+        for l in reversed(range(NL)):
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True); e0.record(stream)
+            check(lib.sa_backward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), P(dOs[l]),
+                                  P(dQs[l]), P(dKs[l]), P(dVs[l]), P(ws), nws, sp), "sa_backward")
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True); e1.record(stream); ev["bwd"].append((e0, e1))
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    time.sleep(0.3)
+    n0 = sattn.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    launches = sattn.launch_count() - n0
+    ms = t0.elapsed_time(t1)
+    ms_max = ms
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_max = float(tt.item())
+    ms_per_step = ms_max / args.steps
+    frames = world * B * T * args.steps
+    value = frames / (ms_max / 1e3)
+
+    fwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["fwd"]]))
+    bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["bwd"]]))
+    units = B * H * T  # head-frames per launch
+    hbm, tc_peak, peak_kind = load_peaks()
+    kern = {"sa_forward": (fwd_ms, FWD_BYTES * units), "sa_backward": (bwd_ms, BWD_BYTES * units)}
+    dom = max(kern, key=lambda k: kern[k][0])
+    achieved = kern[dom][1] / (kern[dom][0] / 1e3) / 1e9
+    traffic = load_traffic(dom, args.kernels)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": kern[dom][1],
+                "per_call_ms": {k: round(v[0], 4) for k, v in kern.items()},
+                "step_frac": {k: round(v[0] * NL / ms_per_step, 3) for k, v in kern.items()},
+                "step_hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * NL / (ms_per_step / 1e3) / 1e9 / hbm, 4)}
+
+    # ---------------- e2e through the public API with host buffers (pinned), H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        hin = [[torch.empty(shp, dtype=bf, pin_memory=True) for _ in range(4)] for _ in range(NL)]
+        hout = [[torch.empty(shp, dtype=bf, pin_memory=True) for _ in range(3)] for _ in range(NL)]
+        for l in range(NL):
+            for j, src in enumerate((Qs, Ks, Vs, dOs)):
+                hin[l][j].copy_(src[l])
+
+        def e2e_step():
+            for l in range(NL):
+                for j, dst in enumerate((Qs, Ks, Vs, dOs)):
+                    dst[l].copy_(hin[l][j], non_blocking=True)
+            step()
+            for l in range(NL):
+                for j, src in enumerate((dQs, dKs, dVs)):
+                    hout[l][j].copy_(src[l], non_blocking=True)
+
+        e2e_step()
+        barrier()
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        n_e2e = max(2, min(args.steps, 5))
+        a0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        a1.record(stream)
+        barrier()
+        e_ms = a0.elapsed_time(a1)
+        if world > 1:
+            tt = torch.tensor([e_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        el = 2 * B * H * T * D
+        e2e = {"value": round(world * B * T * n_e2e / (e_ms / 1e3), 1), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * NL * el, "d2h_bytes_per_step": 3 * NL * el, "steps": n_e2e}
+        del hin, hout
+
+    # ---------------- LLSA step (same shape, C = R+1 channels), reported alongside
+    llsa = None
+    if not args.no_llsa:
+        del Qs, Ks, Vs, dOs, Os, dQs, dKs, dVs
+        torch.cuda.empty_cache()
+        llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_seconds)
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic iid N(0,1) activations",
+           "config": {"workload": "wav2vec2-base attention core: 12 layers x (SA fwd + SA bwd), untied per-layer "
+                                  "Q/K/V/dO, bf16 in/out, fp32 accumulate",
+                      "B": B, "H": H, "T": T, "D": D, "L": L, "R": R, "layers": NL, "global_batch": B * world,
+                      "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
+                      "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
+           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa,
+           "cpu_baseline": cpu}
+    print(json.dumps(out))
+
+
+def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
+    import ctypes
+    import torch
+    lib = sattn.lib()
+    C = R + 1
+    shp = (C, B, H, T, D)
+    bf = torch.bfloat16
+    n_layers = NL
+    Q, K, V, dO = ([rnd(*shp) for _ in range(n_layers)] for _ in range(4))
+    O = [torch.empty(shp, device=dev, dtype=bf) for _ in range(n_layers)]
+    LSE = [torch.empty(shp[:-1], device=dev, dtype=torch.float32) for _ in range(n_layers)]
+    dQ, dK, dV = torch.empty(shp, device=dev, dtype=bf), torch.empty(shp, device=dev, dtype=bf), \
+        torch.empty(shp, device=dev, dtype=bf)
+    desc = sattn.make_desc(B, H, T, D, L, R, sattn.BF16, impl=args.kernels)
+    pd = ctypes.byref(desc)
+    nws = lib.llsa_backward_workspace(pd)
+    ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
+    def step():
+        for l in range(n_layers):
+            assert lib.llsa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), sp) == 0
+        for l in reversed(range(n_layers)):
+            assert lib.llsa_backward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(dO[l]), P(dQ), P(dK),
+                                     P(dV), P(ws), nws, sp) == 0
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    barrier()
+    k = max(1, min(args.steps, 5))
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(k):
+        step()
+    a1.record(stream)
+    barrier()
+    ms = a0.elapsed_time(a1) / k
+    bytes_step = (FWD_BYTES + BWD_BYTES) * C * B * H * T * n_layers
+    return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "channels": C, "hbm_frac": round(bytes_step / (ms / 1e3) / 1e9 / hbm, 4), "steps": k,
+            "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
+
+
+def load_traffic(kernel, impl):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        j = json.load(open(p))
+        e = j.get(f"{kernel}:{impl}") or j.get(kernel)
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------- CPU oracle
+
+def _oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return int(max(n)) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(budget_s: float = 15.0, steps: int | None = None):
+    """Time the oracle (as it stands) on host cores on a bounded sample: SA forward + backward of
+    single (batch, head) planes of one layer at the bench shape; frames/s scaled to the metric
+    (one frame = H heads x 12 layers of fwd+bwd)."""
+    import oracle
+    import synth
+    q, k, v = synth.qkv(0, (T, D), "bf16")
+    do = synth.grad_out(0, (T, D), "bf16")
+    times = []
+    t_start = time.perf_counter()
+    n = 0
+    while True:
+        a = time.perf_counter()
+        oracle.sa.sa_forward(q, k, v, L, R)
+        oracle.sa.sa_backward(q, k, v, do, L, R)
+        times.append(time.perf_counter() - a)
+        n += 1
+        if steps is not None and n >= steps:
+            break
+        if steps is None and time.perf_counter() - t_start > budget_s:
+            break
+    per_head_layer = float(np.mean(times))
+    value = T / (per_head_layer * H * NL)
+    return {"value": round(value, 3), "unit": UNIT, "cores": _oracle_threads(), "kind": "oracle",
+            "sample": f"{n} x one (batch, head) plane, one layer, SA fwd+bwd at T={T}, D={D}, (L,R)=({L},{R}), "
+                      f"numpy fp64 dense masked T x T; {per_head_layer:.3f} s each; scaled to H={H} x {NL} layers",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_baseline(steps=1)
+    t0 = time.perf_counter()
+    cb = cpu_baseline(steps=args.steps)
+    wall = time.perf_counter() - t0
+    out = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall / args.steps * 1e3, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic iid N(0,1) activations (bf16-rounded)",
+           "config": {"workload": "wav2vec2-base attention core: 12 layers x (SA fwd + SA bwd) — CPU oracle on a "
+                                  "bounded sample (one (batch, head) plane of one layer per step)",
+                      "B": B, "H": H, "T": T, "D": D, "L": L, "R": R, "layers": NL},
+           "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernels", default="auto", choices=["auto", "ffma", "tc"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-llsa", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * sattn.h — C ABI of libsattn.so: streaming attention (SA) and low-latency
+ * streaming attention (LLSA) of arXiv 2302.13451 on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:Lx = line x of the paper text; readings G1..G23 are
+ * listed in DESIGN.md §3.  Letters (reading G1): L = look-back (the paper's B),
+ * R = look-ahead (the paper's A), B = batch, H = heads, T = frames (N_T),
+ * D = head dim (d_k = d_v), C = R + 1 LLSA channels.
+ *
+ * Conventions (every entry point):
+ *  - Tensor pointers are DEVICE pointers owned by the caller, contiguous
+ *    row-major, 16-byte aligned.  SA tensors are [B][H][T][D]; LLSA tensors
+ *    are channel-major [C][B][H][T][D] (channel c = the version of a frame
+ *    computed with c look-ahead frames).  LSE / delta are fp32
+ *    [B][H][T] (SA) or [C][B][H][T] (LLSA).
+ *  - Element type of Q/K/V/O/dO/dQ/dK/dV/X/Y is desc->dtype (SATTN_F32 or
+ *    SATTN_BF16); arithmetic is fp32 (FFMA or tensor-core fp32 accumulate).
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Argument
+ *    validation is synchronous and returns an error status before anything is
+ *    enqueued; execution is asynchronous on `stream`.  Hot calls never
+ *    allocate; workspaces are sized by the *_workspace / *_bytes queries.
+ *  - No C++ exception crosses this boundary.  On failure the call returns a
+ *    non-zero sattn_status and sattn_last_error() (thread-local) describes it.
+ *  - Non-finite inputs are not checked on the GPU (NaN propagates).
+ *  - LSE is in natural-log units: LSE_t = log sum_{u in window(t)} exp(z_tu),
+ *    z_tu = scale * q_t . k_u (Eq. 4).
+ */
+#ifndef SATTN_H
+#define SATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SATTN_OK = 0,
+  SATTN_EARG = 1,          /* bad size / pointer / alignment / band */
+  SATTN_ESTATE = 2,        /* call not valid in the handle's current state */
+  SATTN_ECONFIG = 3,       /* inconsistent configuration (e.g. workspace too small) */
+  SATTN_EUNSUPPORTED = 4,  /* valid but not implemented (dtype x D x impl) */
+  SATTN_ECUDA = 5,         /* a CUDA runtime/driver call failed */
+  SATTN_ENCCL = 6          /* reserved for the time-sharded (NCCL) path */
+} sattn_status;
+
+enum { SATTN_F32 = 0, SATTN_BF16 = 1 };            /* desc->dtype */
+enum { SATTN_MODE_SA = 0, SATTN_MODE_LLSA = 1 };   /* stack mode */
+enum {                                             /* desc->impl */
+  SATTN_IMPL_AUTO = 0,  /* fastest available kernel family for dtype x D */
+  SATTN_IMPL_FFMA = 1,  /* CUDA-core fp32 FFMA kernels (any supported D) */
+  SATTN_IMPL_TC = 2     /* tcgen05 tensor-core kernels (bf16, D = 64) */
+};
+
+typedef struct {
+  int64_t B, H, T, D;      /* batch, heads, frames, head dim (D in {2,4,8,16,32,64}) */
+  int32_t L, R;            /* look-back / look-ahead frames, >= 0 (Eq. 4) */
+  int32_t dtype;           /* SATTN_F32 | SATTN_BF16 */
+  float scale;             /* score scale; 0 -> 1/sqrt(D) (G15) */
+  int32_t in_broadcast;    /* LLSA inputs only: 1 -> Q,K,V are a single [B][H][T][D]
+                              tensor read as every channel (layer-1 duplication,
+                              P:L283, G11); 0 -> dense [C][B][H][T][D] */
+  int32_t impl;            /* SATTN_IMPL_* */
+} sattn_desc;
+
+/* ---------------- SA: Eq. 4-13 ----------------------------------
+ * sa_forward: O_t = sum_{u=t-L}^{t+R} softmax_u(z_tu) V_u, window clipped to
+ * [0, T-1] (G2); writes O [B][H][T][D] and LSE [B][H][T].                      */
+sattn_status sa_forward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                        void* O, float* LSE, void* stream);
+
+/* sa_backward: exact gradients dQ, dK, dV of <dO, O> (Eq. 7-13 with Eq. 7's
+ * index condition, G3).  O and LSE must come from sa_forward on the same
+ * inputs (not checked: undefined results otherwise).  ws >= sa_backward_workspace(desc)
+ * bytes of device memory (holds delta_t = dO_t . O_t, fp32).  Deterministic
+ * (no atomics): bitwise reproducible run to run.                              */
+size_t sa_backward_workspace(const sattn_desc* desc);
+sattn_status sa_backward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                         const void* O, const float* LSE, const void* dO,
+                         void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------- LLSA: Eq. 14-16 -------------------------------
+ * Output (t, c) attends the Eq. 14 slots read in the Fig. 3(c) convention (G6):
+ * anchor s = t-(R-c); slots (u, R) for u in [s-L, s] and (s+j, R-j), j=1..R,
+ * clipped to [0, T-1]; query q_{t,c} (G7).  Q,K,V: [C][B][H][T][D] or, with
+ * desc->in_broadcast, one [B][H][T][D] tensor used for every channel.
+ * O: [C][B][H][T][D]; LSE: [C][B][H][T].                                      */
+sattn_status llsa_forward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                          void* O, float* LSE, void* stream);
+
+/* llsa_backward: exact gradient (G8/G9).  dQ,dK,dV are always dense
+ * [C][B][H][T][D] (gradient per channel slot; with in_broadcast the caller
+ * sums over channels).  ws >= llsa_backward_workspace(desc).  Deterministic.  */
+size_t llsa_backward_workspace(const sattn_desc* desc);
+sattn_status llsa_backward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                           const void* O, const float* LSE, const void* dO,
+                           void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------- layer-stack driver (reading G12) ---------
+ * n_layers tied-QKV layers: Y_l = ATT(X_l, X_l, X_l), X_{l+1} = (X_l + Y_l)/2,
+ * ATT = SA (mode SATTN_MODE_SA) or LLSA (SATTN_MODE_LLSA; X_0 duplicated into
+ * all channels).  X0: [B][H][T][D].  Y = X_{n}: [B][H][T][D] (SA) or
+ * [C][B][H][T][D] (LLSA; designated output = channel R, G10).
+ * `saved` (>= sattn_stack_saved_bytes) keeps X_l, O_l, LSE_l for the backward.
+ * desc->in_broadcast is ignored (the driver sets it per layer).               */
+size_t sattn_stack_saved_bytes(const sattn_desc* desc, int mode, int n_layers);
+sattn_status sattn_stack_forward(const sattn_desc* desc, int mode, int n_layers, const void* X0,
+                                 void* saved, size_t saved_bytes, void* Y, void* stream);
+/* Gradient of <dY, Y> w.r.t. X0 (dY shaped like Y; dX0 [B][H][T][D]).
+ * ws >= sattn_stack_workspace(desc, mode, n_layers).                          */
+size_t sattn_stack_workspace(const sattn_desc* desc, int mode, int n_layers);
+sattn_status sattn_stack_backward(const sattn_desc* desc, int mode, int n_layers, const void* saved,
+                                  const void* dY, void* dX0, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------- incremental LLSA inference (infer_llsa) -------------
+ * Library-owned state for n_layers tied-QKV LLSA layers (same block rule as
+ * the stack driver): per layer a ring of the channel-R frames of its input for
+ * the last L frames, plus the last R+1 raw frames.  desc->T is ignored
+ * (unbounded stream).  llsa_stream_step ingests x_new [B][H][D] for frame h
+ * (h = number of previous steps), runs horizon h through every layer in one
+ * kernel launch and, once h >= R, writes the designated output X_n(h-R, R) to
+ * y_out [B][H][D] and sets *out_frame = h-R (else *out_frame = -1; y_out
+ * untouched).  llsa_stream_flush ends the stream: it runs the remaining R
+ * horizons with windows clipped at the last frame and writes frames
+ * T-R..T-1 (those >= 0) to y_tail [R][B][H][D]; *n_out = number written.
+ * A handle is single-owner (not thread-safe); create allocates device memory,
+ * step/flush never allocate.  out_frame / n_out are host pointers.            */
+typedef struct sattn_stream sattn_stream;
+sattn_status llsa_stream_create(const sattn_desc* desc, int n_layers, sattn_stream** out);
+sattn_status llsa_stream_step(sattn_stream* s, const void* x_new, void* y_out, int64_t* out_frame,
+                              void* stream);
+sattn_status llsa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void* stream);
+sattn_status llsa_stream_reset(sattn_stream* s);
+void llsa_stream_destroy(sattn_stream* s);
+
+/* ---------------- misc ---------------------------------------------------------*/
+const char* sattn_last_error(void);      /* thread-local message of the last failure */
+const char* sattn_version(void);
+/* Number of kernel launches this library has enqueued since load (all threads).
+ * Launches replayed from a captured CUDA graph are not re-counted.            */
+int64_t sattn_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SATTN_H */

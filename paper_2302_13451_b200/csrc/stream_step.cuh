@@ -1,0 +1,129 @@
+// stream_step.cuh — one incremental LLSA step (infer_llsa).
+//
+// One launch runs horizon h through every layer.  CTA = one (batch, head) stream.
+// At horizon h each layer computes the R+1 outputs (h-c, c), c = 0..R, which all
+// share one window ("the same keys and values of the red vector are used"):
+//   slot i in [0, L]      (u = h-R-L+i, channel R): ring of the layer input (u < h-R)
+//                                                    or the current diagonal (u = h-R)
+//   slot i in [L+1, L+R]  (u = h-R-L+i, channel L+R-i): the current diagonal
+// so a (R+1) x (L+R+1) attention per layer; tied Q = K = V = the layer input
+// (reading G12), X_{l+1} = (X_l + O_l)/2 rounded exactly like the offline stack
+// (O rounded to the storage type first, then the half-sum).  Layer 1's diagonal is
+// the last R+1 raw frames (every channel of X_0 equals x).
+#pragma once
+#include "common.cuh"
+
+namespace sattn {
+
+struct StreamArgs {
+  const void* x_new;   // [BH][D] or nullptr (flush step)
+  void* raw;           // [BH][R+1][D], slot = frame mod (R+1)
+  void* ring;          // [n_layers][BH][L][D], slot = frame mod L
+  void* y_out;         // [BH][D] or nullptr
+  long long h, last;   // horizon and last valid frame
+  int n_layers, L, R, BH;
+  float scale_log2;
+};
+
+template <int D, typename T>
+__global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
+  constexpr int SD = D + 1;
+  extern __shared__ float sm[];
+  const int C = a.R + 1, W = a.L + a.R + 1;
+  const int L = a.L, R = a.R;
+  float* win = sm;                    // [W][SD]
+  float* diag = win + W * SD;         // [C][SD]
+  float* ndiag = diag + C * SD;       // [C][SD]
+  float* P = ndiag + C * SD;          // [C][W]
+  const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const long long h = a.h, last = a.last;
+  T* raw = reinterpret_cast<T*>(a.raw) + (long long)bh * C * D;
+
+  // layer-1 diagonal: X_0(h - c', c') = x_{h - c'}
+  if (a.x_new) {
+    const T* x = reinterpret_cast<const T*>(a.x_new) + (long long)bh * D;
+    for (int d = tid; d < D; d += nt) raw[(h % C) * D + d] = x[d];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < C * D; idx += nt) {
+    const int cp = idx / D, d = idx % D;
+    const long long f = h - cp;
+    diag[cp * SD + d] = (f >= 0 && f <= last) ? to_f(raw[(f % C) * D + d]) : 0.f;
+  }
+  __syncthreads();
+
+  for (int l = 0; l < a.n_layers; ++l) {
+    T* ring = L > 0 ? reinterpret_cast<T*>(a.ring) + ((long long)l * a.BH + bh) * L * D : nullptr;
+    // window rows (tied K = V)
+    for (int idx = tid; idx < W * D; idx += nt) {
+      const int i = idx / D, d = idx % D;
+      const long long u = h - R - L + i;
+      float x = 0.f;
+      if (u >= 0 && u <= last) {
+        if (i < L) x = to_f(ring[(u % L) * D + d]);
+        else if (i == L) x = diag[R * SD + d];
+        else x = diag[(L + R - i) * SD + d];
+      }
+      win[i * SD + d] = x;
+    }
+    __syncthreads();
+    // scores (log2 domain), masked to -inf for invalid slots / queries
+    for (int idx = tid; idx < C * W; idx += nt) {
+      const int c = idx / W, i = idx % W;
+      const long long u = h - R - L + i, t = h - c;
+      float s = neg_inf();
+      if (u >= 0 && u <= last && t >= 0 && t <= last) {
+        float acc = 0.f;
+#pragma unroll 16
+        for (int d = 0; d < D; ++d) acc = fmaf(diag[c * SD + d], win[i * SD + d], acc);
+        s = acc * a.scale_log2;
+      }
+      P[c * W + i] = s;
+    }
+    __syncthreads();
+    // softmax per query row: one warp per row
+    const int warp = tid >> 5, lane = tid & 31, nwarp = nt >> 5;
+    for (int c = warp; c < C; c += nwarp) {
+      float m = neg_inf();
+      for (int i = lane; i < W; i += 32) m = fmaxf(m, P[c * W + i]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float sum = 0.f;
+      for (int i = lane; i < W; i += 32) {
+        const float e = m == neg_inf() ? 0.f : exp2f(P[c * W + i] - m);
+        P[c * W + i] = e;
+        sum += e;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float inv = sum > 0.f ? 1.f / sum : 0.f;
+      for (int i = lane; i < W; i += 32) P[c * W + i] *= inv;
+    }
+    __syncthreads();
+    // values, block rule, rounding as the offline stack stores them
+    for (int idx = tid; idx < C * D; idx += nt) {
+      const int c = idx / D, d = idx % D;
+      float y = 0.f;
+      for (int i = 0; i < W; ++i) y = fmaf(P[c * W + i], win[i * SD + d], y);
+      const float o = to_f(from_f<T>(y));
+      ndiag[c * SD + d] = to_f(from_f<T>(0.5f * (diag[c * SD + d] + o)));
+    }
+    __syncthreads();
+    // X_l(h-R, R) joins this layer's ring (after every read of the ring above)
+    if (L > 0 && h - R >= 0 && h - R <= last)
+      for (int d = tid; d < D; d += nt) ring[((h - R) % L) * D + d] = from_f<T>(diag[R * SD + d]);
+    for (int idx = tid; idx < C * D; idx += nt) diag[(idx / D) * SD + idx % D] = ndiag[(idx / D) * SD + idx % D];
+    __syncthreads();
+  }
+  if (a.y_out && h - R >= 0 && h - R <= last) {
+    T* y = reinterpret_cast<T*>(a.y_out) + (long long)bh * D;
+    for (int d = tid; d < D; d += nt) y[d] = from_f<T>(diag[R * SD + d]);
+  }
+}
+
+inline size_t stream_smem_bytes(int D, int L, int R) {
+  const int C = R + 1, W = L + R + 1, SD = D + 1;
+  return sizeof(float) * ((size_t)W * SD + 2 * (size_t)C * SD + (size_t)C * W);
+}
+
+}  // namespace sattn

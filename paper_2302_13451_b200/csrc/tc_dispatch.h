@@ -1,0 +1,15 @@
+// tc_dispatch.h — entry points of the tcgen05 (tensor-core) kernel family (tc_sa.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "sattn.h"
+
+namespace sattn {
+struct AttnArgs;
+// true when the tensor-core kernels implement this (dtype, D, band, mode)
+bool tc_supported(int dtype, int D, int L, int R, bool llsa);
+sattn_status tc_forward(const AttnArgs& a, cudaStream_t st);
+sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
+int tc_backward_launches();
+const char* tc_last_error();
+}  // namespace sattn
