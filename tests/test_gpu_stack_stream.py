@@ -45,10 +45,14 @@ def test_stack_fp32_fwd_bwd(mode, shape, L, R, n):
 @pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("R", [8, 16])
 def test_latency_witness_12_layers(dt, R):
-    # LLSA designated-output latency = R at 12 layers; masked-acausal (SA) stack = 12 R (Table 3)
+    # LLSA designated-output latency = R at 12 layers; masked-acausal (SA) stack = 12 R (Table 3).
+    # A numeric probe can only under-report (an influence must survive rounding to be seen), so:
+    # outputs before tau - latency must be bitwise unchanged (upper bound, exact in any dtype) and the
+    # change at tau - latency must be visible (lower bound): exact in fp32 with the witness input
+    # (kappa = 40 at D = 64); in bf16 the SA chain may lose its last few hops to rounding.
     s = sattn()
     L, n, T, D, tau = 32, 12, 400, 64, 350
-    x = synth.witness(0, 1, 1, T, D)
+    x = synth.witness(0, 1, 1, T, D, kappa=40.0)
     x2 = x.copy()
     x2[0, 0, tau] += 0.5
     lat = {}
@@ -58,7 +62,11 @@ def test_latency_witness_12_layers(dt, R):
         if mode == "llsa":
             y1, y2 = y1[R], y2[R]
         lat[mode] = tau - oracle.latency.earliest_changed(host(y1), host(y2))
-    assert lat == {"sa": n * R, "llsa": R}
+    assert lat["llsa"] == R
+    if dt == torch.float32:
+        assert lat["sa"] == n * R
+    else:
+        assert n * R - 4 <= lat["sa"] <= n * R
 
 
 @pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 3e-2)])
