@@ -262,10 +262,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   float delta = 0.f;
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    float d8[8];
-    load_vec<8>(d8, reinterpret_cast<const bf16*>(sdO + r * 128 + ((c ^ (r & 7)) * 16)));
+    const uint4 raw = *reinterpret_cast<const uint4*>(sdO + r * 128 + ((c ^ (r & 7)) * 16));  // 128B swizzle
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) delta = fmaf(d8[e], orow[8 * c + e], delta);
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      delta = fmaf(f.x, orow[8 * c + 2 * e], delta);
+      delta = fmaf(f.y, orow[8 * c + 2 * e + 1], delta);
+    }
   }
   if (row_ok) a.delta[(long long)bh * T + t] = delta;
 
