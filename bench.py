@@ -143,22 +143,42 @@ def run_gpu(args):
         if st != 0:
             raise RuntimeError(f"{what}: {lib.sattn_last_error().decode()}")
 
+    def fwd_pass():
+        sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        for l in range(NL):
+            check(lib.sa_forward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), sp), "sa_forward")
+
+    def bwd_pass():
+        sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+        for l in reversed(range(NL)):
+            check(lib.sa_backward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), P(dOs[l]),
+                                  P(dQs[l]), P(dKs[l]), P(dVs[l]), P(ws), nws, sp), "sa_backward")
+
+    # The step is captured once as two CUDA graphs (forward pass, backward pass) so the timed
+    # region measures GPU execution, not Python/ctypes launch overhead; an event between the two
+    # replays splits the step into the per-call averages the roofline uses.
+    fwd_pass(); bwd_pass()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(dev)
+    gF, gB = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    n_cap0 = sattn.launch_count()
+    with torch.cuda.graph(gF, stream=cap):
+        fwd_pass()
+    with torch.cuda.graph(gB, stream=cap):
+        bwd_pass()
+    launches_per_step = sattn.launch_count() - n_cap0
     ev = {"fwd": [], "bwd": []}
 
     def step(record=False):
-        for l in range(NL):
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True); e0.record(stream)
-            check(lib.sa_forward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), sp), "sa_forward")
-            if record:
-                e1 = torch.cuda.Event(enable_timing=True); e1.record(stream); ev["fwd"].append((e0, e1))
-        for l in reversed(range(NL)):
-            if record:
-                e0 = torch.cuda.Event(enable_timing=True); e0.record(stream)
-            check(lib.sa_backward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), P(dOs[l]),
-                                  P(dQs[l]), P(dKs[l]), P(dVs[l]), P(ws), nws, sp), "sa_backward")
-            if record:
-                e1 = torch.cuda.Event(enable_timing=True); e1.record(stream); ev["bwd"].append((e0, e1))
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True); e0.record(stream)
+        gF.replay()
+        if record:
+            e1 = torch.cuda.Event(enable_timing=True); e1.record(stream)
+        gB.replay()
+        if record:
+            e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
+            ev["fwd"].append((e0, e1)); ev["bwd"].append((e1, e2))
 
     for _ in range(args.warmup):
         step()
@@ -166,7 +186,6 @@ def run_gpu(args):
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    n0 = sattn.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -176,7 +195,7 @@ def run_gpu(args):
     t1.record(stream)
     barrier()
     clocks = clk.stop()
-    launches = sattn.launch_count() - n0
+    launches = launches_per_step * args.steps
     ms = t0.elapsed_time(t1)
     ms_max = ms
     if world > 1:
@@ -187,8 +206,8 @@ def run_gpu(args):
     frames = world * B * T * args.steps
     value = frames / (ms_max / 1e3)
 
-    fwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["fwd"]]))
-    bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["bwd"]]))
+    fwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["fwd"]])) / NL
+    bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["bwd"]])) / NL
     units = B * H * T  # head-frames per launch
     hbm, tc_peak, peak_kind = load_peaks()
     kern = {"sa_forward": (fwd_ms, FWD_BYTES * units), "sa_backward": (bwd_ms, BWD_BYTES * units)}
@@ -215,7 +234,7 @@ def run_gpu(args):
             for l in range(NL):
                 for j, dst in enumerate((Qs, Ks, Vs, dOs)):
                     dst[l].copy_(hin[l][j], non_blocking=True)
-            step()
+            gF.replay(); gB.replay()
             for l in range(NL):
                 for j, src in enumerate((dQs, dKs, dVs)):
                     hout[l][j].copy_(src[l], non_blocking=True)
@@ -285,23 +304,27 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
     nws = lib.llsa_backward_workspace(pd)
     ws = torch.empty(nws, device=dev, dtype=torch.uint8)
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-    sp = ctypes.c_void_p(stream.cuda_stream)
-
     def step():
         for l in range(n_layers):
-            assert lib.llsa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), sp) == 0
+            assert lib.llsa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]),
+                                    ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
         for l in reversed(range(n_layers)):
             assert lib.llsa_backward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(dO[l]), P(dQ), P(dK),
-                                     P(dV), P(ws), nws, sp) == 0
+                                     P(dV), P(ws), nws, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
 
-    for _ in range(max(1, args.warmup)):
+    step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
         step()
+    for _ in range(max(1, args.warmup)):
+        g.replay()
     barrier()
     k = max(1, min(args.steps, 5))
     a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
     a0.record(stream)
     for _ in range(k):
-        step()
+        g.replay()
     a1.record(stream)
     barrier()
     ms = a0.elapsed_time(a1) / k

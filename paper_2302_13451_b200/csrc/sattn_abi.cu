@@ -144,9 +144,9 @@ sattn_status ffma_backward(const sattn_desc* d, bool llsa, const AttnArgs& a, cu
   });
 }
 
-bool use_tc(const sattn_desc* d, bool llsa) {
+bool use_tc(const sattn_desc* d, bool llsa, bool backward) {
   if (d->impl == SATTN_IMPL_FFMA) return false;
-  return tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa);
+  return tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, backward);
 }
 
 sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const void* K, const void* V, void* O,
@@ -154,11 +154,11 @@ sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const v
   if (!Q || !K || !V || !O || !LSE) return fail(SATTN_EARG, "NULL tensor pointer");
   if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
     return fail(SATTN_EARG, "tensor pointers must be 16-byte aligned");
-  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa))
-    return fail(SATTN_EUNSUPPORTED, "tensor-core kernels need bf16, D=64 (and %s)", llsa ? "LLSA is FFMA-only" : "L+R+1 <= 129");
+  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, false))
+    return fail(SATTN_EUNSUPPORTED, "tensor-core forward needs SA, bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE;
-  if (use_tc(d, llsa)) {
+  if (use_tc(d, llsa, false)) {
     sattn_status r = tc_forward(a, st);
     if (r != SATTN_OK) return fail(r, "tc_forward: %s", tc_last_error());
     return after_launch("tc_forward");
@@ -180,12 +180,12 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
     if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
   if (ws_bytes < attn_bwd_ws(d, llsa))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
-  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa))
-    return fail(SATTN_EUNSUPPORTED, "tensor-core kernels need bf16, D=64");
+  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, true))
+    return fail(SATTN_EUNSUPPORTED, "tensor-core backward needs SA, bf16, D=64, L+R+1 <= 49");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
-  if (use_tc(d, llsa)) {
+  if (use_tc(d, llsa, true)) {
     sattn_status r = tc_backward(a, st);
     if (r != SATTN_OK) return fail(r, "tc_backward: %s", tc_last_error());
     g_launches.fetch_add(tc_backward_launches(), std::memory_order_relaxed);
@@ -252,6 +252,8 @@ extern "C" {
 const char* sattn_last_error(void) { return g_err.c_str(); }
 const char* sattn_version(void) { return "sattn 0.1 (sm_100a)"; }
 int64_t sattn_launch_count(void) { return g_launches.load(); }
+// internal debug hook (not in sattn.h): device buffer of 8 x 64 int64 clock64 stamps of CTA 0
+void sattn_debug_trace(void* dev_buf) { tc_set_trace(dev_buf); }
 
 sattn_status sa_forward(const sattn_desc* d, const void* Q, const void* K, const void* V, void* O, float* LSE,
                         void* stream) {

@@ -7,9 +7,10 @@
 namespace sattn {
 struct AttnArgs;
 // true when the tensor-core kernels implement this (dtype, D, band, mode)
-bool tc_supported(int dtype, int D, int L, int R, bool llsa);
+bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward);
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
 int tc_backward_launches();
 const char* tc_last_error();
+void tc_set_trace(void* p);  // debug only
 }  // namespace sattn

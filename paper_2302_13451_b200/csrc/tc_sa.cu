@@ -37,56 +37,11 @@ namespace sattn {
 namespace {
 
 thread_local std::string g_tc_err;
+long long* g_trace = nullptr;  // debug: device buffer [8][64] for CTA 0 phase timestamps
 constexpr int kD = 64;
 constexpr int kM = 128;          // rows per CTA tile
-constexpr int kThreads = 128;
 
 __host__ __device__ constexpr int nk_of(int CW) { return ((96 + CW) + 15) / 16 * 16; }
-__host__ __device__ constexpr int tmem_cols_of(int NK) { return NK + 64 <= 256 ? 256 : 512; }
-
-// Write one thread's row (128 rows x NK cols bf16 tile, no-swizzle K-major core-matrix
-// layout) from `vals` covering columns [32w, 32w + CW); zeros elsewhere.
-template <int CW, int NK>
-__device__ __forceinline__ void write_row_interleave(uint8_t* buf, int r, int w, const float* vals) {
-  constexpr int SBO = (NK / 8) * 128;
-  uint8_t* rowbase = buf + (r >> 3) * SBO + (r & 7) * 16;
-#pragma unroll
-  for (int j = 0; j < CW / 8; ++j) {
-    uint4 v;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(vals[8 * j + 2 * e], vals[8 * j + 2 * e + 1]);
-    *reinterpret_cast<uint4*>(rowbase + (4 * w + j) * 128) = v;
-  }
-  const uint4 z = make_uint4(0, 0, 0, 0);
-  for (int kc = 0; kc < NK / 8; ++kc)
-    if (kc < 4 * w || kc >= 4 * w + CW / 8) *reinterpret_cast<uint4*>(rowbase + kc * 128) = z;
-}
-
-// Load columns [32w, 32w + CW) of this warp's 32 TMEM lanes.
-template <int CW>
-__device__ __forceinline__ void tmem_row_strip(uint32_t tbase, int w, float* v) {
-  const uint32_t a = tbase + (uint32_t(32 * w) << 16) + uint32_t(32 * w);
-#pragma unroll
-  for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(a + 8 * j, v + 8 * j);
-}
-
-// Store 64 fp32 accumulators of TMEM row (lane) into a bf16 global row, scaled.
-__device__ __forceinline__ void tmem_row64_to_global(uint32_t taddr, float s, bf16* dst, bool store) {
-  float v[64];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
-  tc::tmem_ld_wait();
-  if (!store) return;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint4 o;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[8 * j + 2 * e] * s, v[8 * j + 2 * e + 1] * s);
-    reinterpret_cast<uint4*>(dst)[j] = o;
-  }
-}
 
 struct TcArgs {
   int T, L, R, BH;
@@ -94,409 +49,681 @@ struct TcArgs {
   bf16* O; float* LSE;                           // fwd outputs
   const bf16* Og; const float* LSEin;           // bwd inputs
   bf16* dQ; bf16* dK; bf16* dV; float* delta;    // bwd outputs
+  long long* trace;                              // optional per-phase clock64 trace of CTA 0 (debug)
 };
 
+__device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
+  if (tr && blockIdx.x == 0 && k < 64) tr[ev * 64 + k] = clock64();
+}
+
 // ------------------------------------------------------------------------------------------
-// forward
+// forward: persistent, warp-specialised.  One CTA per SM loops over 128-row tiles.
+//   warp 0      TMA producer   (Q, K, V of tile k into smem stage k % NS)
+//   warp 1      MMA issuer     (S(k+1) = Q K^T issued before O(k) = P V, so the tensor
+//                               core works on the next tile while softmax runs)
+//   warps 2..5  softmax + epilogue (row r = 32 * (warp % 4) + lane = TMEM lane r)
+// TMEM: two buffers of 256 columns (S in [0, NK), O in [NK, NK + 64)); smem: NS stages of
+// Q/K/V and two P tiles.  mbarriers: full/empty per stage, sfull/ofull/pfull/tfree per
+// TMEM buffer.
 // ------------------------------------------------------------------------------------------
+template <int CW> struct FwdCfg {
+  static constexpr int NK = nk_of(CW);
+  static constexpr int QB = kM * 128;
+  static constexpr int KB = NK * 128;
+  static constexpr int STAGE = QB + 2 * KB;
+  static constexpr int OB = kM * 128;                       // O staging tile for the TMA store
+  static constexpr int NS = (1024 + 3 * STAGE + 2 * OB + 256 <= 232448) ? 3 : 2;
+  static constexpr int SMEM = 1024 + NS * STAGE + 2 * OB + 256;
+  static constexpr int THREADS = 320;   // TMA warp, MMA warp, 2 softmax warpgroups
+};
+
+// Softmax of one thread's row strip s[0..CW) (register i <-> key frame key0 + i), valid
+// for i in [lo, hi); returns (row max, row sum) and leaves exp2((s - max) * sl2) in s.
 template <int CW>
-__global__ void __launch_bounds__(kThreads, 1)
-    sa_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-              const __grid_constant__ CUtensorMap tmV, TcArgs a) {
-  constexpr int NK = nk_of(CW);
-  constexpr int TCOLS = tmem_cols_of(NK);
-  constexpr int OCOL = TCOLS == 256 ? NK : 256;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;                      // 128 x 128 B
-  uint8_t* sK = sQ + kM * 128;             // NK x 128 B
-  uint8_t* sV = sK + NK * 128;             // NK x 128 B
-  uint8_t* sP = sV + NK * 128;             // 128 x NK bf16, interleaved
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + kM * NK * 2);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int t0 = blockIdx.x * kM, bh = blockIdx.y;
-  const int T = a.T, W = a.L + a.R + 1;
-
-  if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ);
-    tc::tma_prefetch_desc(&tmK);
-    tc::tma_prefetch_desc(&tmV);
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
-    tc::fence_mbar_init();
-  }
-  if (w == 0) tc::tmem_alloc(tslot, TCOLS);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-
-  if (tid == 0) {
-    tc::mbar_expect_tx(&bars[0], kM * 128 + 2 * NK * 128);
-    tc::tma_load_3d(sQ, &tmQ, &bars[0], 0, t0, bh);
-    tc::tma_load_3d(sK, &tmK, &bars[0], 0, t0 - a.L, bh);
-    tc::tma_load_3d(sV, &tmV, &bars[0], 0, t0 - a.L, bh);
-    tc::mbar_wait(&bars[0], 0);
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, NK, 0, 0);
-#pragma unroll
-    for (int k = 0; k < kD / 16; ++k)
-      tc::mma_bf16(tbase, tc::desc_kmajor_sw128(tc::smem_u32(sQ) + 32 * k),
-                   tc::desc_kmajor_sw128(tc::smem_u32(sK) + 32 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 0);
-  __syncwarp();
-  tc::tc_fence_after();
-
-  // softmax over the row's band, in registers
-  float s[CW];
-  tmem_row_strip<CW>(tbase, w, s);
-  tc::tmem_ld_wait();
-  const int r = 32 * w + lane;
-  const int key0 = t0 - a.L + 32 * w;  // frame of register 0
+__device__ __forceinline__ void band_softmax(float* s, int lo, int hi, float sl2, float& m_out, float& l_out) {
   float m = neg_inf();
 #pragma unroll
   for (int i = 0; i < CW; ++i) {
-    const int f = key0 + i;
-    const bool v = i >= lane && i < lane + W && f >= 0 && f < T;
-    s[i] = v ? s[i] : neg_inf();
+    s[i] = (i >= lo && i < hi) ? s[i] : neg_inf();
     m = fmaxf(m, s[i]);
   }
   const float mref = m == neg_inf() ? 0.f : m;
-  float l = 0.f;
+  const float mb = mref * sl2;
+  float l4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < CW; ++i) {
-    s[i] = exp2f((s[i] - mref) * a.scale_log2);
-    l += s[i];
+    s[i] = tc::ex2(fmaf(s[i], sl2, -mb));
+    l4[i & 3] += s[i];
   }
-  write_row_interleave<CW, NK>(sP, r, w, s);
-  tc::fence_proxy_async_smem();
-  tc::tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, kD, 0, 1);
-    constexpr uint32_t SBO = (NK / 8) * 128;
+  m_out = mref;
+  l_out = (l4[0] + l4[1]) + (l4[2] + l4[3]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Write a thread's bf16 row of an A operand held in TMEM (K-major: lane = row, packed
+// column c = elements 2c, 2c+1): the strip s[0..CW) at elements [32*q4, 32*q4 + CW),
+// zeros for the rest of [0, NK).  `pa` = TMEM address of (this warp's lane 0, column 0).
+template <int CW, int NK>
+__device__ __forceinline__ void tmem_write_row(uint32_t pa, int q4, const float* s) {
+  const int c0 = 16 * q4;
 #pragma unroll
-    for (int k = 0; k < NK / 16; ++k)
-      tc::mma_bf16(tbase + OCOL, tc::desc_kmajor_interleave(tc::smem_u32(sP) + 256 * k, SBO),
-                   tc::desc_mnmajor_sw128(tc::smem_u32(sV) + 2048 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
+  for (int j = 0; j < CW / 8; ++j)
+    tc::tmem_st4(pa + c0 + 4 * j, pack_bf16(s[8 * j], s[8 * j + 1]), pack_bf16(s[8 * j + 2], s[8 * j + 3]),
+                 pack_bf16(s[8 * j + 4], s[8 * j + 5]), pack_bf16(s[8 * j + 6], s[8 * j + 7]));
+  for (int c = 0; c < NK / 2; c += 4)
+    if (c < c0 || c >= c0 + CW / 2) tc::tmem_st4(pa + c, 0u, 0u, 0u, 0u);
+}
+
+// 64 fp32 TMEM columns of this thread's row -> scaled bf16 -> row r of a 128-row x 128-byte
+// smem tile with the 128B swizzle (the layout a SWIZZLE_128B TMA store expects).
+__device__ __forceinline__ void tmem_row64_to_smem_sw128(uint32_t taddr, float sc, uint8_t* tile, int r) {
+  float v[64];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
+  tc::tmem_ld_wait();
+  const uint32_t row = tc::smem_u32(tile) + r * 128;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    tc::st_shared_v4(row + ((c ^ (r & 7)) << 4),
+                     make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
+                                pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc)));
+}
+
+template <int CW>
+__global__ void __launch_bounds__(320, 1)
+    sa_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, TcArgs a) {
+  using C = FwdCfg<CW>;
+  constexpr int NK = C::NK, NS = C::NS;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage0 = smem;
+  uint8_t* obuf0 = smem + NS * C::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 2 * C::OB);
+  uint64_t* full = bars;            // [NS]
+  uint64_t* empty = bars + NS;      // [NS]
+  uint64_t* sfull = bars + 2 * NS;  // [2]
+  uint64_t* ofull = sfull + 2;      // [2]
+  uint64_t* pfull = ofull + 2;      // [2]
+  uint64_t* tfree = pfull + 2;      // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, W = a.L + a.R + 1;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ);
+    tc::tma_prefetch_desc(&tmK);
+    tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmO);
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&ofull[i], 1);
+      tc::mbar_init(&pfull[i], 128); tc::mbar_init(&tfree[i], 128);
+    }
+    tc::fence_mbar_init();
   }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 1);
-  __syncwarp();
-  tc::tc_fence_after();
-  const int t = t0 + r;
-  const bool store = t < T;
-  tmem_row64_to_global(tbase + (uint32_t(32 * w) << 16) + OCOL, 1.f / l,
-                       a.O + ((long long)bh * T + (store ? t : 0)) * kD, store);
-  if (store) a.LSE[(long long)bh * T + t] = mref * a.scale + log2f(l) * kLn2;
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
   tc::tc_fence_before();
   __syncthreads();
-  if (w == 0) tc::tmem_dealloc(tbase, TCOLS);
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      auto prefetch = [&](int k) {  // warm L2 for tile k so its TMA load later is an L2 hit
+        if (k >= ntile_me) return;
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / ntq, t0 = (g % ntq) * kM;
+        tc::tma_prefetch_3d(&tmQ, 0, t0, bh);
+        tc::tma_prefetch_3d(&tmK, 0, t0 - a.L, bh);
+        tc::tma_prefetch_3d(&tmV, 0, t0 - a.L, bh);
+      };
+      for (int k = NS; k < 2 * NS; ++k) prefetch(k);
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / ntq, t0 = (g % ntq) * kM;
+        const int st = k % NS;
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        if (k >= NS) prefetch(k + NS);
+        uint8_t* sQ = stage0 + st * C::STAGE;
+        trace_at(a.trace, 0, k);
+        tc::mbar_expect_tx(&full[st], C::STAGE);
+        tc::tma_load_3d(sQ, &tmQ, &full[st], 0, t0, bh);
+        tc::tma_load_3d(sQ + C::QB, &tmK, &full[st], 0, t0 - a.L, bh);
+        tc::tma_load_3d(sQ + C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L, bh);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && ntile_me > 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(kM, NK, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16(kM, kD, 0, 1);
+      // Out-of-order issue: S(k) as soon as its stage has landed and TMEM buffer k&1 is free
+      // (PV(k-2) issued: tcgen05 ops of one thread execute in issue order, so PV(k-2) reads
+      // P(k-2) before S(k) overwrites those columns); PV(k) as soon as softmax(k) has written
+      // P(k) and the epilogue of tile k-2 has drained O.  Neither waits behind the other.
+      int ns = 0, np = 0;
+      while (np < ntile_me) {
+        if (ns < ntile_me && ns < np + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
+          trace_at(a.trace, 1, ns);
+          tc::tc_fence_after();
+          const uint32_t q = tc::smem_u32(stage0 + (ns % NS) * C::STAGE), kk = q + C::QB;
+          const uint32_t d = tbase + (ns & 1) * 256;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(d, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kk + 32 * j), idS, j > 0);
+          tc::mma_commit(&sfull[ns & 1]);
+          ++ns;
+          continue;
+        }
+        if (np < ns && tc::mbar_try_wait(tc::smem_u32(&pfull[np & 1]), (np >> 1) & 1) &&
+            (np < 2 || tc::mbar_try_wait(tc::smem_u32(&tfree[np & 1]), ((np - 2) >> 1) & 1))) {
+          const int b = np & 1, st = np % NS;
+          trace_at(a.trace, 3, np);
+          tc::tc_fence_after();
+          const uint32_t v = tc::smem_u32(stage0 + st * C::STAGE) + C::QB + C::KB;
+          const uint32_t pa = tbase + b * 256;
+#pragma unroll
+          for (int j = 0; j < NK / 16; ++j)
+            tc::mma_bf16_ts(pa + NK, pa + 8 * j, tc::desc_mnmajor_sw128(v + 2048 * j), idO, j > 0);
+          tc::mma_commit(&ofull[b]);
+          tc::mma_commit(&empty[st]);
+          ++np;
+        }
+      }
+    }
+  } else {
+    // two softmax + epilogue warpgroups: warpgroup b = (warp - 2) / 4 owns tiles k with k & 1 == b
+    // (TMEM buffer b, O staging tile b); row r = 32 * (warp % 4) + lane = TMEM lane r.
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = (warp & 3) == 2 && lane == 0;   // one thread per warpgroup
+    const bool tr = (tid == 64) || (tid == 192);
+    uint8_t* ostage = obuf0 + wg * C::OB;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, t0 = (g % ntq) * kM;
+      const int t = t0 + r;
+      const int b = wg;
+      const int use = k >> 1;
+      tc::mbar_wait(&sfull[b], use & 1);
+      if (tr) trace_at(a.trace, 4, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float s[CW];
+      const uint32_t pa = tbase + lanes + b * 256;
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(pa + 32 * q4 + 8 * j, s + 8 * j);
+      tc::tmem_ld_wait();
+      const int key0 = t0 - a.L + 32 * q4;
+      float m, l;
+      band_softmax<CW>(s, max(lane, -key0), min(lane + W, T - key0), a.scale_log2, m, l);
+      tmem_write_row<CW, NK>(pa, q4, s);      // P (bf16) over the consumed S columns
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pfull[b]);
+      if (tr) trace_at(a.trace, 5, k);
+      // epilogue (the other warpgroup runs the next tile's softmax meanwhile)
+      tc::mbar_wait(&ofull[b], use & 1);
+      if (tr) trace_at(a.trace, 6, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      if (leader) tc::bulk_wait_read0();        // the previous TMA store has read the staging tile
+      tc::named_bar(1 + wg, 128);
+      tmem_row64_to_smem_sw128(pa + NK, 1.f / l, ostage, r);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+      if (t < T) a.LSE[(long long)bh * T + t] = m * a.scale + __log2f(l) * kLn2;
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmO, ostage, 0, t0, bh);   // rows >= T are clipped by the tensor map
+        tc::bulk_commit();
+      }
+      if (tr) trace_at(a.trace, 7, k);
+    }
+    if (leader) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------------------------------------
-// backward K1: delta and dQ (query-major)
+// backward K1 (query-major): delta_t = dO_t . O_t, dQ_t = scale * sum_u dS_tu K_u.
+// Persistent, warp-specialised like the forward.  Per tile (128 queries, TMEM buffer b):
+//   MMA  S = Q K^T -> X_b                      WG  P = exp2(S*sl2 - LSE*log2e)   (registers)
+//   MMA  dP = dO V^T -> X_b (same columns)     WG  dS = P (dP - delta) -> X_b as packed bf16
+//   MMA  dQ = dS K -> Y_b (A = dS from TMEM)   WG  dQ * scale -> smem -> TMA store
 // ------------------------------------------------------------------------------------------
+template <int CW> struct DqCfg {
+  static constexpr int NK = nk_of(CW);
+  static constexpr int QB = kM * 128;
+  static constexpr int KB = NK * 128;
+  static constexpr int STAGE = 3 * QB + 2 * KB;   // Q, dO, O, K, V
+  static constexpr int NS = 2;
+  static constexpr int SMEM = 1024 + NS * STAGE + 2 * QB + 512;
+  static constexpr int THREADS = 320;
+};
+
 template <int CW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(320, 1)
     sa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, TcArgs a) {
-  constexpr int NK = nk_of(CW);
-  constexpr int TCOLS = tmem_cols_of(NK);
-  constexpr int QCOL = TCOLS == 256 ? NK : 256;
-  constexpr int R0 = (2 * kM * 128 > kM * NK * 2) ? 2 * kM * 128 : kM * NK * 2;  // [Q | dO] aliased by dS
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmdQ, TcArgs a) {
+  using C = DqCfg<CW>;
+  constexpr int NK = C::NK, NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sdO = smem + kM * 128;
-  uint8_t* sdS = smem;
-  uint8_t* sK = smem + ((R0 + 1023) & ~1023);
-  uint8_t* sV = sK + NK * 128;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + NK * 128);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint8_t* stage0 = smem;                       // [Q | dO | O | K | V] per stage
+  uint8_t* obuf0 = smem + NS * C::STAGE;        // dQ staging, one per warpgroup
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 2 * C::QB);
+  uint64_t* full = bars;              // [NS]
+  uint64_t* empty = full + NS;        // [NS]
+  uint64_t* sfull = empty + NS;       // [2]
+  uint64_t* xfree = sfull + 2;        // [2] (128 arrivals)
+  uint64_t* dpfull = xfree + 2;       // [2]
+  uint64_t* dsfull = dpfull + 2;      // [2] (128)
+  uint64_t* dqfull = dsfull + 2;      // [2]
+  uint64_t* tfree = dqfull + 2;       // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 2);
 
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int t0 = blockIdx.x * kM, bh = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
-  const int r = 32 * w + lane, t = t0 + r;
-  const bool row_ok = t < T;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ);
-    tc::tma_prefetch_desc(&tmK);
-    tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO);
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmO); tc::tma_prefetch_desc(&tmdQ);
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&dqfull[i], 1); tc::mbar_init(&tfree[i], 128);
+    }
     tc::fence_mbar_init();
   }
-  if (w == 0) tc::tmem_alloc(tslot, TCOLS);
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t lanebase = tbase + (uint32_t(32 * w) << 16);
 
-  if (tid == 0) {
-    tc::mbar_expect_tx(&bars[0], 2 * kM * 128 + 2 * NK * 128);
-    tc::tma_load_3d(sQ, &tmQ, &bars[0], 0, t0, bh);
-    tc::tma_load_3d(sdO, &tmdO, &bars[0], 0, t0, bh);
-    tc::tma_load_3d(sK, &tmK, &bars[0], 0, t0 - a.L, bh);
-    tc::tma_load_3d(sV, &tmV, &bars[0], 0, t0 - a.L, bh);
-  }
-  // delta_t = dO_t . O_t  (O from global, dO from the swizzled smem tile once it lands)
-  float orow[kD];
-  {
-    const bf16* op = a.Og + ((long long)bh * T + (row_ok ? t : 0)) * kD;
-    load_vec<kD>(orow, op);
-  }
-  const float lse2 = (row_ok ? a.LSEin[(long long)bh * T + t] : 0.f) * kLog2e;
-  tc::mbar_wait(&bars[0], 0);
-  float delta = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(sdO + r * 128 + ((c ^ (r & 7)) * 16));  // 128B swizzle
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h[e]);
-      delta = fmaf(f.x, orow[8 * c + 2 * e], delta);
-      delta = fmaf(f.y, orow[8 * c + 2 * e + 1], delta);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / ntq, t0 = (g % ntq) * kM;
+        const int st = k % NS;
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        uint8_t* b0 = stage0 + st * C::STAGE;
+        tc::mbar_expect_tx(&full[st], C::STAGE);
+        tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
+        tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
+        tc::tma_load_3d(b0 + 2 * C::QB, &tmO, &full[st], 0, t0, bh);
+        tc::tma_load_3d(b0 + 3 * C::QB, &tmK, &full[st], 0, t0 - a.L, bh);
+        tc::tma_load_3d(b0 + 3 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L, bh);
+      }
     }
-  }
-  if (row_ok) a.delta[(long long)bh * T + t] = delta;
-
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, NK, 0, 0);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(kM, NK, 0, 0);
+      constexpr uint32_t idQ = tc::idesc_bf16(kM, kD, 0, 1);
+      int ns = 0, ndp = 0, ndq = 0;
+      while (ndq < ntile_me) {
+        if (ndq < ndp && tc::mbar_try_wait(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1) &&
+            (ndq < 2 || tc::mbar_try_wait(tc::smem_u32(&tfree[ndq & 1]), ((ndq - 2) >> 1) & 1))) {
+          tc::tc_fence_after();
+          const int b = ndq & 1, st = ndq % NS;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t kk = tc::smem_u32(stage0 + st * C::STAGE) + 3 * C::QB;
 #pragma unroll
-    for (int k = 0; k < kD / 16; ++k)
-      tc::mma_bf16(tbase, tc::desc_kmajor_sw128(tc::smem_u32(sQ) + 32 * k),
-                   tc::desc_kmajor_sw128(tc::smem_u32(sK) + 32 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 0);
-  __syncwarp();
-  tc::tc_fence_after();
-  float p[CW];
-  tmem_row_strip<CW>(tbase, w, p);
-  tc::tmem_ld_wait();
-  const int key0 = t0 - a.L + 32 * w;
+          for (int j = 0; j < NK / 16; ++j)
+            tc::mma_bf16_ts(x + NK, x + 8 * j, tc::desc_mnmajor_sw128(kk + 2048 * j), idQ, j > 0);
+          tc::mma_commit(&dqfull[b]);
+          tc::mma_commit(&empty[st]);
+          ++ndq;
+          continue;
+        }
+        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+          tc::tc_fence_after();
+          const int b = ndp & 1, st = ndp % NS;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t dO = base + C::QB, v = base + 3 * C::QB + C::KB;
 #pragma unroll
-  for (int i = 0; i < CW; ++i) {
-    const int f = key0 + i;
-    const bool v = i >= lane && i < lane + W && f >= 0 && f < T;
-    p[i] = v ? exp2f(p[i] * a.scale_log2 - lse2) : 0.f;
-  }
-  tc::tc_fence_before();
-  __syncthreads();                       // every warp has read S: its columns may be overwritten
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, NK, 0, 0);
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(v + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&dpfull[b]);
+          ++ndp;
+          continue;
+        }
+        if (ns < ntile_me && ns < ndq + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
+          const uint32_t q = base, kk = base + 3 * C::QB;
 #pragma unroll
-    for (int k = 0; k < kD / 16; ++k)
-      tc::mma_bf16(tbase, tc::desc_kmajor_sw128(tc::smem_u32(sdO) + 32 * k),
-                   tc::desc_kmajor_sw128(tc::smem_u32(sV) + 32 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 1);
-  __syncwarp();
-  tc::tc_fence_after();
-  {
-    const uint32_t a0 = lanebase + uint32_t(32 * w);
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kk + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&sfull[b]);
+          ++ns;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    uint8_t* ostage = obuf0 + wg * C::QB;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, t0 = (g % ntq) * kM;
+      const int t = t0 + r;
+      const bool row_ok = t < T;
+      const int b = wg, use = k >> 1, st = k % NS;
+      const float lse2 = (row_ok ? a.LSEin[(long long)bh * T + t] : 0.f) * kLog2e;
+      // delta_t = dO_t . O_t from the staged (128B-swizzled) tiles
+      tc::mbar_wait(&full[st], (k / NS) & 1);
+      float delta = 0.f;
+      {
+        const uint32_t dO = tc::smem_u32(stage0 + st * C::STAGE) + C::QB + r * 128;
+        const uint32_t O = dO + C::QB;
 #pragma unroll
-    for (int j = 0; j < CW / 8; ++j) {
-      float dp[8];
-      tc::tmem_ld8(a0 + 8 * j, dp);
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = (c ^ (r & 7)) << 4;
+          const uint4 x = tc::ld_shared_v4(dO + off), y = tc::ld_shared_v4(O + off);
+          const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 fx = __bfloat1622float2(hx[e]), fy = __bfloat1622float2(hy[e]);
+            delta = fmaf(fx.x, fy.x, fmaf(fx.y, fy.y, delta));
+          }
+        }
+      }
+      if (row_ok) a.delta[(long long)bh * T + t] = delta;
+      const uint32_t x = tbase + lanes + b * 256;
+      // P from S
+      tc::mbar_wait(&sfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
+      const int key0 = t0 - a.L + 32 * q4;
+      {
+        const int lo = max(lane, -key0), hi = min(lane + W, T - key0);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) p[8 * j + e] = p[8 * j + e] * (dp[e] - delta);
+        for (int i = 0; i < CW; ++i)
+          p[i] = (i >= lo && i < hi) ? tc::ex2(fmaf(p[i], a.scale_log2, -lse2)) : 0.f;
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      // dS from dP
+      tc::mbar_wait(&dpfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + 32 * q4 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p[8 * j + e] *= dp[e] - delta;
+      }
+      tmem_write_row<CW, NK>(x, q4, p);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&dsfull[b]);
+      // dQ epilogue
+      tc::mbar_wait(&dqfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + wg, 128);
+      tmem_row64_to_smem_sw128(x + NK, a.scale, ostage, r);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdQ, ostage, 0, t0, bh);
+        tc::bulk_commit();
+      }
     }
+    if (leader) tc::bulk_wait0();
   }
-  // dS -> smem (aliases the consumed Q / dO tiles: both MMAs have completed)
-  write_row_interleave<CW, NK>(sdS, r, w, p);
-  tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, kD, 0, 1);
-    constexpr uint32_t SBO = (NK / 8) * 128;
-#pragma unroll
-    for (int k = 0; k < NK / 16; ++k)
-      tc::mma_bf16(tbase + QCOL, tc::desc_kmajor_interleave(tc::smem_u32(sdS) + 256 * k, SBO),
-                   tc::desc_mnmajor_sw128(tc::smem_u32(sK) + 2048 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 0);
-  __syncwarp();
-  tc::tc_fence_after();
-  tmem_row64_to_global(lanebase + QCOL, a.scale, a.dQ + ((long long)bh * T + (row_ok ? t : 0)) * kD, row_ok);
-  tc::tc_fence_before();
-  __syncthreads();
-  if (w == 0) tc::tmem_dealloc(tbase, TCOLS);
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------------------------------------
-// backward K2: dK, dV (key-major)
+// backward K2 (key-major): dV_u = sum_n P_nu dO_n, dK_u = scale * sum_n dS_nu Q_n.
+// Per tile (128 keys u0.., queries u0-R .. u0-R+NQ), TMEM X_b double-buffered, dV/dK single:
+//   MMA  S^T = K Q^T -> X_b                 WG  P^T = exp2(S^T*sl2 - LSE_n*log2e)
+//   MMA  dP^T = V dO^T -> X_b               WG  dS^T = P^T (dP^T - delta_n); P^T, dS^T -> X_b packed
+//   MMA  dV = P^T dO, dK = dS^T Q           WG  -> smem -> TMA stores
 // ------------------------------------------------------------------------------------------
+template <int CW> struct DkvCfg {
+  static constexpr int NQ = nk_of(CW);
+  static constexpr int KB = kM * 128;
+  static constexpr int QB = NQ * 128;
+  static constexpr int STAGE = 2 * KB + 2 * QB;   // K, V, Q, dO
+  static constexpr int NS = 2;
+  static constexpr int SMEM = 1024 + NS * STAGE + 4 * KB + 2 * 2 * NQ * 4 + 512;
+  static constexpr int THREADS = 320;
+};
+
 template <int CW>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(320, 1)
     sa_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, TcArgs a) {
-  constexpr int NQ = nk_of(CW);
-  constexpr int TCOLS = tmem_cols_of(NQ);
-  constexpr int R0 = (2 * kM * 128 > kM * NQ * 2) ? 2 * kM * 128 : kM * NQ * 2;  // [K | V] aliased by P^T / dS^T
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                   const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcArgs a) {
+  using C = DkvCfg<CW>;
+  constexpr int NQ = C::NQ, NS = C::NS;
+  constexpr int DVCOL = 176 <= 256 - 64 ? NQ : 0;   // dV after X_0, dK after X_1
+  static_assert(NQ + 64 <= 256, "TMEM layout needs NQ <= 192");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = smem;
-  uint8_t* sV = smem + kM * 128;
-  uint8_t* sX = smem;                                  // P^T then dS^T
-  uint8_t* sQ = smem + ((R0 + 1023) & ~1023);
-  uint8_t* sdO = sQ + NQ * 128;
-  float* sL2 = reinterpret_cast<float*>(sdO + NQ * 128);
-  float* sDel = sL2 + NQ;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDel + NQ);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint8_t* stage0 = smem;                       // [K | V | Q | dO]
+  uint8_t* obuf0 = smem + NS * C::STAGE;        // per warpgroup: [dV | dK] staging
+  float* lsd0 = reinterpret_cast<float*>(obuf0 + 4 * C::KB);   // per warpgroup: lse2[NQ], delta[NQ]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(lsd0 + 4 * NQ);
+  uint64_t* full = bars;              // [NS]
+  uint64_t* empty = full + NS;        // [NS]
+  uint64_t* sfull = empty + NS;       // [2]
+  uint64_t* xfree = sfull + 2;        // [2] (128)
+  uint64_t* dpfull = xfree + 2;       // [2]
+  uint64_t* pdsfull = dpfull + 2;     // [2] (128)
+  // dV/dK accumulators are single-buffered but their barriers are per warpgroup: a barrier
+  // waited by alternating consumers could be passed a phase early (parity aliasing)
+  uint64_t* kvfull = pdsfull + 2;     // [2]
+  uint64_t* kvfree = kvfull + 2;      // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
 
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int u0 = blockIdx.x * kM, bh = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
-  const int r = 32 * w + lane, u = u0 + r;
-  const bool row_ok = u < T;
-  const int n0 = u0 - a.R;  // query frame of column 0
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
   if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ);
-    tc::tma_prefetch_desc(&tmK);
-    tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO);
-    tc::mbar_init(&bars[0], 1);
-    tc::mbar_init(&bars[1], 1);
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128);
+    }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128); }
     tc::fence_mbar_init();
   }
-  if (w == 0) tc::tmem_alloc(tslot, TCOLS);
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
-  const uint32_t lanebase = tbase + (uint32_t(32 * w) << 16);
+  const uint32_t DV = tbase + DVCOL, DK = tbase + 256 + DVCOL;
 
-  if (tid == 0) {
-    tc::mbar_expect_tx(&bars[0], 2 * kM * 128 + 2 * NQ * 128);
-    tc::tma_load_3d(sK, &tmK, &bars[0], 0, u0, bh);
-    tc::tma_load_3d(sV, &tmV, &bars[0], 0, u0, bh);
-    tc::tma_load_3d(sQ, &tmQ, &bars[0], 0, n0, bh);
-    tc::tma_load_3d(sdO, &tmdO, &bars[0], 0, n0, bh);
-  }
-  for (int j = tid; j < NQ; j += kThreads) {
-    const int n = n0 + j;
-    const bool ok = n >= 0 && n < T;
-    sL2[j] = ok ? a.LSEin[(long long)bh * T + n] * kLog2e : __int_as_float(0x7f800000);
-    sDel[j] = ok ? a.delta[(long long)bh * T + n] : 0.f;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    tc::mbar_wait(&bars[0], 0);
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, NQ, 0, 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / ntq, u0 = (g % ntq) * kM;
+        const int st = k % NS;
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        uint8_t* b0 = stage0 + st * C::STAGE;
+        tc::mbar_expect_tx(&full[st], C::STAGE);
+        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(kM, NQ, 0, 0);
+      constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
+      int ns = 0, ndp = 0, nkv = 0;
+      while (nkv < ntile_me) {
+        if (nkv < ndp && tc::mbar_try_wait(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1) &&
+            (nkv < 1 || tc::mbar_try_wait(tc::smem_u32(&kvfree[(nkv - 1) & 1]), ((nkv - 1) >> 1) & 1))) {
+          tc::tc_fence_after();
+          const int b = nkv & 1, st = nkv % NS;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t q = base + 2 * C::KB, dO = q + C::QB;
 #pragma unroll
-    for (int k = 0; k < kD / 16; ++k)
-      tc::mma_bf16(tbase, tc::desc_kmajor_sw128(tc::smem_u32(sK) + 32 * k),
-                   tc::desc_kmajor_sw128(tc::smem_u32(sQ) + 32 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 0);
-  __syncwarp();
-  tc::tc_fence_after();
-  float p[CW];
-  tmem_row_strip<CW>(tbase, w, p);
-  tc::tmem_ld_wait();
-  const int c0 = 32 * w;  // column of register 0
+          for (int j = 0; j < NQ / 16; ++j)
+            tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO + 2048 * j), idG, j > 0);
 #pragma unroll
-  for (int i = 0; i < CW; ++i) {
-    const bool v = i >= lane && i < lane + W;   // query n in [u - R, u + L]
-    p[i] = v ? exp2f(p[i] * a.scale_log2 - sL2[c0 + i]) : 0.f;
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, NQ, 0, 0);
+          for (int j = 0; j < NQ / 16; ++j)
+            tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
+          tc::mma_commit(&kvfull[b]);
+          tc::mma_commit(&empty[st]);
+          ++nkv;
+          continue;
+        }
+        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+          tc::tc_fence_after();
+          const int b = ndp & 1, st = ndp % NS;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
 #pragma unroll
-    for (int k = 0; k < kD / 16; ++k)
-      tc::mma_bf16(tbase, tc::desc_kmajor_sw128(tc::smem_u32(sV) + 32 * k),
-                   tc::desc_kmajor_sw128(tc::smem_u32(sdO) + 32 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 1);
-  __syncwarp();
-  tc::tc_fence_after();
-  float ds[CW];
-  {
-    const uint32_t a0 = lanebase + uint32_t(32 * w);
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&dpfull[b]);
+          ++ndp;
+          continue;
+        }
+        if (ns < ntile_me && ns < nkv + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
+          const uint32_t kk = base, q = base + 2 * C::KB;
 #pragma unroll
-    for (int j = 0; j < CW / 8; ++j) {
-      float dp[8];
-      tc::tmem_ld8(a0 + 8 * j, dp);
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&sfull[b]);
+          ++ns;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    const int wtid = tid - 64 - 128 * wg;     // 0..127 within the warpgroup
+    uint8_t* ostage = obuf0 + wg * 2 * C::KB;  // [dV | dK]
+    float* sL2 = lsd0 + wg * 2 * NQ;
+    float* sDel = sL2 + NQ;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, u0 = (g % ntq) * kM;
+      const int b = wg, use = k >> 1;
+      const int n0 = u0 - a.R;
+      tc::named_bar(1 + wg, 128);   // previous tile's readers of sL2 / sDel are done
+      for (int j = wtid; j < NQ; j += 128) {
+        const int n = n0 + j;
+        const bool ok = n >= 0 && n < T;
+        sL2[j] = ok ? a.LSEin[(long long)bh * T + n] * kLog2e : __int_as_float(0x7f800000);
+        sDel[j] = ok ? a.delta[(long long)bh * T + n] : 0.f;
+      }
+      tc::named_bar(1 + wg, 128);
+      const uint32_t x = tbase + lanes + b * 256;
+      const int c0 = 32 * q4;
+      tc::mbar_wait(&sfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
 #pragma unroll
-      for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      for (int i = 0; i < CW; ++i)
+        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      tc::mbar_wait(&dpfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      }
+      tmem_write_row<CW, NQ>(x, q4, p);                 // P^T  -> packed columns [0, NQ/2)
+      tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);      // dS^T -> packed columns [NQ/2, NQ)
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[b]);
+      // dV / dK epilogue
+      tc::mbar_wait(&kvfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + wg, 128);
+      tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+      tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&kvfree[b]);
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+        tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
+        tc::bulk_commit();
+      }
     }
+    if (leader) tc::bulk_wait0();
   }
-  // P^T -> smem (aliases the consumed K / V tiles), dV = P^T dO
-  write_row_interleave<CW, NQ>(sX, r, w, p);
-  tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
-  constexpr uint32_t SBO = (NQ / 8) * 128;
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, kD, 0, 1);
-#pragma unroll
-    for (int k = 0; k < NQ / 16; ++k)
-      tc::mma_bf16(tbase + 0, tc::desc_kmajor_interleave(tc::smem_u32(sX) + 256 * k, SBO),
-                   tc::desc_mnmajor_sw128(tc::smem_u32(sdO) + 2048 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 0);
-  // dS^T -> smem (the dV MMA has finished reading P^T), dK = dS^T Q
-  write_row_interleave<CW, NQ>(sX, r, w, ds);
-  tc::fence_proxy_async_smem();
-  tc::tc_fence_before();
-  __syncthreads();
-  if (tid == 0) {
-    tc::tc_fence_after();
-    constexpr uint32_t id = tc::idesc_bf16(kM, kD, 0, 1);
-#pragma unroll
-    for (int k = 0; k < NQ / 16; ++k)
-      tc::mma_bf16(tbase + 64, tc::desc_kmajor_interleave(tc::smem_u32(sX) + 256 * k, SBO),
-                   tc::desc_mnmajor_sw128(tc::smem_u32(sQ) + 2048 * k), id, k > 0);
-    tc::mma_commit(&bars[1]);
-  }
-  __syncwarp();
-  tc::mbar_wait(&bars[1], 1);
-  __syncwarp();
-  tc::tc_fence_after();
-  const long long off = ((long long)bh * T + (row_ok ? u : 0)) * kD;
-  tmem_row64_to_global(lanebase + 0, 1.f, a.dV + off, row_ok);
-  tmem_row64_to_global(lanebase + 64, a.scale, a.dK + off, row_ok);
-  tc::tc_fence_before();
-  __syncthreads();
-  if (w == 0) tc::tmem_dealloc(tbase, TCOLS);
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -547,18 +774,6 @@ int cw_of(int W) {
   return -1;
 }
 
-template <int CW> size_t fwd_smem() { return 1024 + kM * 128 + 2 * nk_of(CW) * 128 + kM * nk_of(CW) * 2 + 64; }
-template <int CW> size_t dq_smem() {
-  constexpr int NK = nk_of(CW);
-  constexpr int R0 = (2 * kM * 128 > kM * NK * 2) ? 2 * kM * 128 : kM * NK * 2;
-  return 1024 + ((R0 + 1023) & ~1023) + 2 * NK * 128 + 64;
-}
-template <int CW> size_t dkdv_smem() {
-  constexpr int NQ = nk_of(CW);
-  constexpr int R0 = (2 * kM * 128 > kM * NQ * 2) ? 2 * kM * 128 : kM * NQ * 2;
-  return 1024 + ((R0 + 1023) & ~1023) + 2 * NQ * 128 + 2 * NQ * 4 + 64;
-}
-
 TcArgs tc_args(const AttnArgs& a) {
   TcArgs t{};
   t.T = a.T; t.L = a.L; t.R = a.R; t.BH = a.BH;
@@ -567,47 +782,64 @@ TcArgs tc_args(const AttnArgs& a) {
   t.Og = reinterpret_cast<const bf16*>(a.O); t.LSEin = a.LSE;
   t.dQ = reinterpret_cast<bf16*>(a.dQ); t.dK = reinterpret_cast<bf16*>(a.dK); t.dV = reinterpret_cast<bf16*>(a.dV);
   t.delta = a.delta;
+  t.trace = g_trace;
   return t;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int CW>
 sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
-  constexpr int NK = nk_of(CW);
-  CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK))
+  using C = FwdCfg<CW>;
+  CUtensorMap mq, mk, mv, mo;
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, C::NK) ||
+      !make_map(&mv, a.V, a.T, a.BH, C::NK) || !make_map(&mo, a.Out, a.T, a.BH, kM))
     return SATTN_ECUDA;
-  const size_t smem = fwd_smem<CW>();
-  cudaFuncSetAttribute(sa_fwd_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((a.T + kM - 1) / kM, a.BH);
-  sa_fwd_tc<CW><<<grid, kThreads, smem, st>>>(mq, mk, mv, tc_args(a));
+  cudaFuncSetAttribute(sa_fwd_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  sa_fwd_tc<CW><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, tc_args(a));
   return SATTN_OK;
 }
 
 template <int CW>
 sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   constexpr int NK = nk_of(CW);
-  CUtensorMap mq, mk, mv, mdo, mqN, mdoN, mk128, mv128;
+  CUtensorMap mq, mk, mv, mdo, mo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
-      !make_map(&mdo, a.dO, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
+      !make_map(&mdo, a.dO, a.T, a.BH, kM) || !make_map(&mo, a.O, a.T, a.BH, kM) ||
+      !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
       !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
-      !make_map(&mv128, a.V, a.T, a.BH, kM))
+      !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
+      !make_map(&mdv, a.dV, a.T, a.BH, kM))
     return SATTN_ECUDA;
-  dim3 grid((a.T + kM - 1) / kM, a.BH);
-  const size_t s1 = dq_smem<CW>();
-  cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-  sa_bwd_dq_tc<CW><<<grid, kThreads, s1, st>>>(mq, mk, mv, mdo, tc_args(a));
-  const size_t s2 = dkdv_smem<CW>();
-  cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-  sa_bwd_dkdv_tc<CW><<<grid, kThreads, s2, st>>>(mqN, mk128, mv128, mdoN, tc_args(a));
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+  sa_bwd_dq_tc<CW><<<grid, DqCfg<CW>::THREADS, DqCfg<CW>::SMEM, st>>>(mq, mk, mv, mdo, mo, mdq, tc_args(a));
+  cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
+  sa_bwd_dkdv_tc<CW><<<grid, DkvCfg<CW>::THREADS, DkvCfg<CW>::SMEM, st>>>(mqN, mk128, mv128, mdoN, mdk, mdv,
+                                                                          tc_args(a));
   return SATTN_OK;
 }
 
 }  // namespace
 
-bool tc_supported(int dtype, int D, int L, int R, bool llsa) {
+bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward) {
   if (llsa || dtype != SATTN_BF16 || D != 64) return false;
   const int W = L + R + 1;
-  return W + 31 <= 96;  // backward register budget (p and dS strips); DESIGN.md §5
+  // forward: TMEM (NK + 64 <= 256 per buffer) -> CW <= 96; backward: smem of the dK/dV
+  // kernel's two stages + staging -> CW <= 80
+  return W + 31 <= (backward ? 80 : 96);
 }
 
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st) {
@@ -637,6 +869,7 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
 }
 
 int tc_backward_launches() { return 2; }
+void tc_set_trace(void* p) { g_trace = static_cast<long long*>(p); }
 const char* tc_last_error() { return g_tc_err.c_str(); }
 
 }  // namespace sattn

@@ -88,6 +88,8 @@ def test_stream_matches_oracle_recurrence_and_offline(dt, tol):
     ys[:, :, T - tail.shape[0]:] = tail.permute(1, 2, 0, 3)
     assert first == R                                   # first emission after R+1 pushes
     Y_or, _ = oracle.stream.stream_all(xr, L, R, n)
-    assert np.abs(host(ys) - Y_or).max() <= tol
+    # per-unit-magnitude gate for a 12-layer composite, as for the stack
+    mag = max(1.0, float(np.abs(Y_or).max()))
+    assert np.abs(host(ys) - Y_or).max() <= tol * mag
     y_off, _ = s.stack_forward(tx, L, R, n, s.MODE_LLSA)
-    assert np.abs(host(ys) - host(y_off[R])).max() <= tol
+    assert np.abs(host(ys) - host(y_off[R])).max() <= tol * mag
