@@ -69,10 +69,14 @@ def test_latency_witness_12_layers(dt, R):
         assert n * R - 4 <= lat["sa"] <= n * R
 
 
-@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 3e-2)])
-def test_stream_matches_oracle_recurrence_and_offline(dt, tol):
+@pytest.mark.parametrize("dt,tol,n", [(torch.float32, 1e-5, 12), (torch.bfloat16, 2e-2, 2), (torch.bfloat16, 2e-2, 12)])
+def test_stream_matches_oracle_recurrence_and_offline(dt, tol, n):
+    # fp32: 12 layers against the fp64 oracle recurrence.  bf16 rounds every layer's X to bf16
+    # (as the offline stack stores it) while the oracle carries fp64, so the oracle gate is applied
+    # at 2 layers; at 12 layers the stream is checked against the offline GPU stack, which rounds
+    # at the same points.
     s = sattn()
-    B, H, T, D, L, R, n = 1, 2, 200, 64, 32, 8, 12
+    B, H, T, D, L, R = 1, 2, 200, 64, 32, 8
     x = synth.normal(6, "X", (B, H, T, D))
     xr = synth.round_to(x, "f32" if dt == torch.float32 else "bf16")
     tx = dev(xr, dt)
@@ -88,8 +92,9 @@ def test_stream_matches_oracle_recurrence_and_offline(dt, tol):
     ys[:, :, T - tail.shape[0]:] = tail.permute(1, 2, 0, 3)
     assert first == R                                   # first emission after R+1 pushes
     Y_or, _ = oracle.stream.stream_all(xr, L, R, n)
-    # per-unit-magnitude gate for a 12-layer composite, as for the stack
+    # per-unit-magnitude gate for a multi-layer composite, as for the stack
     mag = max(1.0, float(np.abs(Y_or).max()))
-    assert np.abs(host(ys) - Y_or).max() <= tol * mag
+    if dt == torch.float32 or n <= 2:
+        assert np.abs(host(ys) - Y_or).max() <= tol * mag
     y_off, _ = s.stack_forward(tx, L, R, n, s.MODE_LLSA)
     assert np.abs(host(ys) - host(y_off[R])).max() <= tol * mag
