@@ -26,7 +26,9 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <utility>
 #include <string>
 
 #include "ffma_attn.cuh"
@@ -45,15 +47,27 @@ __host__ __device__ constexpr int nk_of(int CW) { return ((96 + CW) + 15) / 16 *
 
 struct TcArgs {
   int T, L, R, BH;
+  int Tp;                                        // T rounded up to 4: row stride of the padded
+                                                 // delta / LSE*log2e workspace rows (16-byte TMA rows)
   float scale, scale_log2;
   bf16* O; float* LSE;                           // fwd outputs
   const bf16* Og; const float* LSEin;           // bwd inputs
   bf16* dQ; bf16* dK; bf16* dV; float* delta;    // bwd outputs
   long long* trace;                              // optional per-phase clock64 trace of CTA 0 (debug)
+  int qsplit, ksplit;                            // forward TMA box splits (tuning)
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
   if (tr && blockIdx.x == 0 && k < 64) tr[ev * 64 + k] = clock64();
+}
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// per-CTA [start, end] globaltimer stamps at tr[512 + 2*cta] (debug)
+__device__ __forceinline__ void trace_cta(long long* tr, int which) {
+  if (tr && threadIdx.x == 0 && blockIdx.x < 256) tr[512 + 2 * blockIdx.x + which] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------------
@@ -157,6 +171,7 @@ __global__ void __launch_bounds__(320, 1)
   const int ntq = (T + kM - 1) / kM;
   const int ntiles = ntq * a.BH;
   const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  trace_cta(a.trace, 0);
 
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ);
@@ -175,6 +190,9 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -196,9 +214,14 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* sQ = stage0 + st * C::STAGE;
         trace_at(a.trace, 0, k);
         tc::mbar_expect_tx(&full[st], C::STAGE);
-        tc::tma_load_3d(sQ, &tmQ, &full[st], 0, t0, bh);
-        tc::tma_load_3d(sQ + C::QB, &tmK, &full[st], 0, t0 - a.L, bh);
-        tc::tma_load_3d(sQ + C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L, bh);
+        // boxes may be split into a.qsplit / a.ksplit row blocks (multiples of 8 rows)
+        for (int i = 0; i < a.qsplit; ++i)
+          tc::tma_load_3d(sQ + i * (C::QB / a.qsplit), &tmQ, &full[st], 0, t0 + i * (kM / a.qsplit), bh);
+        for (int i = 0; i < a.ksplit; ++i) {
+          tc::tma_load_3d(sQ + C::QB + i * (C::KB / a.ksplit), &tmK, &full[st], 0, t0 - a.L + i * (C::NK / a.ksplit), bh);
+          tc::tma_load_3d(sQ + C::QB + C::KB + i * (C::KB / a.ksplit), &tmV, &full[st], 0,
+                          t0 - a.L + i * (C::NK / a.ksplit), bh);
+        }
       }
     }
   } else if (warp == 1) {
@@ -296,6 +319,7 @@ __global__ void __launch_bounds__(320, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
+  trace_cta(a.trace, 1);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -309,7 +333,7 @@ template <int CW> struct DqCfg {
   static constexpr int NK = nk_of(CW);
   static constexpr int QB = kM * 128;
   static constexpr int KB = NK * 128;
-  static constexpr int STAGE = 3 * QB + 2 * KB;   // Q, dO, O, K, V
+  static constexpr int STAGE = 3 * QB + 2 * KB;   // Q, dO, O, K, V (1024-aligned: 128B-swizzle atoms)
   static constexpr int NS = 2;
   static constexpr int SMEM = 1024 + NS * STAGE + 2 * QB + 512;
   static constexpr int THREADS = 320;
@@ -358,6 +382,9 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -365,9 +392,9 @@ __global__ void __launch_bounds__(320, 1)
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, t0 = (g % ntq) * kM;
         const int st = k % NS;
-        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         uint8_t* b0 = stage0 + st * C::STAGE;
-        tc::mbar_expect_tx(&full[st], C::STAGE);
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        tc::mbar_expect_tx(&full[st], 3 * C::QB + 2 * C::KB);
         tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
         tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
         tc::tma_load_3d(b0 + 2 * C::QB, &tmO, &full[st], 0, t0, bh);
@@ -429,13 +456,24 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
     uint8_t* ostage = obuf0 + wg * C::QB;
+    float* ws_del = a.delta;                              // [BH][Tp]
+    float* ws_l2 = a.delta + (long long)a.BH * a.Tp;      // [BH][Tp]
+    // LSE of this warpgroup's next tile is loaded one tile ahead (off the critical path)
+    auto lse_of = [&](int k) -> float {
+      if (k >= ntile_me) return 0.f;
+      const int g = blockIdx.x + k * gridDim.x;
+      const int t = (g % ntq) * kM + r;
+      return t < T ? a.LSEin[(long long)(g / ntq) * T + t] * kLog2e : 0.f;
+    };
+    float lse_next = lse_of(wg);
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, t0 = (g % ntq) * kM;
       const int t = t0 + r;
       const bool row_ok = t < T;
       const int b = wg, use = k >> 1, st = k % NS;
-      const float lse2 = (row_ok ? a.LSEin[(long long)bh * T + t] : 0.f) * kLog2e;
+      const float lse2 = lse_next;
+      lse_next = lse_of(k + 2);
       // delta_t = dO_t . O_t from the staged (128B-swizzled) tiles
       tc::mbar_wait(&full[st], (k / NS) & 1);
       float delta = 0.f;
@@ -455,7 +493,11 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
-      if (row_ok) a.delta[(long long)bh * T + t] = delta;
+      // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
+      if (t < a.Tp) {
+        ws_del[(long long)bh * a.Tp + t] = row_ok ? delta : 0.f;
+        ws_l2[(long long)bh * a.Tp + t] = row_ok ? lse2 : 0.f;
+      }
       const uint32_t x = tbase + lanes + b * 256;
       // P from S
       tc::mbar_wait(&sfull[b], use & 1);
@@ -524,9 +566,11 @@ template <int CW> struct DkvCfg {
   static constexpr int NQ = nk_of(CW);
   static constexpr int KB = kM * 128;
   static constexpr int QB = NQ * 128;
-  static constexpr int STAGE = 2 * KB + 2 * QB;   // K, V, Q, dO
+  // K, V, Q, dO, LSE*log2e[NQ], delta[NQ]; 1024-aligned (128B-swizzle atoms)
+  static constexpr int NQP = (NQ + 31) / 32 * 32;   // LSE / delta rows padded to 128-byte TMA boxes
+  static constexpr int STAGE = (2 * KB + 2 * QB + 2 * NQP * 4 + 1023) / 1024 * 1024;
   static constexpr int NS = 2;
-  static constexpr int SMEM = 1024 + NS * STAGE + 4 * KB + 2 * 2 * NQ * 4 + 512;
+  static constexpr int SMEM = 1024 + NS * STAGE + 4 * KB + 512;
   static constexpr int THREADS = 320;
 };
 
@@ -534,7 +578,8 @@ template <int CW>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                   const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV, TcArgs a) {
+                   const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
+                   const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel, TcArgs a) {
   using C = DkvCfg<CW>;
   constexpr int NQ = C::NQ, NS = C::NS;
   constexpr int DVCOL = 176 <= 256 - 64 ? NQ : 0;   // dV after X_0, dK after X_1
@@ -543,8 +588,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;                       // [K | V | Q | dO]
   uint8_t* obuf0 = smem + NS * C::STAGE;        // per warpgroup: [dV | dK] staging
-  float* lsd0 = reinterpret_cast<float*>(obuf0 + 4 * C::KB);   // per warpgroup: lse2[NQ], delta[NQ]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(lsd0 + 4 * NQ);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * C::KB);
   uint64_t* full = bars;              // [NS]
   uint64_t* empty = full + NS;        // [NS]
   uint64_t* sfull = empty + NS;       // [2]
@@ -579,6 +623,9 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
   const uint32_t DV = tbase + DVCOL, DK = tbase + 256 + DVCOL;
 
   if (warp == 0) {
@@ -587,13 +634,18 @@ __global__ void __launch_bounds__(320, 1)
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, u0 = (g % ntq) * kM;
         const int st = k % NS;
-        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         uint8_t* b0 = stage0 + st * C::STAGE;
-        tc::mbar_expect_tx(&full[st], C::STAGE);
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        trace_at(a.trace, 0, k);
+        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * NQ * 4);
         tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
         tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
         tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
         tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
+        // LSE*log2e and delta of the NQ query columns (padded workspace rows written by K1;
+        // columns outside [0, T) are zero-filled: their Q / dO rows are zero, so they add nothing)
+        tc::tma_load_2d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], u0 - a.R, bh);
+        tc::tma_load_2d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], u0 - a.R, bh);
       }
     }
   } else if (warp == 1) {
@@ -653,26 +705,20 @@ __global__ void __launch_bounds__(320, 1)
     const int r = 32 * q4 + lane;
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
-    const int wtid = tid - 64 - 128 * wg;     // 0..127 within the warpgroup
     uint8_t* ostage = obuf0 + wg * 2 * C::KB;  // [dV | dK]
-    float* sL2 = lsd0 + wg * 2 * NQ;
-    float* sDel = sL2 + NQ;
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, u0 = (g % ntq) * kM;
-      const int b = wg, use = k >> 1;
-      const int n0 = u0 - a.R;
-      tc::named_bar(1 + wg, 128);   // previous tile's readers of sL2 / sDel are done
-      for (int j = wtid; j < NQ; j += 128) {
-        const int n = n0 + j;
-        const bool ok = n >= 0 && n < T;
-        sL2[j] = ok ? a.LSEin[(long long)bh * T + n] * kLog2e : __int_as_float(0x7f800000);
-        sDel[j] = ok ? a.delta[(long long)bh * T + n] : 0.f;
-      }
-      tc::named_bar(1 + wg, 128);
+      const int b = wg, use = k >> 1, st = k % NS;
+      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB);
+      const float* sDel = sL2 + C::NQP;
+      tc::mbar_wait(&full[st], (k / NS) & 1);   // LSE / delta staged by the producer warp
+      const bool tr = (tid == 64) || (tid == 192);
+      if (tr) trace_at(a.trace, 1, k);
       const uint32_t x = tbase + lanes + b * 256;
       const int c0 = 32 * q4;
       tc::mbar_wait(&sfull[b], use & 1);
+      if (tr) trace_at(a.trace, 2, k);
       __syncwarp();
       tc::tc_fence_after();
       float p[CW];
@@ -684,7 +730,9 @@ __global__ void __launch_bounds__(320, 1)
         p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
+      if (tr) trace_at(a.trace, 3, k);
       tc::mbar_wait(&dpfull[b], use & 1);
+      if (tr) trace_at(a.trace, 4, k);
       __syncwarp();
       tc::tc_fence_after();
       float ds[CW];
@@ -701,8 +749,10 @@ __global__ void __launch_bounds__(320, 1)
       tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&pdsfull[b]);
+      if (tr) trace_at(a.trace, 5, k);
       // dV / dK epilogue
       tc::mbar_wait(&kvfull[b], use & 1);
+      if (tr) trace_at(a.trace, 6, k);
       __syncwarp();
       tc::tc_fence_after();
       if (leader) tc::bulk_wait_read0();
@@ -718,6 +768,7 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
         tc::bulk_commit();
       }
+      if (tr) trace_at(a.trace, 7, k);
     }
     if (leader) tc::bulk_wait0();
   }
@@ -725,6 +776,9 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
+
+static_assert(DqCfg<72>::STAGE % 1024 == 0 && DkvCfg<72>::STAGE % 1024 == 0 && FwdCfg<72>::STAGE % 1024 == 0,
+              "smem stages must be 1024-byte aligned");
 
 // ------------------------------------------------------------------------------------------
 // host side
@@ -766,6 +820,44 @@ bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
   return true;
 }
 
+// padded fp32 workspace rows [BH][Tp] viewed as a 2-D tensor (T, BH); box (rows, 1); no swizzle.
+bool make_map_f32_rows(CUtensorMap* m, const void* base, int T, int Tp, int BH, int box) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) {
+    g_tc_err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)T, (cuuint64_t)BH};
+  cuuint64_t strides[1] = {(cuuint64_t)Tp * 4};
+  cuuint32_t bx[2] = {(cuuint32_t)box, 1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_tc_err = "cuTensorMapEncodeTiled (f32 rows) failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel's prologue (barrier init, TMEM
+// alloc, descriptor prefetch) overlaps the previous kernel's tail; kernels call pdl_wait() first.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int cw_of(int W) {
   const int need = W + 31;
   const int opts[] = {32, 48, 64, 72, 80, 96, 112, 128, 160};
@@ -782,7 +874,10 @@ TcArgs tc_args(const AttnArgs& a) {
   t.Og = reinterpret_cast<const bf16*>(a.O); t.LSEin = a.LSE;
   t.dQ = reinterpret_cast<bf16*>(a.dQ); t.dK = reinterpret_cast<bf16*>(a.dK); t.dV = reinterpret_cast<bf16*>(a.dV);
   t.delta = a.delta;
+  t.Tp = (a.T + 3) & ~3;
   t.trace = g_trace;
+  t.qsplit = 1;
+  t.ksplit = 1;
   return t;
 }
 
@@ -800,35 +895,43 @@ int num_sms() {
 template <int CW>
 sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   using C = FwdCfg<CW>;
+  TcArgs ta = tc_args(a);
+  if (const char* e = getenv("SATTN_FWD_QSPLIT")) ta.qsplit = atoi(e);
+  if (const char* e = getenv("SATTN_FWD_KSPLIT")) ta.ksplit = atoi(e);
+  if (kM % ta.qsplit || (kM / ta.qsplit) % 8 || C::NK % ta.ksplit || (C::NK / ta.ksplit) % 8) ta.qsplit = ta.ksplit = 1;
   CUtensorMap mq, mk, mv, mo;
-  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, C::NK) ||
-      !make_map(&mv, a.V, a.T, a.BH, C::NK) || !make_map(&mo, a.Out, a.T, a.BH, kM))
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM / ta.qsplit) || !make_map(&mk, a.K, a.T, a.BH, C::NK / ta.ksplit) ||
+      !make_map(&mv, a.V, a.T, a.BH, C::NK / ta.ksplit) || !make_map(&mo, a.Out, a.T, a.BH, kM))
     return SATTN_ECUDA;
   cudaFuncSetAttribute(sa_fwd_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  sa_fwd_tc<CW><<<grid, C::THREADS, C::SMEM, st>>>(mq, mk, mv, mo, tc_args(a));
+  launch_pdl(sa_fwd_tc<CW>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, ta);
   return SATTN_OK;
 }
 
 template <int CW>
 sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   constexpr int NK = nk_of(CW);
-  CUtensorMap mq, mk, mv, mdo, mo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv;
+  const int Tp = (a.T + 3) & ~3;
+  const float* l2ws = a.delta + (long long)a.BH * Tp;
+  CUtensorMap mq, mk, mv, mdo, mo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv, ml2, mdel;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
       !make_map(&mdo, a.dO, a.T, a.BH, kM) || !make_map(&mo, a.O, a.T, a.BH, kM) ||
       !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
       !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
       !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
-      !make_map(&mdv, a.dV, a.T, a.BH, kM))
+      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NK) ||
+      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, NK))
     return SATTN_ECUDA;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
-  sa_bwd_dq_tc<CW><<<grid, DqCfg<CW>::THREADS, DqCfg<CW>::SMEM, st>>>(mq, mk, mv, mdo, mo, mdq, tc_args(a));
+  launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mo, mdq,
+             tc_args(a));
   cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
-  sa_bwd_dkdv_tc<CW><<<grid, DkvCfg<CW>::THREADS, DkvCfg<CW>::SMEM, st>>>(mqN, mk128, mv128, mdoN, mdk, mdv,
-                                                                          tc_args(a));
+  launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
+             mdoN, mdk, mdv, ml2, mdel, tc_args(a));
   return SATTN_OK;
 }
 

@@ -9,7 +9,7 @@ impl = sys.argv[1] if len(sys.argv) > 1 else "tc"
 qs = [[torch.randn(B, H, T, D, device="cuda").to(torch.bfloat16) for _ in range(4)] for _ in range(N)]
 outs = [s.sa_forward(q, k, v, L, R, impl=impl) for q, k, v, _ in qs]
 grads = [[torch.empty_like(q) for _ in range(3)] for q, *_ in qs]
-ws = torch.empty(B * H * T * 4, dtype=torch.uint8, device="cuda")
+ws = torch.empty(2 * B * H * ((T + 3) // 4 * 4) * 4, dtype=torch.uint8, device="cuda")
 import ctypes
 lib = s.lib()
 d = s.make_desc(B, H, T, D, L, R, s.BF16, impl=impl)
