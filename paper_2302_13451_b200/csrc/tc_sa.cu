@@ -567,7 +567,9 @@ template <int CW> struct DkvCfg {
   static constexpr int KB = kM * 128;
   static constexpr int QB = NQ * 128;
   // K, V, Q, dO, LSE*log2e[NQ], delta[NQ]; 1024-aligned (128B-swizzle atoms)
-  static constexpr int NQP = (NQ + 31) / 32 * 32;   // LSE / delta rows padded to 128-byte TMA boxes
+  // LSE / delta boxes start at a 16-byte-aligned frame (u0 - R rounded down to a multiple of 4)
+  // and are padded to 128 bytes: NQ + 3 frames at most are needed
+  static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
   static constexpr int STAGE = (2 * KB + 2 * QB + 2 * NQP * 4 + 1023) / 1024 * 1024;
   static constexpr int NS = 2;
   static constexpr int SMEM = 1024 + NS * STAGE + 4 * KB + 512;
@@ -637,15 +639,16 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* b0 = stage0 + st * C::STAGE;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         trace_at(a.trace, 0, k);
-        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * NQ * 4);
+        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
         tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
         tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
         tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
         tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
         // LSE*log2e and delta of the NQ query columns (padded workspace rows written by K1;
         // columns outside [0, T) are zero-filled: their Q / dO rows are zero, so they add nothing)
-        tc::tma_load_2d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], u0 - a.R, bh);
-        tc::tma_load_2d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], u0 - a.R, bh);
+        const int na = (u0 - a.R) & ~3;   // floor to a multiple of 4 (also for negatives)
+        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], na, bh, 0);
+        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], na, bh, 0);
       }
     }
   } else if (warp == 1) {
@@ -710,7 +713,8 @@ __global__ void __launch_bounds__(320, 1)
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, u0 = (g % ntq) * kM;
       const int b = wg, use = k >> 1, st = k % NS;
-      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB);
+      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);   // column 0 sits `sh` floats into the aligned box
+      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB) + sh;
       const float* sDel = sL2 + C::NQP;
       tc::mbar_wait(&full[st], (k / NS) & 1);   // LSE / delta staged by the producer warp
       const bool tr = (tid == 64) || (tid == 192);
@@ -827,12 +831,13 @@ bool make_map_f32_rows(CUtensorMap* m, const void* base, int T, int Tp, int BH, 
     g_tc_err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)T, (cuuint64_t)BH};
-  cuuint64_t strides[1] = {(cuuint64_t)Tp * 4};
-  cuuint32_t bx[2] = {(cuuint32_t)box, 1};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, bx, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+  // 3-D view (T, BH, 1) so the load uses the same tensor-tile instruction form as the bf16 tiles
+  cuuint64_t dims[3] = {(cuuint64_t)T, (cuuint64_t)BH, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)Tp * 4, (cuuint64_t)Tp * 4 * BH};
+  cuuint32_t bx[3] = {(cuuint32_t)box, 1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, bx, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled (f32 rows) failed (" + std::to_string((int)r) + ")";
@@ -921,17 +926,23 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
       !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
       !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
       !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
-      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NK) ||
-      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, NK))
+      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, DkvCfg<CW>::NQP) ||
+      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, DkvCfg<CW>::NQP))
     return SATTN_ECUDA;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const char* only = getenv("SATTN_BWD_ONLY");  // debug: run only K1 ("1") or only K2 ("2")
+  if (!only || only[0] != '2') {
   cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
   launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mo, mdq,
              tc_args(a));
+  }
+  if (!only || only[0] != '1')
+  {
   cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
   launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
              mdoN, mdk, mdv, ml2, mdel, tc_args(a));
+  }
   return SATTN_OK;
 }
 
