@@ -1,0 +1,122 @@
+"""Time sharding of SA over ranks: the hour-long-stream partition.
+
+Rank r of P owns frames [t0, t1) of every (b, h) (contiguous, rank order; see
+shard_bounds).  Eq. 4's window makes output t depend on keys/values in
+[t-L, t+R] only, and Eq. 7/13's gathers make dK_u, dV_u depend on queries in
+[u-R, u+L] only (reading G3), so one exchange of boundary frames with the two
+neighbours per call is exact:
+
+    forward   K, V (and Q, to keep tile alignment) halo: L frames from the left
+              neighbour, R frames from the right
+    backward  Q, K, V, O, dO, LSE halo of max(L, R) frames on both sides
+              (halo queries carry their true LSE and O, so P and delta are exact)
+
+The exchange is point-to-point (torch.distributed batch_isend_irecv: NCCL over
+NVLink between GPUs, gloo on CPU for the tests).  The attention runs on the
+halo-extended local slab through the C ABI and only the local rows are kept.
+Halo widths are rounded up to `align` frames (default 128 = the tensor-core tile)
+when every shard is long enough, so each local frame sits at the same tile offset
+as in the unsharded call: with deterministic kernels the sharded result is then
+bitwise equal to the unsharded one.  `attn_fwd` / `attn_bwd` default to the CUDA
+path; tests inject the CPU oracle to check the host-side exchange on gloo.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(T: int, world: int, rank: int, align: int = 1):
+    """[t0, t1) of `rank`: `align`-frame units split as evenly as possible."""
+    units = -(-T // align)
+    u0 = units * rank // world
+    u1 = units * (rank + 1) // world
+    return min(T, u0 * align), min(T, u1 * align)
+
+
+def _round_up(x: int, a: int) -> int:
+    return -(-x // a) * a
+
+
+def _peer(group, r):
+    return dist.get_global_rank(group, r) if group is not None else r
+
+
+def exchange_halo(x: torch.Tensor, left: int, right: int, group=None):
+    """Extend the local slab x[..., T_loc, D] with `left` frames from rank-1 and `right`
+    frames from rank+1 (none at the global edges).  Every rank must pass the same
+    (left, right) and hold at least max(left, right) frames.
+    Returns (x_ext, number of frames prepended)."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    T_loc = x.shape[-2]
+    ops, recv_l, recv_r = [], None, None
+    if rank > 0 and (left or right):
+        if left:
+            recv_l = torch.empty(x.shape[:-2] + (left, x.shape[-1]), dtype=x.dtype, device=x.device)
+            ops.append(dist.P2POp(dist.irecv, recv_l, _peer(group, rank - 1), group))
+        if right:
+            ops.append(dist.P2POp(dist.isend, x[..., :right, :].contiguous(), _peer(group, rank - 1), group))
+    if rank < world - 1 and (left or right):
+        if left:
+            ops.append(dist.P2POp(dist.isend, x[..., T_loc - left:, :].contiguous(), _peer(group, rank + 1), group))
+        if right:
+            recv_r = torch.empty(x.shape[:-2] + (right, x.shape[-1]), dtype=x.dtype, device=x.device)
+            ops.append(dist.P2POp(dist.irecv, recv_r, _peer(group, rank + 1), group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    parts = [p for p in (recv_l, x, recv_r) if p is not None]
+    return torch.cat(parts, dim=-2), (left if recv_l is not None else 0)
+
+
+def _halo(width: int, align: int, T_loc: int, group) -> int:
+    """`width` rounded up to `align` if every shard can supply it (agreed across ranks)."""
+    t = torch.tensor([T_loc], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    min_T = int(t.item())
+    if width > min_T:
+        raise ValueError(f"shards of {min_T} frames cannot supply a {width}-frame halo: use fewer ranks")
+    r = _round_up(width, align) if width else 0
+    return r if r <= min_T else width
+
+
+def _default_fwd(q, k, v, L, R):
+    import paper_2302_13451_b200 as s
+    return s.sa_forward(q, k, v, L, R)
+
+
+def _default_bwd(q, k, v, o, lse, do, L, R):
+    import paper_2302_13451_b200 as s
+    return s.sa_backward(q, k, v, o, lse, do, L, R)
+
+
+def sa_forward_tsharded(q, k, v, L: int, R: int, group=None, align: int = 128, attn_fwd=None):
+    """q, k, v: this rank's slabs [B, H, T_loc, D].  Returns the local (o, lse): the rows
+    [t0, t1) of the unsharded sa_forward."""
+    attn_fwd = attn_fwd or _default_fwd
+    T_loc = q.shape[-2]
+    hl, hr = _halo(L, align, T_loc, group), _halo(R, align, T_loc, group)
+    q_e, nl = exchange_halo(q, hl, hr, group)
+    k_e, _ = exchange_halo(k, hl, hr, group)
+    v_e, _ = exchange_halo(v, hl, hr, group)
+    o, lse = attn_fwd(q_e, k_e, v_e, L, R)
+    return o[..., nl:nl + T_loc, :].contiguous(), lse[..., nl:nl + T_loc].contiguous()
+
+
+def sa_backward_tsharded(q, k, v, o, lse, do, L: int, R: int, group=None, align: int = 128, attn_bwd=None):
+    """Local (dq, dk, dv) [B, H, T_loc, D]: the rows [t0, t1) of the unsharded sa_backward.
+    o, lse are this rank's rows of the forward."""
+    attn_bwd = attn_bwd or _default_bwd
+    T_loc = q.shape[-2]
+    h = _halo(max(L, R), align, T_loc, group)
+    q_e, nl = exchange_halo(q, h, h, group)
+    k_e, _ = exchange_halo(k, h, h, group)
+    v_e, _ = exchange_halo(v, h, h, group)
+    o_e, _ = exchange_halo(o, h, h, group)
+    do_e, _ = exchange_halo(do, h, h, group)
+    lse_e, _ = exchange_halo(lse.unsqueeze(-1).contiguous(), h, h, group)
+    dq, dk, dv = attn_bwd(q_e, k_e, v_e, o_e, lse_e.squeeze(-1).contiguous(), do_e, L, R)
+    sl = slice(nl, nl + T_loc)
+    return dq[..., sl, :].contiguous(), dk[..., sl, :].contiguous(), dv[..., sl, :].contiguous()
