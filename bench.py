@@ -265,6 +265,10 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
 
+    stream_lat = None
+    if not args.no_stream:
+        stream_lat = run_stream(sattn, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_seconds)
@@ -282,6 +286,7 @@ def run_gpu(args):
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
            "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa,
+           "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
 
@@ -332,6 +337,62 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
     return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
             "channels": C, "hbm_frac": round(bytes_step / (ms / 1e3) / 1e9 / hbm, 4), "steps": k,
             "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
+
+
+def run_stream(sattn, dev, n_steps=2000, warm=200):
+    """Incremental LLSA inference (infer_llsa): per-frame step latency, 12 layers,
+    H=12, D=64, (L,R)=(32,8), bf16, one kernel launch per frame for all layers.
+    device = CUDA-event time of the step; host = ABI call + synchronize round trip."""
+    import torch
+    res = {}
+    for nb in (1, 64):
+        st = sattn.LLSAStream(nb, H, D, L, R, NL, dtype=torch.bfloat16, device=dev)
+        xs = torch.randn(warm + n_steps, nb, H, D, device=dev).to(torch.bfloat16)
+        y = torch.empty(nb, H, D, device=dev, dtype=torch.bfloat16)
+        for i in range(warm):
+            st.step_into(xs[i], y)
+        torch.cuda.synchronize()
+        dev_us, host_us = [], []
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_steps)]
+        for i in range(n_steps):
+            t0 = time.perf_counter()
+            ev[i][0].record()
+            st.step_into(xs[warm + i], y)
+            ev[i][1].record()
+            torch.cuda.synchronize()
+            host_us.append((time.perf_counter() - t0) * 1e6)
+        dev_us = [a.elapsed_time(b) * 1e3 for a, b in ev]
+        res[f"B{nb}"] = {"device_p50_us": round(float(np.percentile(dev_us, 50)), 2),
+                         "device_p99_us": round(float(np.percentile(dev_us, 99)), 2),
+                         "host_p50_us": round(float(np.percentile(host_us, 50)), 2),
+                         "host_p99_us": round(float(np.percentile(host_us, 99)), 2),
+                         "streams": nb, "steps": n_steps}
+        del st
+    res["config"] = f"{NL} layers, H={H}, D={D}, (L,R)=({L},{R}), bf16, one launch per frame"
+    return res
+
+
+def latency_check(sattn, dev):
+    """Numeric witness probe: a 12-layer LLSA stack's designated output
+    depends on frames <= t + R only; the masked-acausal (SA) stack's on frames <= t + 12 R."""
+    import torch
+    import synth
+    T_, D_, tau = 400, 64, 350
+    x = synth.witness(0, 1, 1, T_, D_, kappa=40.0)
+    x2 = x.copy()
+    x2[0, 0, tau] += 0.5
+    out = {}
+    for mode, m in (("sa", sattn.MODE_SA), ("llsa", sattn.MODE_LLSA)):
+        ys = []
+        for xx in (x, x2):
+            y, _ = sattn.stack_forward(torch.tensor(xx, dtype=torch.float32, device=dev), L, R, NL, m)
+            ys.append((y[R] if mode == "llsa" else y).double().cpu().numpy())
+        d = np.abs(ys[1] - ys[0])[0, 0].max(-1)
+        out[f"{mode}_frames"] = int(tau - np.nonzero(d > 0)[0][0])
+    out["sa_seconds"] = round(out["sa_frames"] * 0.02, 4)
+    out["llsa_seconds"] = round(out["llsa_frames"] * 0.02, 4)
+    out["paper"] = "Table 3 l32_r8: infer_sa 1.92 s, infer_llsa 0.16 s (P:L391, P:L396)"
+    return out
 
 
 def load_traffic(kernel, impl):
@@ -425,6 +486,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llsa", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stream", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
