@@ -15,7 +15,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
-SOURCES = ["sattn_abi.cu", "tc_sa.cu"]
+SOURCES = ["sattn_abi.cu", "tc_sa.cu", "tc_llsa.cu"]
 
 
 def _deps():

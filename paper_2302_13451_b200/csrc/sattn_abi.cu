@@ -144,9 +144,14 @@ sattn_status ffma_backward(const sattn_desc* d, bool llsa, const AttnArgs& a, cu
   });
 }
 
+bool tc_ok(const sattn_desc* d, bool llsa, bool backward) {
+  if (llsa) return !backward && tc_llsa_supported(d->dtype, (int)d->D, d->L, d->R);
+  return tc_supported(d->dtype, (int)d->D, d->L, d->R, false, backward);
+}
+
 bool use_tc(const sattn_desc* d, bool llsa, bool backward) {
   if (d->impl == SATTN_IMPL_FFMA) return false;
-  return tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, backward);
+  return tc_ok(d, llsa, backward);
 }
 
 sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const void* K, const void* V, void* O,
@@ -154,14 +159,15 @@ sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const v
   if (!Q || !K || !V || !O || !LSE) return fail(SATTN_EARG, "NULL tensor pointer");
   if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
     return fail(SATTN_EARG, "tensor pointers must be 16-byte aligned");
-  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, false))
-    return fail(SATTN_EUNSUPPORTED, "tensor-core forward needs SA, bf16, D=64, L+R+1 <= 65");
+  if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, false))
+    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA forward needs bf16, D=64, 4 <= R <= 8, L <= 32"
+                                         : "tensor-core SA forward needs bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE;
   if (use_tc(d, llsa, false)) {
-    sattn_status r = tc_forward(a, st);
-    if (r != SATTN_OK) return fail(r, "tc_forward: %s", tc_last_error());
-    return after_launch("tc_forward");
+    sattn_status r = llsa ? tc_llsa_forward(a, st) : tc_forward(a, st);
+    if (r != SATTN_OK) return fail(r, "tc_forward: %s", llsa ? tc_llsa_last_error() : tc_last_error());
+    return after_launch(llsa ? "tc_llsa_forward" : "tc_forward");
   }
   return ffma_forward(d, llsa, a, st);
 }
@@ -182,7 +188,7 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
     if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
   if (ws_bytes < attn_bwd_ws(d, llsa))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
-  if (d->impl == SATTN_IMPL_TC && !tc_supported(d->dtype, (int)d->D, d->L, d->R, llsa, true))
+  if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true))
     return fail(SATTN_EUNSUPPORTED, "tensor-core backward needs SA, bf16, D=64, L+R+1 <= 49");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;

@@ -13,4 +13,8 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
 int tc_backward_launches();
 const char* tc_last_error();
 void tc_set_trace(void* p);  // debug only
+// tensor-core LLSA forward (tc_llsa.cu)
+bool tc_llsa_supported(int dtype, int D, int L, int R);
+sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st);
+const char* tc_llsa_last_error();
 }  // namespace sattn
