@@ -1,0 +1,214 @@
+// llsa_stair.cuh — LLSA backward, staircase part: one tiny dense attention gradient per horizon.
+//
+// The staircase slot (u, c'), c' < R, is attended by exactly the R+1 outputs of horizon
+// h = u + c' (Eq. 14, horizon form): (h - c, c), c = 0..R.  So per horizon h the staircase is
+// a dense (R+1) x R block:  S = Q_h K_h^T,  dP = dO_h V_h^T  (Q_h / dO_h: rows (h-c, c);
+// K_h / V_h: rows (h-c', c')), with P = exp(S*scale - LSE) and dS = P (dP - delta) taken from
+// the full-row LSE / delta of the query-major pass (padded workspace rows), and
+//   dQ_h += scale dS K_h         (added to the band part already in dQ)
+//   dK_h  = scale dS^T Q_h,  dV_h = P^T dO_h   (complete: no other horizon touches them)
+// Each block is computed by one warp with mma.sync m16n8k16 (bf16 -> fp32): C = R+1 <= 16 rows,
+// R <= 8 columns.  A CTA owns 16 horizons of one (b, h); the rows it needs are, per channel c,
+// the 16 frames h - c: staged with cp.async into 144-byte rows (channel tiles skewed by 16 B so
+// the ldmatrix row gathers across channels are bank-conflict free).
+#pragma once
+#include "common.cuh"
+
+namespace sattn {
+
+constexpr int kStF = 16;          // horizons per CTA
+constexpr int kStRS = 144;        // padded row stride (bytes)
+constexpr int kStTile = kStF * kStRS + 16;   // one channel's rows (+ skew)
+
+struct StairArgs {
+  const bf16 *Q, *K, *V, *dO;     // Q/K/V channel stride in_cs (0 = broadcast), dO dense
+  bf16 *dQ, *dK, *dV;             // dense [C][BH][T][64]
+  const float *del, *l2;          // padded [C][BH][Tp]
+  int T, L, R, BH, Tp;
+  long long in_cs, plane;
+  float scale, scale_log2;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+// D (16x8 fp32) += A (16x16 bf16, row) * B (16x8 bf16, col)
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ uint32_t bf2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float st_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(256, 2) llsa_bwd_stair(StairArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int R = a.R, C = R + 1, T = a.T;
+  const int h0 = blockIdx.x * kStF, bh = blockIdx.y;
+  // channel tiles: Q[C], dO[C], K[R], V[R]; then a zero row, LSE / delta, per-warp scratch
+  uint8_t* sQ = sm;
+  uint8_t* sD = sQ + C * kStTile;
+  uint8_t* sK = sD + C * kStTile;
+  uint8_t* sV = sK + R * kStTile;
+  uint8_t* zrow = sV + R * kStTile;                    // 144 zero bytes
+  float* sL = reinterpret_cast<float*>(zrow + kStRS);   // [C][16]
+  float* sE = sL + C * kStF;                            // [C][16]
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(sE + C * kStF);   // per warp: P, dS [16][16] bf16
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- stage: rows h - c of channel c for h in [h0, h0 + 16)  (zero outside [0, T))
+  const int nrows = (2 * C + 2 * R) * kStF;
+  for (int idx = tid; idx < nrows * 8; idx += blockDim.x) {
+    const int ch16 = idx & 7, r = (idx >> 3) % kStF, sl = (idx >> 3) / kStF;   // slot = tensor-channel
+    int tsr, c;
+    if (sl < C) { tsr = 0; c = sl; }
+    else if (sl < 2 * C) { tsr = 3; c = sl - C; }
+    else if (sl < 2 * C + R) { tsr = 1; c = sl - 2 * C; }
+    else { tsr = 2; c = sl - 2 * C - R; }
+    const int f = h0 + r - c;
+    const bool ok = f >= 0 && f < T;
+    const bf16* base = tsr == 0 ? a.Q : tsr == 1 ? a.K : tsr == 2 ? a.V : a.dO;
+    const long long cs = tsr == 3 ? a.plane : a.in_cs;
+    const bf16* src = base + c * cs + ((long long)bh * T + (ok ? f : 0)) * 64 + ch16 * 8;
+    uint8_t* dst = (tsr == 0 ? sQ : tsr == 1 ? sK : tsr == 2 ? sV : sD) + c * kStTile + r * kStRS + ch16 * 16;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int idx = tid; idx < C * kStF; idx += blockDim.x) {
+    const int c = idx / kStF, r = idx % kStF, f = h0 + r - c;
+    const bool ok = f >= 0 && f < T;
+    const long long o = ((long long)c * a.BH + bh) * a.Tp + f;
+    sL[idx] = ok ? a.l2[o] : 0.f;
+    sE[idx] = ok ? a.del[o] : 0.f;
+  }
+  if (tid < kStRS / 4) reinterpret_cast<uint32_t*>(zrow)[tid] = 0u;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+
+  const int g = lane >> 2, t4 = lane & 3;
+  const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(zrow);
+  uint8_t* scP = scratch + warp * 2 * 16 * 32;   // [16 rows (c)][16 cols (c')] bf16, 32-byte rows
+  uint8_t* scS = scP + 16 * 32;
+  const uint32_t scPa = (uint32_t)__cvta_generic_to_shared(scP), scSa = (uint32_t)__cvta_generic_to_shared(scS);
+  auto rowaddr = [&](const uint8_t* tile, int c, int nc, int i, int chunk) -> uint32_t {
+    return c < nc ? (uint32_t)__cvta_generic_to_shared(tile + c * kStTile + i * kStRS + chunk * 16) : zaddr;
+  };
+
+  for (int i = warp; i < kStF; i += 8) {
+    const int h = h0 + i;
+    // ---- S = Q_h K_h^T and dP = dO_h V_h^T (16 x 8 each; rows c, cols c')
+    float s[4] = {0.f, 0.f, 0.f, 0.f}, dp[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      // A rows m = lane & 15, 16-byte chunk 2 kk + (lane >> 4); B rows n = lane & 7, chunk 2 kk + ((lane >> 3) & 1)
+      const int am = lane & 15, ach = 2 * kk + (lane >> 4);
+      const int bn = lane & 7, bch = 2 * kk + ((lane >> 3) & 1);
+      uint32_t aq[4], ad[4], bk[2], bv[2];
+      ldsm_x4(rowaddr(sQ, am, C, i, ach), aq);
+      ldsm_x4(rowaddr(sD, am, C, i, ach), ad);
+      ldsm_x2(rowaddr(sK, bn, R, i, bch), bk);
+      ldsm_x2(rowaddr(sV, bn, R, i, bch), bv);
+      mma16816(s, aq, bk);
+      mma16816(dp, ad, bv);
+    }
+    // ---- P, dS (this lane: rows c = g, g + 8; cols c' = 2 t4, 2 t4 + 1)
+    float p[4], ds[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int c = g + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
+      const bool ok = c < C && cp < R && h - c >= 0 && h - c < T && h - cp >= 0 && h - cp < T;
+      const int cc = c < C ? c : 0;
+      p[e] = ok ? st_ex2(s[e] * a.scale_log2 - sL[cc * kStF + i]) : 0.f;
+      ds[e] = p[e] * (dp[e] - sE[cc * kStF + i]);
+    }
+    // scratch copies (rows c, cols c' < 8; cols 8..15 stay zero) for the transposed products
+    *reinterpret_cast<uint32_t*>(scP + g * 32 + 4 * t4) = bf2(p[0], p[1]);
+    *reinterpret_cast<uint32_t*>(scP + (g + 8) * 32 + 4 * t4) = bf2(p[2], p[3]);
+    *reinterpret_cast<uint32_t*>(scS + g * 32 + 4 * t4) = bf2(ds[0], ds[1]);
+    *reinterpret_cast<uint32_t*>(scS + (g + 8) * 32 + 4 * t4) = bf2(ds[2], ds[3]);
+    *reinterpret_cast<uint32_t*>(scP + g * 32 + 16 + 4 * t4) = 0u;
+    *reinterpret_cast<uint32_t*>(scP + (g + 8) * 32 + 16 + 4 * t4) = 0u;
+    *reinterpret_cast<uint32_t*>(scS + g * 32 + 16 + 4 * t4) = 0u;
+    *reinterpret_cast<uint32_t*>(scS + (g + 8) * 32 + 16 + 4 * t4) = 0u;
+    __syncwarp();
+    // ---- dQ_h (16 x 64) = dS (A from the accumulator layout, k = c' < 8) x K_h (rows c')
+    {
+      const uint32_t adq[4] = {bf2(ds[0], ds[1]), bf2(ds[2], ds[3]), 0u, 0u};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t b[2];
+        // B = K_h [k = c'][n = d]: rows k = lane & 15 (>= R -> zero row), 16-byte chunk j
+        ldsm_x2_t(rowaddr(sK, lane & 15, R, i, j), b);
+        mma16816(acc, adq, b);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c = g + 8 * hh, t = h - c;
+          if (c < C && t >= 0 && t < T) {
+            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.dQ + c * a.plane + ((long long)bh * T + t) * 64 +
+                                                                    8 * j + 2 * t4);
+            const float2 cur = __bfloat1622float2(*dst);
+            *dst = __floats2bfloat162_rn(fmaf(acc[2 * hh], a.scale, cur.x), fmaf(acc[2 * hh + 1], a.scale, cur.y));
+          }
+        }
+      }
+    }
+    // ---- dV_h = P^T dO_h and dK_h = scale dS^T Q_h (16 x 64; rows c', k = c)
+    {
+      uint32_t ap[4], as[4];
+      // A = P^T [m = c'][k = c] from the [c][c'] scratch: matrix j = rows c 8(j >> 1).., cols c' 8(j & 1)..
+      const int jm = lane >> 3, rr = lane & 7;
+      ldsm_x4_t(scPa + (8 * (jm >> 1) + rr) * 32 + 16 * (jm & 1), ap);
+      ldsm_x4_t(scSa + (8 * (jm >> 1) + rr) * 32 + 16 * (jm & 1), as);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float dv[4] = {0.f, 0.f, 0.f, 0.f}, dk[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t bd[2], bq[2];
+        ldsm_x2_t(rowaddr(sD, lane & 15, C, i, j), bd);   // B = dO_h [k = c][n = d]
+        ldsm_x2_t(rowaddr(sQ, lane & 15, C, i, j), bq);   // B = Q_h  [k = c][n = d]
+        mma16816(dv, ap, bd);
+        mma16816(dk, as, bq);
+        const int cp = g;                                 // rows c' = g (rows g + 8 are padding)
+        const int u = h - cp;
+        if (cp < R && u >= 0 && u < T) {
+          const long long off = cp * a.plane + ((long long)bh * T + u) * 64 + 8 * j + 2 * t4;
+          *reinterpret_cast<__nv_bfloat162*>(a.dV + off) = __floats2bfloat162_rn(dv[0], dv[1]);
+          *reinterpret_cast<__nv_bfloat162*>(a.dK + off) =
+              __floats2bfloat162_rn(dk[0] * a.scale, dk[1] * a.scale);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+inline size_t stair_smem_bytes(int R) {
+  const int C = R + 1;
+  return (size_t)(2 * C + 2 * R) * kStTile + kStRS + 2 * (size_t)C * kStF * sizeof(float) + 8 * 2 * 16 * 32;
+}
+
+}  // namespace sattn

@@ -145,7 +145,9 @@ sattn_status ffma_backward(const sattn_desc* d, bool llsa, const AttnArgs& a, cu
 }
 
 bool tc_ok(const sattn_desc* d, bool llsa, bool backward) {
-  if (llsa) return !backward && tc_llsa_supported(d->dtype, (int)d->D, d->L, d->R);
+  if (llsa)
+    return backward ? tc_llsa_bwd_supported(d->dtype, (int)d->D, d->L, d->R)
+                    : tc_llsa_supported(d->dtype, (int)d->D, d->L, d->R);
   return tc_supported(d->dtype, (int)d->D, d->L, d->R, false, backward);
 }
 
@@ -189,14 +191,15 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
   if (ws_bytes < attn_bwd_ws(d, llsa))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
   if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true))
-    return fail(SATTN_EUNSUPPORTED, "tensor-core backward needs SA, bf16, D=64, L+R+1 <= 49");
+    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA backward needs bf16, D=64, 1 <= R <= 8, L <= 48"
+                                         : "tensor-core SA backward needs bf16, D=64, L+R+1 <= 49");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
   if (use_tc(d, llsa, true)) {
-    sattn_status r = tc_backward(a, st);
+    sattn_status r = llsa ? tc_llsa_backward(a, st) : tc_backward(a, st);
     if (r != SATTN_OK) return fail(r, "tc_backward: %s", tc_last_error());
-    g_launches.fetch_add(tc_backward_launches(), std::memory_order_relaxed);
+    g_launches.fetch_add(llsa ? tc_llsa_backward_launches(d->R) : tc_backward_launches(), std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_backward launch: %s", cudaGetErrorString(e));
     return SATTN_OK;

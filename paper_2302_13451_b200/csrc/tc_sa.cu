@@ -32,6 +32,7 @@
 #include <string>
 
 #include "ffma_attn.cuh"
+#include "llsa_stair.cuh"
 #include "tc_dispatch.h"
 #include "tc_ptx.cuh"
 
@@ -55,6 +56,9 @@ struct TcArgs {
   bf16* dQ; bf16* dK; bf16* dV; float* delta;    // bwd outputs
   long long* trace;                              // optional per-phase clock64 trace of CTA 0 (debug)
   int qsplit, ksplit;                            // forward TMA box splits (tuning)
+  int kshift;                                    // keys of query t are frames [t-L-kshift, t+R-kshift]
+                                                 // (0 for SA; R-c for LLSA channel c's band, with R := 0)
+  float* ws_del; float* ws_l2;                   // padded [BH][Tp] delta / LSE*log2e rows (K1 -> K2)
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
@@ -398,8 +402,8 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
         tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
         tc::tma_load_3d(b0 + 2 * C::QB, &tmO, &full[st], 0, t0, bh);
-        tc::tma_load_3d(b0 + 3 * C::QB, &tmK, &full[st], 0, t0 - a.L, bh);
-        tc::tma_load_3d(b0 + 3 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L, bh);
+        tc::tma_load_3d(b0 + 3 * C::QB, &tmK, &full[st], 0, t0 - a.L - a.kshift, bh);
+        tc::tma_load_3d(b0 + 3 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - a.kshift, bh);
       }
     }
   } else if (warp == 1) {
@@ -456,8 +460,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
     uint8_t* ostage = obuf0 + wg * C::QB;
-    float* ws_del = a.delta;                              // [BH][Tp]
-    float* ws_l2 = a.delta + (long long)a.BH * a.Tp;      // [BH][Tp]
+    float* ws_del = a.ws_del;                             // [BH][Tp]
+    float* ws_l2 = a.ws_l2;                               // [BH][Tp]
     // LSE of this warpgroup's next tile is loaded one tile ahead (off the critical path)
     auto lse_of = [&](int k) -> float {
       if (k >= ntile_me) return 0.f;
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
-      const int key0 = t0 - a.L + 32 * q4;
+      const int key0 = t0 - a.L - a.kshift + 32 * q4;
       {
         const int lo = max(lane, -key0), hi = min(lane + W, T - key0);
 #pragma unroll
@@ -781,6 +785,244 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
+// ------------------------------------------------------------------------------------------
+// LLSA backward, band keys (channel R), key-major: for a tile of 128 channel-R keys u, every
+// query channel c = 0..R contributes through the band: query (t, c) sees (u, R) iff
+// u in [t + c - R - L, t + c - R]  <=>  t in [u + s_c, u + s_c + L],  s_c = R - c
+// (Eq. 14 in the horizon form).  Per (tile, c) sub-item, exactly the SA key-major step with
+// the query tile shifted by s_c:
+//   S^T = K Q_c^T -> P^T (LSE of channel c);  dP^T = V dO_c^T -> dS^T (delta of channel c)
+//   dV += P^T dO_c,  dK += dS^T Q_c            accumulated in TMEM over the R+1 channels
+// Rings: K/V per key tile (2 stages), Q_c/dO_c/LSE_c/delta_c per sub-item (2 stages).
+// ------------------------------------------------------------------------------------------
+template <int CW> struct LkvCfg {
+  static constexpr int NQ = nk_of(CW);
+  static constexpr int KB = kM * 128;
+  static constexpr int QB = NQ * 128;
+  static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
+  static constexpr int KVSTAGE = 2 * KB;
+  static constexpr int QSTAGE = (2 * QB + 2 * NQP * 4 + 1023) / 1024 * 1024;
+  static constexpr int SMEM = 1024 + 2 * KVSTAGE + 2 * QSTAGE + 4 * KB + 512;
+};
+
+template <int CW>
+__global__ void __launch_bounds__(320, 1)
+    llsa_bwd_kv_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                   const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
+                   const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel, TcArgs a,
+                   int C, int bcast) {
+  using Cf = LkvCfg<CW>;
+  constexpr int NQ = Cf::NQ;
+  static_assert(NQ + 64 <= 256, "TMEM layout needs NQ <= 192");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* kv0 = smem;                                   // [K | V] x 2
+  uint8_t* qs0 = smem + 2 * Cf::KVSTAGE;                 // [Q_c | dO_c | lse2 | delta] x 2
+  uint8_t* obuf0 = qs0 + 2 * Cf::QSTAGE;                 // per warpgroup [dV | dK]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * Cf::KB);
+  uint64_t* kvfull_ld = bars;         // [2] K/V of a tile landed
+  uint64_t* kvempty = kvfull_ld + 2;  // [2] K/V stage free
+  uint64_t* qfull = kvempty + 2;      // [2]
+  uint64_t* qempty = qfull + 2;       // [2]
+  uint64_t* sfull = qempty + 2;       // [2]
+  uint64_t* xfree = sfull + 2;        // [2] (128)
+  uint64_t* dpfull = xfree + 2;       // [2]
+  uint64_t* pdsfull = dpfull + 2;     // [2] (128)
+  uint64_t* kvfull = pdsfull + 2;     // [2] dK/dV of a tile accumulated (by tile parity)
+  uint64_t* kvfree = kvfull + 2;      // [2] (128) dK/dV drained (by tile parity)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, L = a.L, R = a.R;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int nsub = ntile_me * C;
+
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&kvfull_ld[i], 1); tc::mbar_init(&kvempty[i], 1);
+      tc::mbar_init(&qfull[i], 1); tc::mbar_init(&qempty[i], 1);
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t DV = tbase + NQ, DK = tbase + 256 + NQ;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int k = 0;
+      for (int kt = 0; kt < ntile_me; ++kt) {
+        const int g = blockIdx.x + kt * gridDim.x;
+        const int bh = g / ntq, u0 = (g % ntq) * kM;
+        const int ks = kt & 1;
+        if (kt >= 2) tc::mbar_wait(&kvempty[ks], ((kt - 2) >> 1) & 1);
+        uint8_t* kvb = kv0 + ks * Cf::KVSTAGE;
+        tc::mbar_expect_tx(&kvfull_ld[ks], 2 * Cf::KB);
+        tc::tma_load_3d(kvb, &tmK, &kvfull_ld[ks], 0, u0, bh);
+        tc::tma_load_3d(kvb + Cf::KB, &tmV, &kvfull_ld[ks], 0, u0, bh);
+        for (int c = 0; c < C; ++c, ++k) {
+          const int qs = k & 1;
+          if (k >= 2) tc::mbar_wait(&qempty[qs], ((k - 2) >> 1) & 1);
+          uint8_t* qb = qs0 + qs * Cf::QSTAGE;
+          const int n0 = u0 + (R - c);                    // query frame of column 0
+          const int na = n0 & ~3;
+          tc::mbar_expect_tx(&qfull[qs], 2 * Cf::QB + 2 * Cf::NQP * 4);
+          tc::tma_load_4d(qb, &tmQ, &qfull[qs], 0, n0, bh, bcast ? 0 : c);
+          tc::tma_load_4d(qb + Cf::QB, &tmdO, &qfull[qs], 0, n0, bh, c);
+          tc::tma_load_3d(qb + 2 * Cf::QB, &tmL2, &qfull[qs], na, c * a.BH + bh, 0);
+          tc::tma_load_3d(qb + 2 * Cf::QB + Cf::NQP * 4, &tmDel, &qfull[qs], na, c * a.BH + bh, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(kM, NQ, 0, 0);
+      constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
+      int ns = 0, ndp = 0, nkv = 0;
+      while (nkv < nsub) {
+        if (nkv < ndp && tc::mbar_try_wait(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1)) {
+          const int kt = nkv / C, c = nkv % C;
+          if (c == 0 && kt >= 1 && !tc::mbar_try_wait(tc::smem_u32(&kvfree[(kt - 1) & 1]), ((kt - 1) >> 1) & 1)) {
+            // accumulators still being drained by the previous tile's epilogue
+          } else {
+            tc::tc_fence_after();
+            const int b = nkv & 1, qs = nkv & 1;
+            const uint32_t x = tbase + b * 256;
+            const uint32_t q = tc::smem_u32(qs0 + qs * Cf::QSTAGE), dO = q + Cf::QB;
+#pragma unroll
+            for (int j = 0; j < NQ / 16; ++j)
+              tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO + 2048 * j), idG, (c > 0) || (j > 0));
+#pragma unroll
+            for (int j = 0; j < NQ / 16; ++j)
+              tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, (c > 0) || (j > 0));
+            tc::mma_commit(&qempty[qs]);
+            if (c == C - 1) {
+              tc::mma_commit(&kvfull[kt & 1]);
+              tc::mma_commit(&kvempty[kt & 1]);
+            }
+            ++nkv;
+            continue;
+          }
+        }
+        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+          tc::tc_fence_after();
+          const int b = ndp & 1, kt = ndp / C;
+          const uint32_t v = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE) + Cf::KB;
+          const uint32_t dO = tc::smem_u32(qs0 + (ndp & 1) * Cf::QSTAGE) + Cf::QB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&dpfull[b]);
+          ++ndp;
+          continue;
+        }
+        if (ns < nsub && ns < nkv + 2) {
+          const int kt = ns / C;
+          if (tc::mbar_try_wait(tc::smem_u32(&kvfull_ld[kt & 1]), (kt >> 1) & 1) &&
+              tc::mbar_try_wait(tc::smem_u32(&qfull[ns & 1]), (ns >> 1) & 1)) {
+            tc::tc_fence_after();
+            const int b = ns & 1;
+            const uint32_t kk = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE);
+            const uint32_t q = tc::smem_u32(qs0 + (ns & 1) * Cf::QSTAGE);
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
+                           j > 0);
+            tc::mma_commit(&sfull[b]);
+            ++ns;
+          }
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    const int W = L + 1;
+    uint8_t* ostage = obuf0 + wg * 2 * Cf::KB;  // [dV | dK]
+    for (int k = wg; k < nsub; k += 2) {
+      const int kt = k / C, c = k % C;
+      const int g = blockIdx.x + kt * gridDim.x;
+      const int bh = g / ntq, u0 = (g % ntq) * kM;
+      const int b = k & 1, use = k >> 1, qs = k & 1;
+      const int n0 = u0 + (R - c);
+      const int sh = n0 - (n0 & ~3);
+      const float* sL2 = reinterpret_cast<const float*>(qs0 + qs * Cf::QSTAGE + 2 * Cf::QB) + sh;
+      const float* sDel = sL2 + Cf::NQP;
+      tc::mbar_wait(&qfull[qs], use & 1);
+      const uint32_t x = tbase + lanes + b * 256;
+      const int c0 = 32 * q4;
+      tc::mbar_wait(&sfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      tc::mbar_wait(&dpfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      }
+      tmem_write_row<CW, NQ>(x, q4, p);
+      tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[b]);
+      if (c == C - 1) {
+        // dV / dK of the tile (accumulated over the R+1 query channels)
+        tc::mbar_wait(&kvfull[kt & 1], (kt >> 1) & 1);
+        __syncwarp();
+        tc::tc_fence_after();
+        if (leader) tc::bulk_wait_read0();
+        tc::named_bar(1 + wg, 128);
+        tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+        tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + Cf::KB, r);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&kvfree[kt & 1]);
+        tc::fence_proxy_async_smem();
+        tc::named_bar(1 + wg, 128);
+        if (leader) {
+          tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+          tc::tma_store_3d(&tmdK, ostage + Cf::KB, 0, u0, bh);
+          tc::bulk_commit();
+        }
+      }
+    }
+    if (leader) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
 static_assert(DqCfg<72>::STAGE % 1024 == 0 && DkvCfg<72>::STAGE % 1024 == 0 && FwdCfg<72>::STAGE % 1024 == 0,
               "smem stages must be 1024-byte aligned");
 
@@ -819,6 +1061,27 @@ bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+// [C][BH][T][64] bf16 as a 4-D tensor (64, T, BH, C); box (64, rows, 1, 1), 128B swizzle.
+bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) {
+    g_tc_err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)BH, (cuuint64_t)C};
+  cuuint64_t strides[3] = {128, (cuuint64_t)T * 128, (cuuint64_t)BH * T * 128};
+  cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_tc_err = "cuTensorMapEncodeTiled (4d) failed (" + std::to_string((int)r) + ")";
     return false;
   }
   return true;
@@ -883,6 +1146,9 @@ TcArgs tc_args(const AttnArgs& a) {
   t.trace = g_trace;
   t.qsplit = 1;
   t.ksplit = 1;
+  t.kshift = 0;
+  t.ws_del = a.delta;
+  t.ws_l2 = a.delta + (long long)a.BH * t.Tp;
   return t;
 }
 
@@ -946,6 +1212,78 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   return SATTN_OK;
 }
 
+// LLSA backward: band (channel-R keys) on the tensor-core kernels, staircase on CUDA cores.
+template <int CW>
+sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
+  constexpr int NK = nk_of(CW);
+  using LC = LkvCfg<CW>;
+  const int R = a.R, C = R + 1;
+  const bool bc = a.in_cs == 0;
+  const long long plane = (long long)a.BH * a.T * kD;
+  const bf16* Q = reinterpret_cast<const bf16*>(a.Q);
+  const bf16* K = reinterpret_cast<const bf16*>(a.K);
+  const bf16* V = reinterpret_cast<const bf16*>(a.V);
+  const bf16* O = reinterpret_cast<const bf16*>(a.O);
+  const bf16* dO = reinterpret_cast<const bf16*>(a.dO);
+  bf16* dQ = reinterpret_cast<bf16*>(a.dQ);
+  bf16* dK = reinterpret_cast<bf16*>(a.dK);
+  bf16* dV = reinterpret_cast<bf16*>(a.dV);
+  const bf16* Kr = K + a.in_cs * R;
+  const bf16* Vr = V + a.in_cs * R;
+  const int Tp = (a.T + 3) & ~3;
+  float* ws_del = a.delta;                          // [C][BH][Tp]
+  float* ws_l2 = a.delta + (long long)C * a.BH * Tp;
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  // (1) query-major band pass per channel c: SA dQ kernel with R := 0 and keys shifted by R - c
+  cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+  for (int c = 0; c < C; ++c) {
+    CUtensorMap mq, mk, mv, mdo, mo, mdq;
+    if (!make_map(&mq, Q + a.in_cs * c, a.T, a.BH, kM) || !make_map(&mk, Kr, a.T, a.BH, NK) ||
+        !make_map(&mv, Vr, a.T, a.BH, NK) || !make_map(&mdo, dO + plane * c, a.T, a.BH, kM) ||
+        !make_map(&mo, O + plane * c, a.T, a.BH, kM) || !make_map(&mdq, dQ + plane * c, a.T, a.BH, kM))
+      return SATTN_ECUDA;
+    TcArgs t = tc_args(a);
+    t.R = 0;
+    t.kshift = R - c;
+    t.Og = O + plane * c;
+    t.LSEin = a.LSE + (long long)c * a.BH * a.T;
+    t.ws_del = ws_del + (long long)c * a.BH * Tp;
+    t.ws_l2 = ws_l2 + (long long)c * a.BH * Tp;
+    launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mo, mdq,
+               t);
+  }
+  // (2) key-major band pass: dK, dV of channel R accumulated over the C query channels
+  {
+    CUtensorMap mq4, mdo4, mk, mv, mdk, mdv, ml2, mdel;
+    if (!make_map4(&mq4, Q, a.T, a.BH, bc ? 1 : C, LC::NQ) || !make_map4(&mdo4, dO, a.T, a.BH, C, LC::NQ) ||
+        !make_map(&mk, Kr, a.T, a.BH, kM) || !make_map(&mv, Vr, a.T, a.BH, kM) ||
+        !make_map(&mdk, dK + plane * R, a.T, a.BH, kM) || !make_map(&mdv, dV + plane * R, a.T, a.BH, kM) ||
+        !make_map_f32_rows(&ml2, ws_l2, a.T, Tp, C * a.BH, LC::NQP) ||
+        !make_map_f32_rows(&mdel, ws_del, a.T, Tp, C * a.BH, LC::NQP))
+      return SATTN_ECUDA;
+    TcArgs t = tc_args(a);
+    cudaFuncSetAttribute(llsa_bwd_kv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, LC::SMEM);
+    launch_pdl(llsa_bwd_kv_tc<CW>, dim3(grid), dim3(320), LC::SMEM, st, mq4, mk, mv, mdo4, mdk, mdv, ml2, mdel, t, C,
+               bc ? 1 : 0);
+  }
+  // (3) staircase keys and the staircase part of dQ (CUDA cores)
+  {
+    StairArgs sa{};
+    sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
+    sa.dQ = dQ; sa.dK = dK; sa.dV = dV;
+    sa.del = ws_del; sa.l2 = ws_l2;
+    sa.T = a.T; sa.L = a.L; sa.R = R; sa.BH = a.BH; sa.Tp = Tp;
+    sa.in_cs = a.in_cs; sa.plane = plane;
+    sa.scale = a.scale; sa.scale_log2 = a.scale_log2;
+    const size_t smem = stair_smem_bytes(R);
+    cudaFuncSetAttribute(llsa_bwd_stair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // horizons run to T - 1 + R (the last staircase keys / queries of channels > 0)
+    llsa_bwd_stair<<<dim3((a.T + R + kStF - 1) / kStF, a.BH), 256, smem, st>>>(sa);
+  }
+  return SATTN_OK;
+}
+
 }  // namespace
 
 bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward) {
@@ -983,6 +1321,25 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
 }
 
 int tc_backward_launches() { return 2; }
+
+bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {
+  // band width L+1 on the SA kernels (CW <= 80), staircase staging of 16 + 2R frames x C channels
+  return dtype == SATTN_BF16 && D == 64 && R >= 1 && R <= 8 && L + 1 + 31 <= 80;
+}
+
+sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
+  switch (cw_of(a.L + 1)) {
+    case 32: return llsa_bwd_launch<32>(a, st);
+    case 48: return llsa_bwd_launch<48>(a, st);
+    case 64: return llsa_bwd_launch<64>(a, st);
+    case 72: return llsa_bwd_launch<72>(a, st);
+    case 80: return llsa_bwd_launch<80>(a, st);
+  }
+  g_tc_err = "band too wide for the LLSA tensor-core backward";
+  return SATTN_EUNSUPPORTED;
+}
+
+int tc_llsa_backward_launches(int R) { return (R + 1) + 2; }
 void tc_set_trace(void* p) { g_trace = static_cast<long long*>(p); }
 const char* tc_last_error() { return g_tc_err.c_str(); }
 

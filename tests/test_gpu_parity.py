@@ -102,6 +102,9 @@ LLSA_CASES = [
     ("f32", (1, 1, 16, 4), 3, 1), ("f32", (2, 3, 37, 4), 5, 2), ("f32", (1, 2, 300, 64), 32, 8),
     ("f32", (1, 1, 40, 8), 0, 3), ("f32", (1, 1, 9, 4), 4, 6), ("f32", (1, 2, 130, 16), 2, 0),
     ("bf16", (2, 2, 1750, 64), 32, 8), ("bf16", (1, 2, 600, 64), 32, 16),
+    # tensor-core LLSA (forward: 4 <= R <= 8, L <= 32; backward: 1 <= R <= 8) incl. ragged tails
+    ("bf16", (1, 3, 777, 64), 32, 8), ("bf16", (1, 2, 200, 64), 16, 4), ("bf16", (1, 1, 130, 64), 5, 1),
+    ("bf16", (1, 1, 96, 64), 16, 6),
 ]
 
 
