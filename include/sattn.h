@@ -73,8 +73,10 @@ sattn_status sa_forward(const sattn_desc* desc, const void* Q, const void* K, co
 /* sa_backward: exact gradients dQ, dK, dV of <dO, O> (Eq. 7-13 with Eq. 7's
  * index condition, G3).  O and LSE must come from sa_forward on the same
  * inputs (not checked: undefined results otherwise).  ws >= sa_backward_workspace(desc)
- * bytes of device memory (holds delta_t = dO_t . O_t, fp32).  Deterministic
- * (no atomics): bitwise reproducible run to run.                              */
+ * bytes of device memory (holds delta_t = sum_u P_tu dP_tu, fp32, which equals
+ * dO_t . O_t for the exact O: the tensor-core path forms it from P and dP (G26),
+ * the CUDA-core path from dO and O).  Deterministic (no atomics): bitwise
+ * reproducible run to run.                                                    */
 size_t sa_backward_workspace(const sattn_desc* desc);
 sattn_status sa_backward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
                          const void* O, const float* LSE, const void* dO,

@@ -175,10 +175,11 @@ sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const v
 }
 
 size_t attn_bwd_ws(const sattn_desc* d, bool llsa) {
-  // delta and LSE*log2(e), fp32, rows padded to a multiple of 4 frames (16-byte TMA rows)
+  // delta and LSE*log2(e) (+ for LLSA the staircase part of delta), fp32, per channel, rows
+  // padded to a multiple of 4 frames (16-byte TMA rows)
   const size_t C = llsa ? d->R + 1 : 1;
   const size_t Tp = (size_t)((d->T + 3) & ~3LL);
-  return 2 * C * d->B * d->H * Tp * sizeof(float);
+  return (llsa ? 3 : 2) * C * d->B * d->H * Tp * sizeof(float);
 }
 
 sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const void* K, const void* V,

@@ -13,8 +13,9 @@
 //
 //  forward  (sa_fwd_tc):   S = Q K^T -> softmax (row max/sum in registers, one thread
 //                          per row) -> P -> O = P V (V read MN-major) -> O / l, LSE.
-//  backward K1 (sa_bwd_dq_tc, query-major):  delta = rowsum(dO o O); S = Q K^T ->
-//                          P = exp(S - LSE); dP = dO V^T (same TMEM columns) ->
+//  backward K1 (sa_bwd_dq_tc, query-major):  S = Q K^T -> P = exp(S - LSE);
+//                          dP = dO V^T (same TMEM columns) -> delta = rowsum(P o dP)
+//                          (G26: not dO . O, so the bf16 rounding of O never enters) ->
 //                          dS = P (dP - delta); dQ = scale dS K.
 //  backward K2 (sa_bwd_dkdv_tc, key-major):   S^T = K Q^T -> P^T; dP^T = V dO^T ->
 //                          dS^T; dV = P^T dO; dK = scale dS^T Q.
@@ -59,6 +60,9 @@ struct TcArgs {
   int kshift;                                    // keys of query t are frames [t-L-kshift, t+R-kshift]
                                                  // (0 for SA; R-c for LLSA channel c's band, with R := 0)
   float* ws_del; float* ws_l2;                   // padded [BH][Tp] delta / LSE*log2e rows (K1 -> K2)
+  const float* ws_dx;                            // padded [BH][Tp] rowsum(P o dP) over slots outside the
+                                                 // band (LLSA staircase, from the stair pre-pass); null for SA
+  int dq_split;                                  // K1: dQ MMA on bf16 dS hi + lo (LLSA, whose dQ is rounded twice)
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
@@ -125,13 +129,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // Write a thread's bf16 row of an A operand held in TMEM (K-major: lane = row, packed
 // column c = elements 2c, 2c+1): the strip s[0..CW) at elements [32*q4, 32*q4 + CW),
 // zeros for the rest of [0, NK).  `pa` = TMEM address of (this warp's lane 0, column 0).
-template <int CW, int NK>
+// x - bf16(x): the rounding residual, itself rounded to bf16 (x ~= hi + lo to ~2^-17 relative)
+__device__ __forceinline__ float bf16_resid(float x) { return x - __bfloat162float(__float2bfloat16_rn(x)); }
+
+template <int CW, int NK, bool LO = false>
 __device__ __forceinline__ void tmem_write_row(uint32_t pa, int q4, const float* s) {
   const int c0 = 16 * q4;
 #pragma unroll
-  for (int j = 0; j < CW / 8; ++j)
-    tc::tmem_st4(pa + c0 + 4 * j, pack_bf16(s[8 * j], s[8 * j + 1]), pack_bf16(s[8 * j + 2], s[8 * j + 3]),
-                 pack_bf16(s[8 * j + 4], s[8 * j + 5]), pack_bf16(s[8 * j + 6], s[8 * j + 7]));
+  for (int j = 0; j < CW / 8; ++j) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = LO ? bf16_resid(s[8 * j + e]) : s[8 * j + e];
+    tc::tmem_st4(pa + c0 + 4 * j, pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                 pack_bf16(v[6], v[7]));
+  }
   for (int c = 0; c < NK / 2; c += 4)
     if (c < c0 || c >= c0 + CW / 2) tc::tmem_st4(pa + c, 0u, 0u, 0u, 0u);
 }
@@ -327,17 +338,18 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// backward K1 (query-major): delta_t = dO_t . O_t, dQ_t = scale * sum_u dS_tu K_u.
+// backward K1 (query-major): delta_t = sum_u P_tu dP_tu, dQ_t = scale * sum_u dS_tu K_u.
 // Persistent, warp-specialised like the forward.  Per tile (128 queries, TMEM buffer b):
 //   MMA  S = Q K^T -> X_b                      WG  P = exp2(S*sl2 - LSE*log2e)   (registers)
-//   MMA  dP = dO V^T -> X_b (same columns)     WG  dS = P (dP - delta) -> X_b as packed bf16
+//   MMA  dP = dO V^T -> X_b (same columns)     WG  delta = rowsum(P dP) (+ ws_dx);
+//                                                  dS = P (dP - delta) -> X_b as packed bf16
 //   MMA  dQ = dS K -> Y_b (A = dS from TMEM)   WG  dQ * scale -> smem -> TMA store
 // ------------------------------------------------------------------------------------------
 template <int CW> struct DqCfg {
   static constexpr int NK = nk_of(CW);
   static constexpr int QB = kM * 128;
   static constexpr int KB = NK * 128;
-  static constexpr int STAGE = 3 * QB + 2 * KB;   // Q, dO, O, K, V (1024-aligned: 128B-swizzle atoms)
+  static constexpr int STAGE = 2 * QB + 2 * KB;   // Q, dO, K, V (1024-aligned: 128B-swizzle atoms)
   static constexpr int NS = 2;
   static constexpr int SMEM = 1024 + NS * STAGE + 2 * QB + 512;
   static constexpr int THREADS = 320;
@@ -347,12 +359,12 @@ template <int CW>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                 const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmdQ, TcArgs a) {
+                 const __grid_constant__ CUtensorMap tmdQ, TcArgs a) {
   using C = DqCfg<CW>;
   constexpr int NK = C::NK, NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage0 = smem;                       // [Q | dO | O | K | V] per stage
+  uint8_t* stage0 = smem;                       // [Q | dO | K | V] per stage
   uint8_t* obuf0 = smem + NS * C::STAGE;        // dQ staging, one per warpgroup
   uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 2 * C::QB);
   uint64_t* full = bars;              // [NS]
@@ -373,7 +385,7 @@ __global__ void __launch_bounds__(320, 1)
 
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmO); tc::tma_prefetch_desc(&tmdQ);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdQ);
     for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
@@ -398,12 +410,11 @@ __global__ void __launch_bounds__(320, 1)
         const int st = k % NS;
         uint8_t* b0 = stage0 + st * C::STAGE;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
-        tc::mbar_expect_tx(&full[st], 3 * C::QB + 2 * C::KB);
+        tc::mbar_expect_tx(&full[st], 2 * C::QB + 2 * C::KB);
         tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
         tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
-        tc::tma_load_3d(b0 + 2 * C::QB, &tmO, &full[st], 0, t0, bh);
-        tc::tma_load_3d(b0 + 3 * C::QB, &tmK, &full[st], 0, t0 - a.L - a.kshift, bh);
-        tc::tma_load_3d(b0 + 3 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - a.kshift, bh);
+        tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - a.kshift, bh);
+        tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - a.kshift, bh);
       }
     }
   } else if (warp == 1) {
@@ -417,10 +428,15 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = ndq & 1, st = ndq % NS;
           const uint32_t x = tbase + b * 256;
-          const uint32_t kk = tc::smem_u32(stage0 + st * C::STAGE) + 3 * C::QB;
+          const uint32_t kk = tc::smem_u32(stage0 + st * C::STAGE) + 2 * C::QB;
 #pragma unroll
           for (int j = 0; j < NK / 16; ++j)
             tc::mma_bf16_ts(x + NK, x + 8 * j, tc::desc_mnmajor_sw128(kk + 2048 * j), idQ, j > 0);
+          if (a.dq_split) {
+#pragma unroll
+            for (int j = 0; j < NK / 16; ++j)   // + dS_lo K
+              tc::mma_bf16_ts(x + NK, x + NK / 2 + 8 * j, tc::desc_mnmajor_sw128(kk + 2048 * j), idQ, true);
+          }
           tc::mma_commit(&dqfull[b]);
           tc::mma_commit(&empty[st]);
           ++ndq;
@@ -430,7 +446,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t dO = base + C::QB, v = base + 3 * C::QB + C::KB;
+          const uint32_t dO = base + C::QB, v = base + 2 * C::QB + C::KB;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(v + 32 * j), idS,
@@ -443,7 +459,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
-          const uint32_t q = base, kk = base + 3 * C::QB;
+          const uint32_t q = base, kk = base + 2 * C::QB;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kk + 32 * j), idS,
@@ -460,48 +476,23 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
     uint8_t* ostage = obuf0 + wg * C::QB;
-    float* ws_del = a.ws_del;                             // [BH][Tp]
-    float* ws_l2 = a.ws_l2;                               // [BH][Tp]
-    // LSE of this warpgroup's next tile is loaded one tile ahead (off the critical path)
-    auto lse_of = [&](int k) -> float {
-      if (k >= ntile_me) return 0.f;
+    // LSE (and the staircase rowsum) of this warpgroup's next tile are loaded one tile ahead
+    auto row_of = [&](int k, const float* src, int stride, float mul) -> float {
+      if (k >= ntile_me || !src) return 0.f;
       const int g = blockIdx.x + k * gridDim.x;
       const int t = (g % ntq) * kM + r;
-      return t < T ? a.LSEin[(long long)(g / ntq) * T + t] * kLog2e : 0.f;
+      return t < T ? src[(long long)(g / ntq) * stride + t] * mul : 0.f;
     };
-    float lse_next = lse_of(wg);
+    float lse_next = row_of(wg, a.LSEin, T, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, t0 = (g % ntq) * kM;
       const int t = t0 + r;
       const bool row_ok = t < T;
-      const int b = wg, use = k >> 1, st = k % NS;
-      const float lse2 = lse_next;
-      lse_next = lse_of(k + 2);
-      // delta_t = dO_t . O_t from the staged (128B-swizzled) tiles
-      tc::mbar_wait(&full[st], (k / NS) & 1);
-      float delta = 0.f;
-      {
-        const uint32_t dO = tc::smem_u32(stage0 + st * C::STAGE) + C::QB + r * 128;
-        const uint32_t O = dO + C::QB;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint32_t off = (c ^ (r & 7)) << 4;
-          const uint4 x = tc::ld_shared_v4(dO + off), y = tc::ld_shared_v4(O + off);
-          const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
-          const __nv_bfloat162* hy = reinterpret_cast<const __nv_bfloat162*>(&y);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 fx = __bfloat1622float2(hx[e]), fy = __bfloat1622float2(hy[e]);
-            delta = fmaf(fx.x, fy.x, fmaf(fx.y, fy.y, delta));
-          }
-        }
-      }
-      // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
-      if (t < a.Tp) {
-        ws_del[(long long)bh * a.Tp + t] = row_ok ? delta : 0.f;
-        ws_l2[(long long)bh * a.Tp + t] = row_ok ? lse2 : 0.f;
-      }
+      const int b = wg, use = k >> 1;
+      const float lse2 = lse_next, dx = dx_next;
+      lse_next = row_of(k + 2, a.LSEin, T, kLog2e);
+      dx_next = row_of(k + 2, a.ws_dx, a.Tp, 1.f);
       const uint32_t x = tbase + lanes + b * 256;
       // P from S
       tc::mbar_wait(&sfull[b], use & 1);
@@ -520,22 +511,50 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
-      // dS from dP
+      // delta = rowsum(P o dP), then dS from dP
       tc::mbar_wait(&dpfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
+      float delta = dx;
+      if constexpr (CW <= 72) {   // dP held in registers
+        float dp[CW];
 #pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + 32 * q4 + 8 * j, dp);
+        for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, dp + 8 * j);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) p[8 * j + e] *= dp[e] - delta;
+        for (int i = 0; i < CW; ++i) delta = fmaf(p[i], dp[i], delta);
+#pragma unroll
+        for (int i = 0; i < CW; ++i) p[i] *= dp[i] - delta;
+      } else {                    // wide bands: read dP from TMEM twice instead of spilling
+#pragma unroll
+        for (int j = 0; j < CW / 8; ++j) {
+          float dp[8];
+          tc::tmem_ld8(x + 32 * q4 + 8 * j, dp);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) delta = fmaf(p[8 * j + e], dp[e], delta);
+        }
+#pragma unroll
+        for (int j = 0; j < CW / 8; ++j) {
+          float dp[8];
+          tc::tmem_ld8(x + 32 * q4 + 8 * j, dp);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; ++e) p[8 * j + e] *= dp[e] - delta;
+        }
       }
+      // LLSA: dS as bf16 hi + lo (columns [0, NK/2) and [NK/2, NK), both dead fp32 S/dP by now):
+      // the dQ MMA then sees dS to ~2^-17 instead of bf16's 2^-9 (G27: LLSA dQ is rounded twice)
       tmem_write_row<CW, NK>(x, q4, p);
+      if (a.dq_split) tmem_write_row<CW, NK, true>(x + NK / 2, q4, p);
       tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&dsfull[b]);
+      // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
+      if (t < a.Tp) {
+        a.ws_del[(long long)bh * a.Tp + t] = row_ok ? delta : 0.f;
+        a.ws_l2[(long long)bh * a.Tp + t] = row_ok ? lse2 : 0.f;
+      }
       // dQ epilogue
       tc::mbar_wait(&dqfull[b], use & 1);
       __syncwarp();
@@ -1186,9 +1205,9 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   constexpr int NK = nk_of(CW);
   const int Tp = (a.T + 3) & ~3;
   const float* l2ws = a.delta + (long long)a.BH * Tp;
-  CUtensorMap mq, mk, mv, mdo, mo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv, ml2, mdel;
+  CUtensorMap mq, mk, mv, mdo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv, ml2, mdel;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
-      !make_map(&mdo, a.dO, a.T, a.BH, kM) || !make_map(&mo, a.O, a.T, a.BH, kM) ||
+      !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
       !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
       !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
       !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
@@ -1200,7 +1219,7 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   const char* only = getenv("SATTN_BWD_ONLY");  // debug: run only K1 ("1") or only K2 ("2")
   if (!only || only[0] != '2') {
   cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
-  launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mo, mdq,
+  launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq,
              tc_args(a));
   }
   if (!only || only[0] != '1')
@@ -1223,7 +1242,6 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   const bf16* Q = reinterpret_cast<const bf16*>(a.Q);
   const bf16* K = reinterpret_cast<const bf16*>(a.K);
   const bf16* V = reinterpret_cast<const bf16*>(a.V);
-  const bf16* O = reinterpret_cast<const bf16*>(a.O);
   const bf16* dO = reinterpret_cast<const bf16*>(a.dO);
   bf16* dQ = reinterpret_cast<bf16*>(a.dQ);
   bf16* dK = reinterpret_cast<bf16*>(a.dK);
@@ -1233,25 +1251,41 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   const int Tp = (a.T + 3) & ~3;
   float* ws_del = a.delta;                          // [C][BH][Tp]
   float* ws_l2 = a.delta + (long long)C * a.BH * Tp;
+  float* ws_dx = a.delta + 2LL * C * a.BH * Tp;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  StairArgs sa{};
+  sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
+  sa.dQ = dQ; sa.dK = dK; sa.dV = dV;
+  sa.del = ws_del; sa.l2 = ws_l2; sa.lse = a.LSE; sa.dx = ws_dx;
+  sa.T = a.T; sa.L = a.L; sa.R = R; sa.BH = a.BH; sa.Tp = Tp;
+  sa.in_cs = a.in_cs; sa.plane = plane;
+  sa.scale = a.scale; sa.scale_log2 = a.scale_log2;
+  // horizons run to T - 1 + R (the last staircase keys / queries of channels > 0)
+  const dim3 sgrid((a.T + R + kStF - 1) / kStF, a.BH);
+  // (0) staircase part of delta = rowsum(P o dP)
+  {
+    const size_t smem = stair_smem_bytes(R, true);
+    cudaFuncSetAttribute(llsa_bwd_stair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    llsa_bwd_stair<true><<<sgrid, 256, smem, st>>>(sa);
+  }
   // (1) query-major band pass per channel c: SA dQ kernel with R := 0 and keys shifted by R - c
   cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
   for (int c = 0; c < C; ++c) {
-    CUtensorMap mq, mk, mv, mdo, mo, mdq;
+    CUtensorMap mq, mk, mv, mdo, mdq;
     if (!make_map(&mq, Q + a.in_cs * c, a.T, a.BH, kM) || !make_map(&mk, Kr, a.T, a.BH, NK) ||
         !make_map(&mv, Vr, a.T, a.BH, NK) || !make_map(&mdo, dO + plane * c, a.T, a.BH, kM) ||
-        !make_map(&mo, O + plane * c, a.T, a.BH, kM) || !make_map(&mdq, dQ + plane * c, a.T, a.BH, kM))
+        !make_map(&mdq, dQ + plane * c, a.T, a.BH, kM))
       return SATTN_ECUDA;
     TcArgs t = tc_args(a);
     t.R = 0;
     t.kshift = R - c;
-    t.Og = O + plane * c;
     t.LSEin = a.LSE + (long long)c * a.BH * a.T;
     t.ws_del = ws_del + (long long)c * a.BH * Tp;
     t.ws_l2 = ws_l2 + (long long)c * a.BH * Tp;
-    launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mo, mdq,
-               t);
+    t.ws_dx = ws_dx + (long long)c * a.BH * Tp;
+    t.dq_split = 1;
+    launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq, t);
   }
   // (2) key-major band pass: dK, dV of channel R accumulated over the C query channels
   {
@@ -1267,19 +1301,11 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
     launch_pdl(llsa_bwd_kv_tc<CW>, dim3(grid), dim3(320), LC::SMEM, st, mq4, mk, mv, mdo4, mdk, mdv, ml2, mdel, t, C,
                bc ? 1 : 0);
   }
-  // (3) staircase keys and the staircase part of dQ (CUDA cores)
+  // (3) staircase keys and the staircase part of dQ (mma.sync)
   {
-    StairArgs sa{};
-    sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
-    sa.dQ = dQ; sa.dK = dK; sa.dV = dV;
-    sa.del = ws_del; sa.l2 = ws_l2;
-    sa.T = a.T; sa.L = a.L; sa.R = R; sa.BH = a.BH; sa.Tp = Tp;
-    sa.in_cs = a.in_cs; sa.plane = plane;
-    sa.scale = a.scale; sa.scale_log2 = a.scale_log2;
-    const size_t smem = stair_smem_bytes(R);
-    cudaFuncSetAttribute(llsa_bwd_stair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    // horizons run to T - 1 + R (the last staircase keys / queries of channels > 0)
-    llsa_bwd_stair<<<dim3((a.T + R + kStF - 1) / kStF, a.BH), 256, smem, st>>>(sa);
+    const size_t smem = stair_smem_bytes(R, false);
+    cudaFuncSetAttribute(llsa_bwd_stair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    llsa_bwd_stair<false><<<sgrid, 256, smem, st>>>(sa);
   }
   return SATTN_OK;
 }
@@ -1339,7 +1365,7 @@ sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-int tc_llsa_backward_launches(int R) { return (R + 1) + 2; }
+int tc_llsa_backward_launches(int R) { return (R + 1) + 3; }
 void tc_set_trace(void* p) { g_trace = static_cast<long long*>(p); }
 const char* tc_last_error() { return g_tc_err.c_str(); }
 

@@ -76,9 +76,9 @@ def test_null_and_misaligned_pointers_rejected(lib):
 def test_workspace_and_saved_sizes(lib):
     import paper_2302_13451_b200 as pkg
     d = _desc(B=2, H=3, T=37, D=8, L=5, R=2)
-    # delta + LSE*log2(e), rows padded to 40 frames
+    # delta + LSE*log2(e) (+ LLSA: staircase part of delta) per channel, rows padded to 40 frames
     assert lib.sa_backward_workspace(ctypes.byref(d)) == 2 * 2 * 3 * 40 * 4
-    assert lib.llsa_backward_workspace(ctypes.byref(d)) == 2 * 3 * 2 * 3 * 40 * 4
+    assert lib.llsa_backward_workspace(ctypes.byref(d)) == 3 * 3 * 2 * 3 * 40 * 4
     assert lib.sattn_stack_saved_bytes(ctypes.byref(d), pkg.MODE_SA, 2) > 0
     assert lib.sattn_stack_saved_bytes(ctypes.byref(d), 9, 2) == 0
     bad = _desc(T=0)

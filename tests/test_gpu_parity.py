@@ -36,6 +36,25 @@ def maxerr(got, ref):
     return float(np.abs(host(got) - np.asarray(ref)).max()) if np.asarray(ref).size else 0.0
 
 
+def bf16_ulp(ref):
+    """Spacing of the bf16 grid at |ref| (8 significant bits)."""
+    a = np.abs(np.asarray(ref, dtype=np.float64))
+    return np.exp2(np.floor(np.log2(np.maximum(a, 2.0 ** -126))) - 7)
+
+
+def excess(got, ref, dt):
+    """max over elements of |got - ref| - bound, bound = TOL (fp32) or, for bf16 outputs,
+    max(TOL, ulp_bf16(ref)) (G27: a bf16 result is within the gate or is one of the
+    two bf16 neighbours of the exact value; the relaxation only acts where |ref| >= 4, where a
+    correctly rounded value alone may sit 0.0156 from it).  <= 0 passes."""
+    ref = np.asarray(ref)
+    if not ref.size:
+        return 0.0
+    e = np.abs(host(got) - ref)
+    bound = TOL[dt] if dt == "f32" else np.maximum(TOL[dt], bf16_ulp(ref))
+    return float((e - bound).max())
+
+
 SA_F32 = [
     ((1, 1, 16, 4), 3, 1), ((2, 3, 37, 4), 0, 0), ((2, 3, 37, 4), 3, 1), ((2, 3, 37, 4), 0, 5),
     ((2, 3, 37, 4), 5, 0), ((1, 2, 129, 64), 32, 8), ((1, 2, 129, 64), 32, 16), ((1, 2, 300, 64), 200, 150),
@@ -75,7 +94,7 @@ def test_sa_bf16(shape, L, R, impl):
     O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
     G = oracle.sa.sa_backward(q, k, v, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert maxerr(got, ref) <= TOL["bf16"], (name, maxerr(got, ref))
+        assert excess(got, ref, "bf16") <= 0, (name, maxerr(got, ref))
 
 
 @pytest.mark.parametrize("impl", ["auto", "ffma"])
@@ -95,7 +114,7 @@ def test_sa_full_base_shape_sampled_heads(impl):
         G = oracle.sa.sa_backward(q, k, v, do, L, R)
         for name, got, ref in (("O", o[b, h], O), ("LSE", lse[b, h], LSE), ("dQ", dq[b, h], G[0]),
                                ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert maxerr(got, ref) <= TOL["bf16"], (b, h, name, maxerr(got, ref))
+            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
 
 
 LLSA_CASES = [
@@ -125,7 +144,7 @@ def test_llsa(dt, shape, L, R, broadcast):
     O, LSE = oracle.llsa.llsa_forward(Q, K, V, L, R)
     G = oracle.llsa.llsa_backward(Q, K, V, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert maxerr(got, ref) <= TOL[dt], (name, maxerr(got, ref))
+        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
 
 
 def test_deterministic_bitwise():
