@@ -147,10 +147,14 @@ __global__ void __launch_bounds__(320, 1)
       const int nstair = 2 * R;                           // 16-row k-steps over the stair V blocks
       int ns = 0, np = 0;
       while (np < nitems) {
+        const int kts = ns / NI;
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&hfull[kts & 1]), (kts >> 1) & 1,
+                                          tc::smem_u32(&qfull[ns % Cf::NSQ]), (ns / Cf::NSQ) & 1,
+                                          tc::smem_u32(&pfull[np & 1]), (np >> 1) & 1,
+                                          tc::smem_u32(&tfree[np & 1]), ((np + 2) >> 1) & 1);   // = (np-2)>>1 parity
         if (ns < nitems && ns < np + 2) {
-          const int kt = ns / NI, qs = ns % Cf::NSQ;
-          if (tc::mbar_try_wait(tc::smem_u32(&hfull[kt & 1]), (kt >> 1) & 1) &&
-              tc::mbar_try_wait(tc::smem_u32(&qfull[qs]), (ns / Cf::NSQ) & 1)) {
+          const int kt = kts, qs = ns % Cf::NSQ;
+          if ((m & 1) && (m & 2)) {
             tc::tc_fence_after();
             const uint32_t q = tc::smem_u32(qstage0 + qs * Cf::QB);
             const uint32_t kb = tc::smem_u32(hstage0 + (kt & 1) * Cf::HSTAGE);
@@ -163,8 +167,7 @@ __global__ void __launch_bounds__(320, 1)
             continue;
           }
         }
-        if (np < ns && tc::mbar_try_wait(tc::smem_u32(&pfull[np & 1]), (np >> 1) & 1) &&
-            (np < 2 || tc::mbar_try_wait(tc::smem_u32(&tfree[np & 1]), ((np - 2) >> 1) & 1))) {
+        if (np < ns && (m & 4) && (np < 2 || (m & 8))) {
           tc::tc_fence_after();
           const int kt = np / NI, b = np & 1;
           const uint32_t hb = tc::smem_u32(hstage0 + (kt & 1) * Cf::HSTAGE);

@@ -34,6 +34,38 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking probe (mbarrier.test_wait): for the out-of-order polling loops of the MMA
+// issuers.  try_wait may suspend the thread for a while before reporting "not yet", which
+// would stall every other ready task of the loop behind one unready barrier.
+__device__ __forceinline__ bool mbar_test(uint32_t a, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// Four independent probes in one asm block: their ~150-cycle latencies overlap instead of adding
+// up.  Bit i of the result = barrier i has completed phase p_i.
+__device__ __forceinline__ uint32_t mbar_test4(uint32_t a0, uint32_t p0, uint32_t a1, uint32_t p1, uint32_t a2,
+                                               uint32_t p2, uint32_t a3, uint32_t p3) {
+  uint32_t m;
+  asm volatile(
+      "{\n\t.reg .pred Q0, Q1, Q2, Q3;\n\t.reg .b32 r0, r1, r2, r3;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 Q0, [%1], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 Q1, [%3], %4;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 Q2, [%5], %6;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 Q3, [%7], %8;\n\t"
+      "selp.b32 r0, 1, 0, Q0;\n\tselp.b32 r1, 2, 0, Q1;\n\tselp.b32 r2, 4, 0, Q2;\n\tselp.b32 r3, 8, 0, Q3;\n\t"
+      "or.b32 r0, r0, r1;\n\tor.b32 r2, r2, r3;\n\tor.b32 %0, r0, r2;\n\t}"
+      : "=r"(m)
+      : "r"(a0), "r"(p0), "r"(a1), "r"(p1), "r"(a2), "r"(p2), "r"(a3), "r"(p3)
+      : "memory");
+  return m;
+}
 // Blocking wait for the completion of phase `phase` (parity).  Bounded: a barrier that never
 // completes (a protocol bug) traps instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {

@@ -73,29 +73,34 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// per-CTA [start, end] globaltimer stamps at tr[512 + 2*cta] (debug)
+// per-CTA [start, end] globaltimer stamps at tr[1024 + 2*cta] (debug); phase events at tr[ev*64 + k], ev < 16
 __device__ __forceinline__ void trace_cta(long long* tr, int which) {
-  if (tr && threadIdx.x == 0 && blockIdx.x < 256) tr[512 + 2 * blockIdx.x + which] = gtimer();
+  if (tr && threadIdx.x == 0 && blockIdx.x < 256) tr[1024 + 2 * blockIdx.x + which] = gtimer();
 }
 
 // ------------------------------------------------------------------------------------------
 // forward: persistent, warp-specialised.  One CTA per SM loops over 128-row tiles.
-//   warp 0      TMA producer   (Q, K, V of tile k into smem stage k % NS)
+//   warp 0      TMA producer   (Q, K of tile k into QK stage k % NQK)
 //   warp 1      MMA issuer     (S(k+1) = Q K^T issued before O(k) = P V, so the tensor
-//                               core works on the next tile while softmax runs)
-//   warps 2..5  softmax + epilogue (row r = 32 * (warp % 4) + lane = TMEM lane r)
-// TMEM: two buffers of 256 columns (S in [0, NK), O in [NK, NK + 64)); smem: NS stages of
-// Q/K/V and two P tiles.  mbarriers: full/empty per stage, sfull/ofull/pfull/tfree per
-// TMEM buffer.
+//                               core works on the next tile while softmax runs) and the
+//                               V loads: V(k) is fetched into V stage k % NV only once S(k-1)
+//                               is issued, so a V stage is held ~TMA latency + softmax, not
+//                               for the tile's whole life (more tiles in flight per smem byte)
+//   warps 2..9  two softmax + epilogue warpgroups (row r = 32 * (warp % 4) + lane = TMEM lane r)
+// TMEM: two buffers of 256 columns (S in [0, NK), O in [NK, NK + 64)); smem: NQK stages of
+// Q/K, NV stages of V, two O staging tiles.  mbarriers: full/empty per stage, sfull/ofull/
+// pfull/tfree per TMEM buffer.
 // ------------------------------------------------------------------------------------------
 template <int CW> struct FwdCfg {
   static constexpr int NK = nk_of(CW);
   static constexpr int QB = kM * 128;
   static constexpr int KB = NK * 128;
   static constexpr int STAGE = QB + 2 * KB;
+  static constexpr int QKB = QB + KB;                       // Q/K stage (1024-aligned)
   static constexpr int OB = kM * 128;                       // O staging tile for the TMA store
   static constexpr int NS = (1024 + 3 * STAGE + 2 * OB + 256 <= 232448) ? 3 : 2;
-  static constexpr int SMEM = 1024 + NS * STAGE + 2 * OB + 256;
+  static constexpr int NQK = NS, NV = NS;
+  static constexpr int SMEM = 1024 + NQK * QKB + NV * KB + 2 * OB + 256;
   static constexpr int THREADS = 320;   // TMA warp, MMA warp, 2 softmax warpgroups
 };
 
@@ -167,15 +172,18 @@ __global__ void __launch_bounds__(320, 1)
     sa_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, TcArgs a) {
   using C = FwdCfg<CW>;
-  constexpr int NK = C::NK, NS = C::NS;
+  constexpr int NK = C::NK, NQK = C::NQK, NV = C::NV;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage0 = smem;
-  uint8_t* obuf0 = smem + NS * C::STAGE;
+  uint8_t* qk0 = smem;                          // [Q | K] x NQK
+  uint8_t* v0 = qk0 + NQK * C::QKB;             // V x NV
+  uint8_t* obuf0 = v0 + NV * C::KB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 2 * C::OB);
-  uint64_t* full = bars;            // [NS]
-  uint64_t* empty = bars + NS;      // [NS]
-  uint64_t* sfull = bars + 2 * NS;  // [2]
+  uint64_t* full = bars;            // [NQK] Q/K landed
+  uint64_t* empty = full + NQK;     // [NQK] Q/K stage free (S issued and done)
+  uint64_t* vfull = empty + NQK;    // [NV]
+  uint64_t* vempty = vfull + NV;    // [NV]
+  uint64_t* sfull = vempty + NV;    // [2]
   uint64_t* ofull = sfull + 2;      // [2]
   uint64_t* pfull = ofull + 2;      // [2]
   uint64_t* tfree = pfull + 2;      // [2]
@@ -193,7 +201,8 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch_desc(&tmK);
     tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmO);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NQK; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NV; ++i) { tc::mbar_init(&vfull[i], 1); tc::mbar_init(&vempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&ofull[i], 1);
       tc::mbar_init(&pfull[i], 128); tc::mbar_init(&tfree[i], 128);
@@ -219,24 +228,29 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_prefetch_3d(&tmK, 0, t0 - a.L, bh);
         tc::tma_prefetch_3d(&tmV, 0, t0 - a.L, bh);
       };
-      for (int k = NS; k < 2 * NS; ++k) prefetch(k);
+      for (int k = NQK; k < 2 * NQK; ++k) prefetch(k);
       for (int k = 0; k < ntile_me; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, t0 = (g % ntq) * kM;
-        const int st = k % NS;
-        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
-        if (k >= NS) prefetch(k + NS);
-        uint8_t* sQ = stage0 + st * C::STAGE;
+        const int st = k % NQK;
+        if (k >= NQK) tc::mbar_wait(&empty[st], ((k - NQK) / NQK) & 1);
+        if (k >= NQK) prefetch(k + NQK);
+        uint8_t* sQ = qk0 + st * C::QKB;
         trace_at(a.trace, 0, k);
-        tc::mbar_expect_tx(&full[st], C::STAGE);
+        tc::mbar_expect_tx(&full[st], C::QKB);
         // boxes may be split into a.qsplit / a.ksplit row blocks (multiples of 8 rows)
         for (int i = 0; i < a.qsplit; ++i)
           tc::tma_load_3d(sQ + i * (C::QB / a.qsplit), &tmQ, &full[st], 0, t0 + i * (kM / a.qsplit), bh);
-        for (int i = 0; i < a.ksplit; ++i) {
+        for (int i = 0; i < a.ksplit; ++i)
           tc::tma_load_3d(sQ + C::QB + i * (C::KB / a.ksplit), &tmK, &full[st], 0, t0 - a.L + i * (C::NK / a.ksplit), bh);
-          tc::tma_load_3d(sQ + C::QB + C::KB + i * (C::KB / a.ksplit), &tmV, &full[st], 0,
+        // V(k) into its own ring: the stage frees when PV(k - NV) completes
+        const int sv = k % NV;
+        if (k >= NV) tc::mbar_wait(&vempty[sv], ((k - NV) / NV) & 1);
+        trace_at(a.trace, 9, k);
+        tc::mbar_expect_tx(&vfull[sv], C::KB);
+        for (int i = 0; i < a.ksplit; ++i)
+          tc::tma_load_3d(v0 + sv * C::KB + i * (C::KB / a.ksplit), &tmV, &vfull[sv], 0,
                           t0 - a.L + i * (C::NK / a.ksplit), bh);
-        }
       }
     }
   } else if (warp == 1) {
@@ -247,34 +261,42 @@ __global__ void __launch_bounds__(320, 1)
       // (PV(k-2) issued: tcgen05 ops of one thread execute in issue order, so PV(k-2) reads
       // P(k-2) before S(k) overwrites those columns); PV(k) as soon as softmax(k) has written
       // P(k) and the epilogue of tile k-2 has drained O.  Neither waits behind the other.
-      int ns = 0, np = 0;
-      while (np < ntile_me) {
-        if (ns < ntile_me && ns < np + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
-          trace_at(a.trace, 1, ns);
-          tc::tc_fence_after();
-          const uint32_t q = tc::smem_u32(stage0 + (ns % NS) * C::STAGE), kk = q + C::QB;
-          const uint32_t d = tbase + (ns & 1) * 256;
+      // In-order schedule with blocking waits (mbarrier.try_wait sleeps and wakes ~60 cycles after
+      // the arrive; a polling loop pays ~150 cycles per probe):  S(0) S(1) | PV(0) S(2) | PV(1) S(3) ...
+      // PV(k) needs P(k) (softmax), the epilogue of tile k-2 (O columns) and V(k); S(k+2) reuses
+      // TMEM buffer k&1, whose P(k) the just-issued PV(k) reads first (tcgen05 ops of one thread
+      // execute in issue order).
+      auto issue_s = [&](int k) {
+        tc::mbar_wait(&full[k % NQK], (k / NQK) & 1);
+        trace_at(a.trace, 1, k);
+        tc::tc_fence_after();
+        const uint32_t q = tc::smem_u32(qk0 + (k % NQK) * C::QKB), kk = q + C::QB;
+        const uint32_t d = tbase + (k & 1) * 256;
 #pragma unroll
-          for (int j = 0; j < kD / 16; ++j)
-            tc::mma_bf16(d, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kk + 32 * j), idS, j > 0);
-          tc::mma_commit(&sfull[ns & 1]);
-          ++ns;
-          continue;
-        }
-        if (np < ns && tc::mbar_try_wait(tc::smem_u32(&pfull[np & 1]), (np >> 1) & 1) &&
-            (np < 2 || tc::mbar_try_wait(tc::smem_u32(&tfree[np & 1]), ((np - 2) >> 1) & 1))) {
-          const int b = np & 1, st = np % NS;
-          trace_at(a.trace, 3, np);
-          tc::tc_fence_after();
-          const uint32_t v = tc::smem_u32(stage0 + st * C::STAGE) + C::QB + C::KB;
-          const uint32_t pa = tbase + b * 256;
+        for (int j = 0; j < kD / 16; ++j)
+          tc::mma_bf16(d, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kk + 32 * j), idS, j > 0);
+        tc::mma_commit(&sfull[k & 1]);
+        tc::mma_commit(&empty[k % NQK]);
+        trace_at(a.trace, 2, k);
+      };
+      issue_s(0);
+      if (ntile_me > 1) issue_s(1);
+      for (int k = 0; k < ntile_me; ++k) {
+        const int b = k & 1, st = k % NV;
+        tc::mbar_wait(&pfull[b], (k >> 1) & 1);
+        if (k >= 2) tc::mbar_wait(&tfree[b], ((k - 2) >> 1) & 1);
+        tc::mbar_wait(&vfull[st], (k / NV) & 1);
+        trace_at(a.trace, 3, k);
+        tc::tc_fence_after();
+        const uint32_t v = tc::smem_u32(v0 + st * C::KB);
+        const uint32_t pa = tbase + b * 256;
 #pragma unroll
-          for (int j = 0; j < NK / 16; ++j)
-            tc::mma_bf16_ts(pa + NK, pa + 8 * j, tc::desc_mnmajor_sw128(v + 2048 * j), idO, j > 0);
-          tc::mma_commit(&ofull[b]);
-          tc::mma_commit(&empty[st]);
-          ++np;
-        }
+        for (int j = 0; j < NK / 16; ++j)
+          tc::mma_bf16_ts(pa + NK, pa + 8 * j, tc::desc_mnmajor_sw128(v + 2048 * j), idO, j > 0);
+        tc::mma_commit(&ofull[b]);
+        tc::mma_commit(&vempty[st]);
+        trace_at(a.trace, 8, k);
+        if (k + 2 < ntile_me) issue_s(k + 2);
       }
     }
   } else {
@@ -423,8 +445,11 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idQ = tc::idesc_bf16(kM, kD, 0, 1);
       int ns = 0, ndp = 0, ndq = 0;
       while (ndq < ntile_me) {
-        if (ndq < ndp && tc::mbar_try_wait(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1) &&
-            (ndq < 2 || tc::mbar_try_wait(tc::smem_u32(&tfree[ndq & 1]), ((ndq - 2) >> 1) & 1))) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
+                                          tc::smem_u32(&tfree[ndq & 1]), ((ndq + 2) >> 1) & 1,   // = (ndq-2)>>1 parity
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
+        if (ndq < ndp && (m & 1) && (ndq < 2 || (m & 2))) {
           tc::tc_fence_after();
           const int b = ndq & 1, st = ndq % NS;
           const uint32_t x = tbase + b * 256;
@@ -442,7 +467,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndq;
           continue;
         }
-        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+        if (ndp < ns && (m & 4)) {
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
@@ -455,7 +480,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndp;
           continue;
         }
-        if (ns < ntile_me && ns < ndq + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
+        if (ns < ntile_me && ns < ndq + 2 && (m & 8)) {
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
@@ -680,8 +705,11 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
       int ns = 0, ndp = 0, nkv = 0;
       while (nkv < ntile_me) {
-        if (nkv < ndp && tc::mbar_try_wait(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1) &&
-            (nkv < 1 || tc::mbar_try_wait(tc::smem_u32(&kvfree[(nkv - 1) & 1]), ((nkv - 1) >> 1) & 1))) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,  // = (nkv-1)>>1 parity
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
+        if (nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
           tc::tc_fence_after();
           const int b = nkv & 1, st = nkv % NS;
           const uint32_t x = tbase + b * 256;
@@ -698,7 +726,7 @@ __global__ void __launch_bounds__(320, 1)
           ++nkv;
           continue;
         }
-        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+        if (ndp < ns && (m & 4)) {
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
@@ -711,7 +739,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndp;
           continue;
         }
-        if (ns < ntile_me && ns < nkv + 2 && tc::mbar_try_wait(tc::smem_u32(&full[ns % NS]), (ns / NS) & 1)) {
+        if (ns < ntile_me && ns < nkv + 2 && (m & 8)) {
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
@@ -911,9 +939,14 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
       int ns = 0, ndp = 0, nkv = 0;
       while (nkv < nsub) {
-        if (nkv < ndp && tc::mbar_try_wait(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1)) {
+        const int kts = ns / C;
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+                                          tc::smem_u32(&kvfull_ld[kts & 1]), (kts >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&qfull[ns & 1]), (ns >> 1) & 1);
+        if (nkv < ndp && (m & 1)) {
           const int kt = nkv / C, c = nkv % C;
-          if (c == 0 && kt >= 1 && !tc::mbar_try_wait(tc::smem_u32(&kvfree[(kt - 1) & 1]), ((kt - 1) >> 1) & 1)) {
+          if (c == 0 && kt >= 1 && !tc::mbar_test(tc::smem_u32(&kvfree[(kt - 1) & 1]), ((kt - 1) >> 1) & 1)) {
             // accumulators still being drained by the previous tile's epilogue
           } else {
             tc::tc_fence_after();
@@ -935,7 +968,7 @@ __global__ void __launch_bounds__(320, 1)
             continue;
           }
         }
-        if (ndp < ns && tc::mbar_try_wait(tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1)) {
+        if (ndp < ns && (m & 4)) {
           tc::tc_fence_after();
           const int b = ndp & 1, kt = ndp / C;
           const uint32_t v = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE) + Cf::KB;
@@ -949,9 +982,8 @@ __global__ void __launch_bounds__(320, 1)
           continue;
         }
         if (ns < nsub && ns < nkv + 2) {
-          const int kt = ns / C;
-          if (tc::mbar_try_wait(tc::smem_u32(&kvfull_ld[kt & 1]), (kt >> 1) & 1) &&
-              tc::mbar_try_wait(tc::smem_u32(&qfull[ns & 1]), (ns >> 1) & 1)) {
+          const int kt = kts;
+          if ((m & 2) && (m & 8)) {
             tc::tc_fence_after();
             const int b = ns & 1;
             const uint32_t kk = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE);

@@ -1,0 +1,12 @@
+"""One LLSA forward + backward at the bench shape (no graphs): for ncu launch lists."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2302_13451_b200 as s
+B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
+C = R + 1
+q, k, v, do = (torch.randn(C, B, H, T, D, device="cuda").to(torch.bfloat16) for _ in range(4))
+for _ in range(2):
+    o, lse = s.llsa_forward(q, k, v, L, R)
+    g = s.llsa_backward(q, k, v, o, lse, do, L, R)
+torch.cuda.synchronize()

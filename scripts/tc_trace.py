@@ -5,7 +5,7 @@ import torch
 import paper_2302_13451_b200 as s
 B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
 q, k, v = (torch.randn(B, H, T, D, device="cuda").to(torch.bfloat16) for _ in range(3))
-buf = torch.zeros(8 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(1024 + 512, dtype=torch.int64, device="cuda")
 lib = s.lib()
 lib.sattn_debug_trace.argtypes = [ctypes.c_void_p]
 for _ in range(3):
@@ -14,10 +14,10 @@ lib.sattn_debug_trace(ctypes.c_void_p(buf.data_ptr()))
 s.sa_forward(q, k, v, L, R, impl="tc")
 torch.cuda.synchronize()
 lib.sattn_debug_trace(None)
-t = buf.view(8, 64).cpu()
+t = buf[:1024].view(16, 64).cpu()
 t0 = int(t[0, 0])
-names = ["tma_issue", "full_ok(S issue)", "pfull_ok", "tfree_ok(PV issue)", "sfull_ok", "P_written", "ofull_ok", "epi_done"]
+names = ["QK_issue", "S_issue", "S_issued", "PV_issue", "sfull_ok", "P_written", "ofull_ok", "epi_done", "PV_issued", "V_issue"]
 n = int((t[0] > 0).sum())
-print("tile " + " ".join(f"{nm:>17s}" for nm in names))
+print("tile " + " ".join(f"{nm:>9s}" for nm in names))
 for kk in range(n):
-    print(f"{kk:4d} " + " ".join(f"{(int(t[e, kk]) - t0) if t[e, kk] else -1:17d}" for e in range(8)))
+    print(f"{kk:4d} " + " ".join(f"{(int(t[e, kk]) - t0) if t[e, kk] else -1:9d}" for e in range(10)))

@@ -6,7 +6,7 @@ import paper_2302_13451_b200 as s
 B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
 q, k, v, do = (torch.randn(B, H, T, D, device="cuda").to(torch.bfloat16) for _ in range(4))
 o, lse = s.sa_forward(q, k, v, L, R, impl="tc")
-buf = torch.zeros(8 * 64, dtype=torch.int64, device="cuda")
+buf = torch.zeros(1024 + 512, dtype=torch.int64, device="cuda")
 lib = s.lib()
 lib.sattn_debug_trace.argtypes = [ctypes.c_void_p]
 for _ in range(3):
@@ -16,7 +16,7 @@ lib.sattn_debug_trace(ctypes.c_void_p(buf.data_ptr()))
 s.sa_backward(q, k, v, o, lse, do, L, R, impl="tc")
 torch.cuda.synchronize()
 lib.sattn_debug_trace(None)
-t = buf.view(8, 64).cpu()
+t = buf[:1024].view(16, 64).cpu()
 t0 = int(t[0, 0])
 names = ["tma_issue", "lsd_loaded", "sfull", "P_done", "dpfull", "PdS_written", "kvfull", "epi_done"]
 n = int((t[0] > 0).sum())
