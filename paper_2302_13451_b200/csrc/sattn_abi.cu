@@ -179,7 +179,10 @@ size_t attn_bwd_ws(const sattn_desc* d, bool llsa) {
   // padded to a multiple of 4 frames (16-byte TMA rows)
   const size_t C = llsa ? d->R + 1 : 1;
   const size_t Tp = (size_t)((d->T + 3) & ~3LL);
-  return (llsa ? 3 : 2) * C * d->B * d->H * Tp * sizeof(float);
+  const size_t rows = (llsa ? 3 : 2) * C * d->B * d->H * Tp * sizeof(float);
+  // SA tensor-core backward: + the fused sweep's CTA hand-off rows (SATTN_SA_BWD=fused)
+  const size_t hand = (!llsa && tc_ok(d, false, true)) ? tc_backward_ws_bytes() : 0;
+  return rows > hand ? rows : hand;
 }
 
 sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const void* K, const void* V,

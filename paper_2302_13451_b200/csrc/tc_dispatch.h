@@ -11,6 +11,7 @@ bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward);
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
 int tc_backward_launches();
+size_t tc_backward_ws_bytes();   // SA tensor-core backward: CTA hand-off rows (fused sweep)
 const char* tc_last_error();
 void tc_set_trace(void* p);  // debug only
 // tensor-core LLSA forward (tc_llsa.cu)

@@ -24,6 +24,7 @@
 // 128B swizzle (K-major for Q/K/V/dO as the head-dim-contracted operand, the same
 // bytes read MN-major when the frame index is the contraction); thread-written
 // P / dS tiles use the no-swizzle 8x16B core-matrix layout.
+#include <cooperative_groups.h>
 #include <cuda.h>
 
 #include <cstdio>
@@ -39,6 +40,7 @@
 
 namespace sattn {
 namespace {
+namespace cg = cooperative_groups;
 
 thread_local std::string g_tc_err;
 long long* g_trace = nullptr;  // debug: device buffer [8][64] for CTA 0 phase timestamps
@@ -63,6 +65,8 @@ struct TcArgs {
   const float* ws_dx;                            // padded [BH][Tp] rowsum(P o dP) over slots outside the
                                                  // band (LLSA staircase, from the stair pre-pass); null for SA
   int dq_split;                                  // K1: dQ MMA on bf16 dS hi + lo (LLSA, whose dQ is rounded twice)
+  int mma_order;                                 // fused backward: MMA issue priority (tuning)
+  float* ws_hand;                                // fused backward: per-CTA dQ hand-off rows [grid][48][64] fp32
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
@@ -1074,6 +1078,440 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
+// ------------------------------------------------------------------------------------------
+// backward, fused single pass (SA): one key-major sweep per CTA over a contiguous range of key
+// tiles (head-major, time-minor), so each dQ row is finished inside the sweep instead of by a
+// second, query-major kernel (1028 B per head-frame instead of K1 + K2's 1424).
+// Per key tile (128 keys u0.., query window n0 = u0 - R .. n0 + NQ):
+//   WG   LSE*log2e and delta_n = dO_n . O_n of the NQ window rows (Eq. 9's <g, p> term)
+//   MMA  S^T = K Q^T -> X_b                  WG  P^T = exp2(S^T*sl2 - LSE_n*log2e)
+//   MMA  dP^T = V dO^T -> X_b                WG  dS^T = P^T (dP^T - delta_n); P^T, dS^T -> X_b
+//                                                (packed bf16, TMEM A operands) and dS^T -> smem
+//   MMA  dV = P^T dO, dK = dS^T Q            WG  rows -> global
+//   MMA  dQ0 = dS[queries 0..127] K  -> X_b[0, 64)      (A = dS^T read MN-major from smem)
+//        dQ1 = dS[queries 128..255] K -> X_b[64, 128)   (only keys >= 128 - W + 1 reach them)
+//                                            WG  dQ rows 0..W-2 of a tile also receive the previous
+//                                                key tile's dQ1 (the "carry", in smem) -> global
+// The dS^T buffer holds the window's query columns as three 64-column chunks in the order
+// [c2 | c0 | c1] (16 KB each, 128 key rows, 128B swizzle).  dQ0 reads c0, c1 (LBO = 16 KB); dQ1
+// reads c2 and then "c3" = c2 + 16 KB = c0, whose key rows >= 64 are never written (every row's
+// band starts at its own key, so rows >= 64 only reach columns >= 64): zeros, as the padded
+// query rows 192..255 must be.  A CTA's first tile (if not a head start) and last tile (if not a
+// head end) meet the neighbouring CTA's tiles: the first tile's dQ0 rows 0..W-2 go to a per-CTA
+// workspace slot, a grid-wide barrier (cooperative launch) orders them, and the CTA owning the
+// previous key tile adds them to its dQ1 carry.  fp32 a + b == b + a, so the result is bitwise
+// independent of where the CTA ranges fall (time-sharded == unsharded, G18).
+// ------------------------------------------------------------------------------------------
+template <int CW> struct FusCfg {
+  static constexpr int NQ = nk_of(CW);
+  static constexpr int KB = kM * 128;
+  static constexpr int QB = NQ * 128;
+  static constexpr int STAGE = 2 * KB + 2 * QB;   // [K | V | Q | dO]
+  static constexpr int NS = 2;
+  static constexpr int DSB = 3 * 16384;           // dS^T chunks [c2 | c0 | c1]
+  static constexpr int NCR = 48;                  // carry rows (W - 1)
+  static constexpr int CARRY = NCR * 256;
+  static constexpr int NQA = 192;
+  static constexpr int ROWS = NS * 2 * NQA * 4;   // per stage: LSE*log2e [NQA], delta [NQA]
+  static constexpr int SMEM = 1024 + NS * STAGE + DSB + CARRY + ROWS + 512;
+  static constexpr int THREADS = 384;            // TMA, MMA, 2 x 4 WG warps, 2 row warps
+};
+
+__device__ __forceinline__ float dot8_bf16(uint4 a, uint4 b) {
+  const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 u = __bfloat1622float2(x[i]), v = __bfloat1622float2(y[i]);
+    s = fmaf(u.x, v.x, s);
+    s = fmaf(u.y, v.y, s);
+  }
+  return s;
+}
+// 64 fp32 of one row -> bf16 (x sc) -> 128 contiguous bytes in global memory
+__device__ __forceinline__ void store_row_bf16(bf16* dst, const float* v, float sc) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    d[c] = make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
+                      pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc));
+}
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
+  tc::tmem_ld_wait();
+}
+// carry row r (64 fp32) in smem, float4 s stored at slot s ^ (r & 15) (conflict-free row-per-thread)
+__device__ __forceinline__ float4* carry_at(float* carry, int r, int s) {
+  return reinterpret_cast<float4*>(carry + r * 64) + (s ^ (r & 15));
+}
+
+template <int CW>
+__global__ void __launch_bounds__(384, 1)
+    sa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                    const __grid_constant__ CUtensorMap tmO, TcArgs a) {
+  using C = FusCfg<CW>;
+  constexpr int NQ = C::NQ, NS = C::NS;
+  static_assert(NQ + 64 <= 256 && NQ >= 128 && 96 + CW <= NQ, "TMEM / window layout");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage0 = smem;                                   // [K | V | Q | dO] x NS
+  uint8_t* dsb = smem + NS * C::STAGE;                      // dS^T [c2 | c0 | c1]
+  float* carry = reinterpret_cast<float*>(dsb + C::DSB);    // dQ1 rows of the previous tile
+  float* rows = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(carry) + C::CARRY);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(rows) + C::ROWS);
+  uint64_t* full = bars;              // [NS]
+  uint64_t* empty = full + NS;        // [NS]
+  uint64_t* sfull = empty + NS;       // [2]
+  uint64_t* xfree = sfull + 2;        // [2] (128)
+  uint64_t* dpfull = xfree + 2;       // [2]
+  uint64_t* pdsfull = dpfull + 2;     // [2] (128)
+  uint64_t* kvfull = pdsfull + 2;     // [2]
+  uint64_t* kvfree = kvfull + 2;      // [2] (128)
+  uint64_t* dqfull = kvfree + 2;      // [2]
+  uint64_t* tfree = dqfull + 2;       // [2] (128) X_b drained (dQ read)
+  uint64_t* dsfree = tfree + 2;       // [2] dQ MMAs of tile k done (by tile parity): smem dS^T reusable
+  uint64_t* cfull = dsfree + 2;       // [1] (128) tile k's dQ epilogue done (carry written), tiles in order
+  uint64_t* rfull = cfull + 1;        // [NS] (64) LSE / delta rows of the stage's tile written
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + NS);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, R = a.R, W = a.L + a.R + 1;
+  const int nc = W - 1;                                     // carry rows
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int G = gridDim.x;
+  const int g_begin = (int)((long long)blockIdx.x * ntiles / G);
+  const int g_end = (int)((long long)(blockIdx.x + 1) * ntiles / G);
+  const int ntile_me = g_end - g_begin;
+  trace_cta(a.trace, 0);
+
+  // dS^T buffer starts (and, outside the rows' band strips, stays) zero
+  for (int i = tid; i < C::DSB / 16; i += blockDim.x) tc::st_shared_v4(tc::smem_u32(dsb) + 16 * i, make_uint4(0, 0, 0, 0));
+  tc::fence_proxy_async_smem();
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmO);
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
+      tc::mbar_init(&dqfull[i], 1); tc::mbar_init(&tfree[i], 128);
+    }
+    tc::mbar_init(&dsfree[0], 1); tc::mbar_init(&dsfree[1], 1);
+    tc::mbar_init(cfull, 128);
+    for (int i = 0; i < NS; ++i) tc::mbar_init(&rfull[i], 64);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t DV = tbase + NQ, DK = tbase + 256 + NQ;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = g_begin + k;
+        const int bh = g / ntq, u0 = (g % ntq) * kM;
+        const int st = k % NS;
+        uint8_t* b0 = stage0 + st * C::STAGE;
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        trace_at(a.trace, 0, k);
+        tc::mbar_expect_tx(&full[st], C::STAGE);
+        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - R, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - R, bh);
+        // warm L2 for tile k + NS (its stage is only free once tile k's dQ MMAs are done; the O rows
+        // are read by the row warps with plain loads)
+        if (a.qsplit && k + NS < ntile_me) {
+          const int g2 = g + NS, bh2 = g2 / ntq, v0 = (g2 % ntq) * kM;
+          tc::tma_prefetch_3d(&tmK, 0, v0, bh2);
+          tc::tma_prefetch_3d(&tmV, 0, v0, bh2);
+          tc::tma_prefetch_3d(&tmQ, 0, v0 - R, bh2);
+          tc::tma_prefetch_3d(&tmdO, 0, v0 - R, bh2);
+          tc::tma_prefetch_3d(&tmO, 0, v0 - R, bh2);
+        }
+        if (k == 0) tc::tma_prefetch_3d(&tmO, 0, u0 - R, bh);
+        if (k == 1 || (k == 0 && ntile_me > 1)) {
+          const int g1 = g_begin + 1, bh1 = g1 / ntq, v1 = (g1 % ntq) * kM;
+          if (k == 0) tc::tma_prefetch_3d(&tmO, 0, v1 - R, bh1);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(kM, NQ, 0, 0);
+      constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
+      constexpr uint32_t idQ = tc::idesc_bf16(kM, kD, 1, 1);
+      const int ks1 = (kM - W + 1) / 16;                    // first 16-key step that reaches window rows >= 128
+      const uint32_t dsc2 = tc::smem_u32(dsb), dsc0 = dsc2 + 16384;
+      int ns = 0, ndp = 0, nkv = 0;
+      while (nkv < ntile_me) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
+        const bool kv_ok = nkv < ndp && (m & 1) && (nkv < 1 || (m & 2));
+        const bool dp_ok = ndp < ns && (m & 4);
+        const bool s_ok = ns < ntile_me && (m & 8) &&
+                          (ns < 2 || tc::mbar_test(tc::smem_u32(&tfree[ns & 1]), ((ns - 2) >> 1) & 1));
+        // issue priority (a.mma_order): 0 = kv/dQ > dP > S, 1 = dP > S > kv/dQ, 2 = dP > kv/dQ > S
+        int pick = -1;
+        if (a.mma_order == 0) pick = kv_ok ? 0 : dp_ok ? 1 : s_ok ? 2 : -1;
+        else if (a.mma_order == 1) pick = dp_ok ? 1 : s_ok ? 2 : kv_ok ? 0 : -1;
+        else pick = dp_ok ? 1 : kv_ok ? 0 : s_ok ? 2 : -1;
+        if (pick == 0) {
+          tc::tc_fence_after();
+          const int b = nkv & 1, st = nkv % NS;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t kk = base, q = base + 2 * C::KB, dO = q + C::QB;
+#pragma unroll
+          for (int j = 0; j < NQ / 16; ++j)
+            tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO + 2048 * j), idG, j > 0);
+#pragma unroll
+          for (int j = 0; j < NQ / 16; ++j)
+            tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
+          tc::mma_commit(&kvfull[b]);
+          // dQ0 / dQ1 over X_b's first 128 columns (P^T / dS^T there were read by the MMAs above)
+#pragma unroll
+          for (int j = 0; j < kM / 16; ++j)
+            tc::mma_bf16(x, tc::sdesc(dsc0 + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(kk + 2048 * j), idQ,
+                         j > 0);
+          for (int j = ks1; j < kM / 16; ++j)
+            tc::mma_bf16(x + 64, tc::sdesc(dsc2 + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(kk + 2048 * j),
+                         idQ, j > ks1);
+          tc::mma_commit(&dqfull[b]);
+          tc::mma_commit(&dsfree[b]);
+          tc::mma_commit(&empty[st]);
+          ++nkv;
+        } else if (pick == 1) {
+          tc::tc_fence_after();
+          const int b = ndp & 1, st = ndp % NS;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&dpfull[b]);
+          ++ndp;
+        } else if (pick == 2) {
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
+          const uint32_t kk = base, q = base + 2 * C::KB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&sfull[b]);
+          ++ns;
+        }
+      }
+    }
+  } else if (warp < 10) {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const int c0 = 32 * q4;
+    const uint32_t dsu = tc::smem_u32(dsb);
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = g_begin + k;
+      const int bh = g / ntq, kt = g % ntq, u0 = kt * kM;
+      const int n0 = u0 - R;                         // frame of window row 0
+      const int b = wg, use = k >> 1, st = k % NS;
+      const bool tr = (tid == 64) || (tid == 192);
+      const float* lse2_s = rows + st * 2 * C::NQA;
+      const float* del_s = lse2_s + C::NQA;
+      tc::mbar_wait(&rfull[st], (k / NS) & 1);       // LSE / delta of the window rows (row warps)
+      if (tr) trace_at(a.trace, 1, k);
+      const uint32_t x = tbase + lanes + b * 256;
+      tc::mbar_wait(&sfull[b], use & 1);
+      if (tr) trace_at(a.trace, 2, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -lse2_s[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      tc::mbar_wait(&dpfull[b], use & 1);
+      if (tr) trace_at(a.trace, 3, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - del_s[c0 + 8 * j + e]);
+      }
+      tmem_write_row<CW, NQ>(x, q4, p);               // P^T  -> packed columns [0, NQ/2)
+      tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);     // dS^T -> packed columns [NQ/2, NQ)
+      // dS^T -> smem for the dQ MMAs, once the previous tile's dQ MMAs have read the buffer
+      if (k >= 1) tc::mbar_wait(&dsfree[(k - 1) & 1], ((k - 1) >> 1) & 1);
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        const int col8 = 4 * q4 + j, ch = col8 >> 3, s = col8 & 7;
+        const uint32_t addr = dsu + (ch == 2 ? 0 : (ch + 1) * 16384) + r * 128 + ((s ^ (r & 7)) << 4);
+        tc::st_shared_v4(addr, make_uint4(pack_bf16(ds[8 * j], ds[8 * j + 1]), pack_bf16(ds[8 * j + 2], ds[8 * j + 3]),
+                                          pack_bf16(ds[8 * j + 4], ds[8 * j + 5]), pack_bf16(ds[8 * j + 6], ds[8 * j + 7])));
+      }
+      tc::tmem_st_wait();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[b]);
+      if (tr) trace_at(a.trace, 4, k);
+      // dV / dK rows (lane r = key u0 + r)
+      tc::mbar_wait(&kvfull[b], use & 1);
+      if (tr) trace_at(a.trace, 5, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      {
+        float v[64];
+        const long long row = (long long)bh * T + u0 + r;
+        tmem_ld64(DV + lanes, v);
+        if (u0 + r < T) store_row_bf16(a.dV + row * kD, v, 1.f);
+        tmem_ld64(DK + lanes, v);
+        if (u0 + r < T) store_row_bf16(a.dK + row * kD, v, a.scale);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&kvfree[b]);
+      // dQ rows (lane r = window row r = frame n0 + r; dQ1 lane r = frame n0 + 128 + r)
+      tc::mbar_wait(&dqfull[b], use & 1);
+      if (tr) trace_at(a.trace, 6, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      const bool has_prev = kt > 0, prev_local = has_prev && k > 0;
+      const bool has_next = kt + 1 < ntq;
+      // tiles finish their dQ epilogues in order (cfull completes once per tile: the carry of
+      // tile k - 1 is written, and no arrivals of two tiles can mix in one phase)
+      if (k >= 1) tc::mbar_wait(cfull, (k - 1) & 1);
+      {
+        float v[64];
+        tmem_ld64(x, v);
+        const int n = n0 + r;
+        bool out = n >= 0 && n < T;
+        if (r < nc && has_prev) {
+          if (prev_local) {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+              const float4 c = *carry_at(carry, r, s);
+              v[4 * s] += c.x; v[4 * s + 1] += c.y; v[4 * s + 2] += c.z; v[4 * s + 3] += c.w;
+            }
+          } else {   // first tile of this CTA: the partial goes to the CTA owning key tile kt - 1
+            float4* dst = reinterpret_cast<float4*>(a.ws_hand + ((long long)blockIdx.x * C::NCR + r) * kD);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) dst[s] = make_float4(v[4 * s], v[4 * s + 1], v[4 * s + 2], v[4 * s + 3]);
+            out = false;
+          }
+        }
+        if (out) store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
+      }
+      if (q4 * 32 < nc) {                              // warp-uniform: warps holding carry rows
+        float v[64];
+        tmem_ld64(x + 64, v);
+        if (r < nc) {
+          if (!has_next) {                             // last key tile: these rows are complete
+            const int n = n0 + kM + r;
+            if (n < T) store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
+          } else {                                     // carry for the next tile (here or in the next CTA)
+#pragma unroll
+            for (int s = 0; s < 16; ++s) *carry_at(carry, r, s) = make_float4(v[4 * s], v[4 * s + 1], v[4 * s + 2], v[4 * s + 3]);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+      tc::mbar_arrive(cfull);
+      if (tr) trace_at(a.trace, 7, k);
+    }
+  } else {
+    // row warps 10, 11: LSE*log2e and delta_n = dO_n . O_n of each tile's NQ window rows into the
+    // stage's row arrays.  The O loads do not depend on the stage, so they are issued before the
+    // stage lands (latency overlapped with the TMA); dO comes from the landed stage.
+    const int dl = tid - 320;
+    for (int k = 0; k < ntile_me; ++k) {
+      const int g = g_begin + k;
+      const int bh = g / ntq, u0 = (g % ntq) * kM, n0 = u0 - R, st = k % NS;
+      uint4 ov[3][8];
+      float l2[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int w = dl + 64 * i, n = n0 + w;
+        l2[i] = 0.f;
+        if (w < NQ && n >= 0 && n < T) {
+          const uint4* orow = reinterpret_cast<const uint4*>(a.Og + ((long long)bh * T + n) * kD);
+#pragma unroll
+          for (int s = 0; s < 8; ++s) ov[i][s] = __ldg(orow + s);
+          l2[i] = a.LSEin[(long long)bh * T + n] * kLog2e;
+        } else {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) ov[i][s] = make_uint4(0, 0, 0, 0);
+        }
+      }
+      tc::mbar_wait(&full[st], (k / NS) & 1);
+      float* lse2_s = rows + st * 2 * C::NQA;
+      float* del_s = lse2_s + C::NQA;
+      const uint32_t dOs = tc::smem_u32(stage0 + st * C::STAGE + 2 * C::KB + C::QB);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int w = dl + 64 * i;
+        if (w < NQ) {
+          float de = 0.f;
+#pragma unroll
+          for (int s = 0; s < 8; ++s) de += dot8_bf16(ov[i][s], tc::ld_shared_v4(dOs + w * 128 + ((s ^ (w & 7)) << 4)));
+          lse2_s[w] = l2[i];
+          del_s[w] = de;
+        }
+      }
+      tc::mbar_arrive(&rfull[st]);
+    }
+  }
+  // hand-off between neighbouring CTAs' tiles of one head (see above)
+  if (a.trace && tid == 64 && blockIdx.x == 0) a.trace[8 * 64] = clock64();
+  __threadfence();
+  cg::this_grid().sync();
+  if (ntile_me > 0) {
+    const int kl = ntile_me - 1;                       // last tile of this CTA
+    const int g = g_begin + kl;
+    const int bh = g / ntq, kt = g % ntq;
+    if (kt + 1 < ntq && warp >= 2 && ((warp - 2) >> 2) == (kl & 1)) {
+      const int r = 32 * (warp & 3) + lane;
+      const int n = kt * kM + kM - R + r;
+      if (r < nc && n < T) {
+        const float4* src = reinterpret_cast<const float4*>(a.ws_hand + ((long long)(blockIdx.x + 1) * C::NCR + r) * kD);
+        float v[64];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+          const float4 c = *carry_at(carry, r, s), o = __ldcg(src + s);
+          v[4 * s] = c.x + o.x; v[4 * s + 1] = c.y + o.y; v[4 * s + 2] = c.z + o.z; v[4 * s + 3] = c.w + o.w;
+        }
+        store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+  trace_cta(a.trace, 1);
+}
+
 static_assert(DqCfg<72>::STAGE % 1024 == 0 && DkvCfg<72>::STAGE % 1024 == 0 && FwdCfg<72>::STAGE % 1024 == 0,
               "smem stages must be 1024-byte aligned");
 
@@ -1232,8 +1670,54 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   return SATTN_OK;
 }
 
+size_t fused_ws_bytes() { return (size_t)num_sms() * FusCfg<72>::NCR * kD * sizeof(float); }
+
+// SA backward variant: the two-kernel K1 + K2 path (default; faster on B200 as measured)
+// or, with SATTN_SA_BWD=fused, the single-pass key-major sweep (sa_bwd_fused_tc).  Read per call.
+bool sa_bwd_split() {
+  const char* e = getenv("SATTN_SA_BWD");
+  return !(e && !strcmp(e, "fused"));
+}
+
+template <int CW>
+sattn_status bwd_fused_launch(const AttnArgs& a, cudaStream_t st) {
+  using C = FusCfg<CW>;
+  CUtensorMap mk, mv, mq, mdo, mo;
+  if (!make_map(&mk, a.K, a.T, a.BH, kM) || !make_map(&mv, a.V, a.T, a.BH, kM) ||
+      !make_map(&mq, a.Q, a.T, a.BH, C::NQ) || !make_map(&mdo, a.dO, a.T, a.BH, C::NQ) ||
+      !make_map(&mo, a.O, a.T, a.BH, C::NQ))
+    return SATTN_ECUDA;
+  TcArgs t = tc_args(a);
+  t.ws_hand = a.delta;
+  if (const char* e = getenv("SATTN_FUSED_ORDER")) t.mma_order = atoi(e);
+  t.qsplit = 1;   // fused: L2 prefetch of tile k + 2 (SATTN_FUSED_PREFETCH=0 disables)
+  if (const char* e = getenv("SATTN_FUSED_PREFETCH")) t.qsplit = atoi(e);
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  cudaFuncSetAttribute(sa_bwd_fused_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;   // grid-wide barrier for the CTA-boundary dQ rows
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, sa_bwd_fused_tc<CW>, mk, mv, mq, mdo, mo, t);
+  if (e != cudaSuccess) {
+    g_tc_err = std::string("fused backward launch: ") + cudaGetErrorString(e);
+    return SATTN_ECUDA;
+  }
+  return SATTN_OK;
+}
+
 template <int CW>
 sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
+  if (!sa_bwd_split()) return bwd_fused_launch<CW>(a, st);
   constexpr int NK = nk_of(CW);
   const int Tp = (a.T + 3) & ~3;
   const float* l2ws = a.delta + (long long)a.BH * Tp;
@@ -1378,7 +1862,8 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-int tc_backward_launches() { return 2; }
+int tc_backward_launches() { return sa_bwd_split() ? 2 : 1; }
+size_t tc_backward_ws_bytes() { return fused_ws_bytes(); }
 
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {
   // band width L+1 on the SA kernels (CW <= 80), staircase staging of 16 + 2R frames x C channels

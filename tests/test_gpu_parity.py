@@ -187,3 +187,44 @@ def test_sa_locality_exact_zero_fwd_and_bwd(dt):
     changed = (dv2 != dv).any(-1).any(0).any(0).cpu().numpy()
     expect = np.array([u - R <= sf <= u + L for u in range(shape[2])])
     assert not changed[~expect].any()
+
+
+# The single-pass key-major backward (SATTN_SA_BWD=fused, sa_bwd_fused_tc): a CTA sweeps a
+# contiguous range of key tiles; dQ rows near tile and CTA boundaries combine two partial sums
+# (a carry in smem, or a workspace hand-off across a grid barrier).  Same gates as the default.
+FUSED = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16),
+         ((1, 3, 777, 64), 32, 8), ((1, 1, 130, 64), 8, 40), ((3, 2, 300, 64), 24, 0)]
+
+
+@pytest.mark.parametrize("shape,L,R", FUSED)
+def test_sa_bf16_fused_backward(shape, L, R, monkeypatch):
+    monkeypatch.setenv("SATTN_SA_BWD", "fused")
+    s = sattn()
+    q, k, v = synth.qkv(5, shape, "bf16")
+    do = synth.grad_out(5, shape, "bf16")
+    tq, tk, tv, tdo = (dev(x, "bf16") for x in (q, k, v, do))
+    o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
+    dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
+    G = oracle.sa.sa_backward(q, k, v, do, L, R)
+    for name, got, ref in (("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
+        assert excess(got, ref, "bf16") <= 0, (name, maxerr(got, ref))
+    # run-to-run bitwise
+    dq2, dk2, dv2 = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+
+
+def test_sa_fused_backward_full_shape_cta_boundaries(monkeypatch):
+    # B=8, H=12, T=1750: 1344 key tiles over the grid, so CTA ranges start and end inside heads;
+    # check every head in full against the oracle (dQ rows at hand-offs included)
+    monkeypatch.setenv("SATTN_SA_BWD", "fused")
+    s = sattn()
+    B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
+    g = torch.Generator("cuda").manual_seed(11)
+    tq, tk, tv, tdo = (torch.randn(B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
+    dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
+    for (b, h) in ((0, 0), (0, 1), (2, 5), (4, 9), (7, 11)):
+        q, k, v, do = (host(x[b, h]) for x in (tq, tk, tv, tdo))
+        G = oracle.sa.sa_backward(q, k, v, do, L, R)
+        for name, got, ref in (("dQ", dq[b, h], G[0]), ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
+            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
