@@ -59,6 +59,8 @@ struct TcArgs {
   bf16* dQ; bf16* dK; bf16* dV; float* delta;    // bwd outputs
   long long* trace;                              // optional per-phase clock64 trace of CTA 0 (debug)
   int qsplit, ksplit;                            // forward TMA box splits (tuning)
+  int ksplit_pf;                                 // forward L2 prefetch distance (tiles)
+  int mma_sleep;                                 // backward MMA issuers: ns to sleep when nothing is ready
   int kshift;                                    // keys of query t are frames [t-L-kshift, t+R-kshift]
                                                  // (0 for SA; R-c for LLSA channel c's band, with R := 0)
   float* ws_del; float* ws_l2;                   // padded [BH][Tp] delta / LSE*log2e rows (K1 -> K2)
@@ -232,13 +234,14 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_prefetch_3d(&tmK, 0, t0 - a.L, bh);
         tc::tma_prefetch_3d(&tmV, 0, t0 - a.L, bh);
       };
-      for (int k = NQK; k < 2 * NQK; ++k) prefetch(k);
+      const int pfd = a.ksplit_pf;                 // L2 prefetch distance in tiles (0: none)
+      for (int k = NQK; k < NQK + pfd; ++k) prefetch(k);
       for (int k = 0; k < ntile_me; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, t0 = (g % ntq) * kM;
         const int st = k % NQK;
         if (k >= NQK) tc::mbar_wait(&empty[st], ((k - NQK) / NQK) & 1);
-        if (k >= NQK) prefetch(k + NQK);
+        if (k >= NQK && pfd) prefetch(k + pfd);
         uint8_t* sQ = qk0 + st * C::QKB;
         trace_at(a.trace, 0, k);
         tc::mbar_expect_tx(&full[st], C::QKB);
@@ -495,7 +498,9 @@ __global__ void __launch_bounds__(320, 1)
                          j > 0);
           tc::mma_commit(&sfull[b]);
           ++ns;
+          continue;
         }
+        if (a.mma_sleep) __nanosleep(a.mma_sleep);   // nothing ready: leave the issue slots to the WGs
       }
     }
   } else {
@@ -754,7 +759,9 @@ __global__ void __launch_bounds__(320, 1)
                          j > 0);
           tc::mma_commit(&sfull[b]);
           ++ns;
+          continue;
         }
+        if (a.mma_sleep) __nanosleep(a.mma_sleep);   // nothing ready: leave the issue slots to the WGs
       }
     }
   } else {
@@ -1535,6 +1542,13 @@ EncodeTiledFn encoder() {
 }
 
 // [BH][T][64] bf16 viewed as a 3-D tensor (64, T, BH); box (64, rows, 1), 128B swizzle.
+CUtensorMapL2promotion l2_promo() {   // SATTN_L2_PROMO = 0 (none) / 64 / 128 / 256 (default) bytes
+  const char* e = getenv("SATTN_L2_PROMO");
+  const int v = e ? atoi(e) : 256;
+  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
   EncodeTiledFn enc = encoder();
   if (!enc) {
@@ -1546,7 +1560,7 @@ bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
   cuuint32_t box[3] = {64, (cuuint32_t)rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
@@ -1625,6 +1639,7 @@ int cw_of(int W) {
 
 TcArgs tc_args(const AttnArgs& a) {
   TcArgs t{};
+  if (const char* e = getenv("SATTN_MMA_SLEEP")) t.mma_sleep = atoi(e);
   t.T = a.T; t.L = a.L; t.R = a.R; t.BH = a.BH;
   t.scale = a.scale; t.scale_log2 = a.scale_log2;
   t.O = reinterpret_cast<bf16*>(a.Out); t.LSE = a.LSEout;
@@ -1658,6 +1673,8 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   TcArgs ta = tc_args(a);
   if (const char* e = getenv("SATTN_FWD_QSPLIT")) ta.qsplit = atoi(e);
   if (const char* e = getenv("SATTN_FWD_KSPLIT")) ta.ksplit = atoi(e);
+  ta.ksplit_pf = 0;   // L2 prefetch of later tiles measured slower (18.7 vs 22.6 us, gpurun_out/diag8)
+  if (const char* e = getenv("SATTN_FWD_PF")) ta.ksplit_pf = atoi(e);
   if (kM % ta.qsplit || (kM / ta.qsplit) % 8 || C::NK % ta.ksplit || (C::NK / ta.ksplit) % 8) ta.qsplit = ta.ksplit = 1;
   CUtensorMap mq, mk, mv, mo;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM / ta.qsplit) || !make_map(&mk, a.K, a.T, a.BH, C::NK / ta.ksplit) ||
