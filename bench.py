@@ -265,6 +265,11 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
 
+    hour = None
+    if not args.no_hour:
+        torch.cuda.empty_cache()
+        hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
+
     stream_lat = None
     if not args.no_stream:
         stream_lat = run_stream(sattn, dev)
@@ -286,7 +291,7 @@ def run_gpu(args):
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
            "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa,
-           "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
+           "hour": hour, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
 
@@ -337,6 +342,67 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
     return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
             "channels": C, "hbm_frac": round(bytes_step / (ms / 1e3) / 1e9 / hbm, 4), "steps": k,
             "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
+
+
+def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
+    """BASELINE configs[4]: one hour-long stream (B=1, H=12, T=180,000 frames = 1 h at 50 Hz),
+    12 layers x (SA fwd + SA bwd), bf16, time-sharded over the ranks: rank r owns
+    frames [r T/N, (r+1) T/N) and every call exchanges the L+R boundary frames with its two
+    neighbours (tshard: NCCL point-to-point over NVLink), so the whole-job rate counts each frame
+    once.  At N = 1 the calls run on the whole sequence with no exchange."""
+    import torch
+    import torch.distributed as dist
+    from paper_2302_13451_b200 import tshard
+    Th, Bh, n_layers = 180_000, 1, NL
+    t0, t1 = tshard.shard_bounds(Th, world, rank, 128)
+    shp = (Bh, H, t1 - t0, D)
+    Q, K, V, dO = ([rnd(*shp) for _ in range(n_layers)] for _ in range(4))
+    O, LSE = [None] * n_layers, [None] * n_layers
+    ws = [None]
+
+    def fwd(l):
+        if world == 1:
+            O[l], LSE[l] = sattn.sa_forward(Q[l], K[l], V[l], L, R)
+        else:
+            O[l], LSE[l] = tshard.sa_forward_tsharded(Q[l], K[l], V[l], L, R)
+
+    def bwd(l):
+        if world == 1:
+            return sattn.sa_backward(Q[l], K[l], V[l], O[l], LSE[l], dO[l], L, R, ws=ws[0])
+        return tshard.sa_backward_tsharded(Q[l], K[l], V[l], O[l], LSE[l], dO[l], L, R)
+
+    import ctypes
+    ws[0] = torch.empty(sattn.lib().sa_backward_workspace(ctypes.byref(sattn.make_desc(Bh, H, t1 - t0, D, L, R,
+                                                                                        sattn.BF16))),
+                        device=dev, dtype=torch.uint8)
+
+    def step():
+        for l in range(n_layers):
+            fwd(l)
+        for l in reversed(range(n_layers)):
+            bwd(l)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        step()
+    barrier()
+    k = max(1, min(args.steps, 3))
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(k):
+        step()
+    a1.record(stream)
+    barrier()
+    ms = a0.elapsed_time(a1) / k
+    if world > 1:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    bytes_step = (FWD_BYTES + BWD_BYTES) * Bh * H * Th * n_layers
+    return {"value": round(Bh * Th / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": k,
+            "hbm_frac": round(bytes_step / world / (ms / 1e3) / 1e9 / hbm, 4),
+            "workload": f"hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), {n_layers} layers x (SA fwd + bwd), "
+                        f"time-sharded x{world} (halo exchange {'NCCL P2P' if world > 1 else 'none'}), eager calls",
+            "frames_per_rank": t1 - t0}
 
 
 def run_stream(sattn, dev, n_steps=2000, warm=200):
@@ -487,6 +553,7 @@ def main():
     ap.add_argument("--no-llsa", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
+    ap.add_argument("--no-hour", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
