@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idO = tc::idesc_bf16(128, kD, 0, 1);
       const int nstair = 2 * R;                           // 16-row k-steps over the stair V blocks
       int ns = 0, np = 0;
+      int kts = 0, nsi = 0;                               // ns / NI, ns % NI (no division in the poll loop)
       while (np < nitems) {
-        const int kts = ns / NI;
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&hfull[kts & 1]), (kts >> 1) & 1,
                                           tc::smem_u32(&qfull[ns % Cf::NSQ]), (ns / Cf::NSQ) & 1,
                                           tc::smem_u32(&pfull[np & 1]), (np >> 1) & 1,
@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(320, 1)
               tc::mma_bf16(d, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kb + 32 * j), idS, j > 0);
             tc::mma_commit(&sfull[ns & 1]);
             ++ns;
+            if (++nsi == NI) { nsi = 0; ++kts; }
             continue;
           }
         }
@@ -205,37 +206,36 @@ __global__ void __launch_bounds__(320, 1)
       // ---- stair scores on CUDA cores: q_{t,c} . k_{h-c', c'} (row i of stair tile c')
       float sst[kRmax];
       {
-        float q[kD];
+        // q as fp32 pairs; k_stair rows unpacked with shifts (bf16 -> fp32 is a 16-bit shift)
+        // and accumulated with packed fp32x2 FMAs (sm_100 FFMA2): the dot products are the
+        // WG's largest instruction block (ncu: ~1/3 of the kernel's instructions before)
+        float2 q2[kD / 2];
         const uint32_t qrow = tc::smem_u32(qstage0 + qs * Cf::QB) + r * 128;
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
           const uint4 x = tc::ld_shared_v4(qrow + ((ch ^ (r & 7)) << 4));
-          const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+          const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(hx[e]);
-            q[8 * ch + 2 * e] = f.x;
-            q[8 * ch + 2 * e + 1] = f.y;
-          }
+          for (int e = 0; e < 4; ++e)
+            q2[4 * ch + e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
         }
 #pragma unroll
         for (int cp = 0; cp < kRmax; ++cp) {
-          float acc = 0.f;
+          float2 acc = make_float2(0.f, 0.f);
           if (cp < R) {
             const uint32_t krow = tc::smem_u32(hb + 2 * Cf::BB + cp * Cf::SB) + i * 128;
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {
               const uint4 x = tc::ld_shared_v4(krow + ((ch ^ (i & 7)) << 4));
-              const __nv_bfloat162* hx = reinterpret_cast<const __nv_bfloat162*>(&x);
+              const uint32_t w[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(hx[e]);
-                acc = fmaf(q[8 * ch + 2 * e], f.x, fmaf(q[8 * ch + 2 * e + 1], f.y, acc));
-              }
+              for (int e = 0; e < 4; ++e)
+                acc = __ffma2_rn(q2[4 * ch + e],
+                                 make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u)), acc);
             }
           }
           const int f = h - cp;                           // stair key frame
-          sst[cp] = (cp < R && f >= 0 && f < T) ? acc : neg_inf();
+          sst[cp] = (cp < R && f >= 0 && f < T) ? acc.x + acc.y : neg_inf();
         }
       }
       // ---- band strip from TMEM + joint softmax
@@ -248,12 +248,11 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < NB / 8; ++j) tc::tmem_ld8(pa + 8 * j, s + 8 * j);
       tc::tmem_ld_wait();
       const int key0 = h0 - R - L;                       // frame of band column 0
+      const int jlo = max(i, -key0), jhi = min(i + L, T - 1 - key0);   // valid band columns [jlo, jhi]
       float m = neg_inf();
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const int f = key0 + j;
-        const bool v = j >= i && j <= i + L && f >= 0 && f < T;
-        s[j] = v ? s[j] : neg_inf();
+        s[j] = (j >= jlo && j <= jhi) ? s[j] : neg_inf();
         m = fmaxf(m, s[j]);
       }
 #pragma unroll

@@ -23,8 +23,23 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps until the phase completes (or
+// the hint expires) instead of re-polling every few hundred cycles; the re-poll loops of
+// waiting warps otherwise take issue slots from the working warps of the same SM sub-partition.
+#ifndef SATTN_WAIT_HINT_NS
+#define SATTN_WAIT_HINT_NS 200000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
   uint32_t ok;
+#if SATTN_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(phase), "r"((uint32_t)SATTN_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
@@ -32,6 +47,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t phase) {
       : "=r"(ok)
       : "r"(a), "r"(phase)
       : "memory");
+#endif
   return ok != 0;
 }
 // Non-blocking probe (mbarrier.test_wait): for the out-of-order polling loops of the MMA
