@@ -222,6 +222,10 @@ def run_gpu(args):
                 "step_hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * NL / (ms_per_step / 1e3) / 1e9 / hbm, 4)}
 
     # ---------------- e2e through the public API with host buffers (pinned), H2D + D2H inside
+    # Every step copies its inputs (all layers' Q, K, V, dO) from pinned host memory and reads
+    # its results (dQ, dK, dV) back.  The copies are layer-granular on two copy streams
+    # (PCIe is full duplex: the H2D of step i+1 overlaps the D2H of step i) and the compute
+    # stream waits per layer on events, so each layer starts as soon as its own inputs landed.
     e2e = None
     if not args.no_e2e:
         hin = [[torch.empty(shp, dtype=bf, pin_memory=True) for _ in range(4)] for _ in range(NL)]
@@ -229,23 +233,54 @@ def run_gpu(args):
         for l in range(NL):
             for j, src in enumerate((Qs, Ks, Vs, dOs)):
                 hin[l][j].copy_(src[l])
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        # two device buffer sets, alternating by step: the H2D of step i+1 need not wait for
+        # step i's compute to release its inputs
+        sets = [(Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs),
+                tuple([torch.empty_like(t) for t in ts] for ts in (Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs))]
+        used = [[None] * NL for _ in range(2)]      # compute finished reading set p, layer l
+        drained = [[None] * NL for _ in range(2)]   # D2H of set p, layer l finished
+        par = [0]
 
         def e2e_step():
+            p_ = par[0]; par[0] ^= 1
+            q_, k_, v_, do_, o_, lse_, dq_, dk_, dv_ = sets[p_]
+            landed = []
             for l in range(NL):
-                for j, dst in enumerate((Qs, Ks, Vs, dOs)):
-                    dst[l].copy_(hin[l][j], non_blocking=True)
-            gF.replay(); gB.replay()
+                with torch.cuda.stream(s_in):
+                    if used[p_][l] is not None:
+                        s_in.wait_event(used[p_][l])
+                    for j, dst in enumerate((q_, k_, v_, do_)):
+                        dst[l].copy_(hin[l][j], non_blocking=True)
+                    e = ev(); e.record(s_in); landed.append(e)
+            spp = ctypes.c_void_p(stream.cuda_stream)
             for l in range(NL):
-                for j, src in enumerate((dQs, dKs, dVs)):
-                    hout[l][j].copy_(src[l], non_blocking=True)
+                stream.wait_event(landed[l])
+                check(lib.sa_forward(pd, P(q_[l]), P(k_[l]), P(v_[l]), P(o_[l]), P(lse_[l]), spp), "sa_forward")
+            for l in reversed(range(NL)):
+                if drained[p_][l] is not None:
+                    stream.wait_event(drained[p_][l])
+                check(lib.sa_backward(pd, P(q_[l]), P(k_[l]), P(v_[l]), P(o_[l]), P(lse_[l]), P(do_[l]),
+                                      P(dq_[l]), P(dk_[l]), P(dv_[l]), P(ws), nws, spp), "sa_backward")
+                e = ev(); e.record(stream); used[p_][l] = e
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(e)
+                    for j, src in enumerate((dq_, dk_, dv_)):
+                        hout[l][j].copy_(src[l], non_blocking=True)
+                    d = ev(); d.record(s_out); drained[p_][l] = d
 
         e2e_step()
+        torch.cuda.synchronize()
         barrier()
-        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
         n_e2e = max(2, min(args.steps, 5))
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
         a0.record(stream)
+        s_in.wait_event(a0)          # the first copies start after the start event
         for _ in range(n_e2e):
             e2e_step()
+        for d in drained[0] + drained[1]:   # the end event follows every copy of the last steps
+            stream.wait_event(d)
         a1.record(stream)
         barrier()
         e_ms = a0.elapsed_time(a1)
@@ -255,8 +290,10 @@ def run_gpu(args):
             e_ms = float(tt.item())
         el = 2 * B * H * T * D
         e2e = {"value": round(world * B * T * n_e2e / (e_ms / 1e3), 1), "unit": UNIT,
-               "h2d_bytes_per_step": 4 * NL * el, "d2h_bytes_per_step": 3 * NL * el, "steps": n_e2e}
-        del hin, hout
+               "h2d_bytes_per_step": 4 * NL * el, "d2h_bytes_per_step": 3 * NL * el, "steps": n_e2e,
+               "pipeline": "layer-granular H2D / compute / D2H on three streams (CUDA events), two device "
+                           "buffer sets alternating by step"}
+        del hin, hout, sets
 
     # ---------------- LLSA step (same shape, C = R+1 channels), reported alongside
     llsa = None
