@@ -430,7 +430,12 @@ sattn_status stream_launch(sattn_stream* s, const void* x, void* y, long long h,
   a.R = s->d.R;
   a.BH = (int)(s->d.B * s->d.H);
   a.scale_log2 = eff_scale(&s->d) * kLog2e;
-  const size_t smem = stream_smem_bytes((int)s->d.D, a.L, a.R);
+  size_t smem = stream_smem_bytes((int)s->d.D, a.L, a.R, a.n_layers, elem_size(s->d.dtype));
+  a.preload = 1;
+  if (smem > 160 * 1024) {   // rings too large to stage: each layer reads its ring rows from global memory
+    a.preload = 0;
+    smem = stream_smem_bytes((int)s->d.D, a.L, a.R);
+  }
   if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
   return dispatch(s->d.D, s->d.dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
     constexpr int D = decltype(dc)::value;

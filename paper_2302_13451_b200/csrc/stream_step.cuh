@@ -23,8 +23,14 @@ struct StreamArgs {
   long long h, last;   // horizon and last valid frame
   int n_layers, L, R, BH;
   float scale_log2;
+  int preload;         // 1: every layer's ring rows are staged into shared memory at the start
 };
 
+// Latency structure: the layers of a step are sequential, so the step costs n_layers x (one
+// layer's dependent phases).  Everything a layer reads that is known at launch — the ring rows
+// of every layer (frames h-R-L .. h-R-1, written by earlier steps) and their slot indices — is
+// fetched once, up front, in parallel; a layer then touches only shared memory, and writes its
+// one new ring row back without waiting.
 template <int D, typename T>
 __global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
   constexpr int SD = D + 1;
@@ -35,32 +41,65 @@ __global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
   float* diag = win + W * SD;         // [C][SD]
   float* ndiag = diag + C * SD;       // [C][SD]
   float* P = ndiag + C * SD;          // [C][W]
+  int* slot = reinterpret_cast<int*>(P + C * W);   // [W] ring slot of window row i < L, -1 if invalid
+  int* rslot = slot + W;                             // [C] raw slot of frame h - c', -1 if invalid
+  T* rings = reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(rslot + C + 3) & ~uintptr_t(15));  // [n_layers][L][D]
   const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const long long h = a.h, last = a.last;
   T* raw = reinterpret_cast<T*>(a.raw) + (long long)bh * C * D;
 
+  // slot indices (the only 64-bit modulo work of the step)
+  for (int i = tid; i < W; i += nt) {
+    const long long u = h - R - L + i;
+    slot[i] = (i < L && u >= 0 && u <= last) ? (int)(u % L) : -1;
+  }
+  for (int cp = tid; cp < C; cp += nt) {
+    const long long f = h - cp;
+    rslot[cp] = (f >= 0 && f <= last) ? (int)(f % C) : -1;
+  }
   // layer-1 diagonal: X_0(h - c', c') = x_{h - c'}
   if (a.x_new) {
     const T* x = reinterpret_cast<const T*>(a.x_new) + (long long)bh * D;
-    for (int d = tid; d < D; d += nt) raw[(h % C) * D + d] = x[d];
+    const int sx = (int)(h % C);
+    for (int d = tid; d < D; d += nt) raw[sx * D + d] = x[d];
   }
   __syncthreads();
+  if (a.preload && L > 0) {
+    // every layer's ring rows, in parallel (16-byte copies when rows are 16-byte multiples)
+    constexpr bool VEC = (D * sizeof(T)) % 16 == 0;
+    constexpr int PER = VEC ? (int)(D * sizeof(T) / 16) : D;   // chunks (or elements) per row
+    const int n = a.n_layers * L * PER;
+    for (int idx = tid; idx < n; idx += nt) {
+      const int ch = idx % PER, i = (idx / PER) % L, l = idx / (PER * L);
+      const int sl = slot[i];
+      const T* src = reinterpret_cast<const T*>(a.ring) + (((long long)l * a.BH + bh) * L + (sl < 0 ? 0 : sl)) * D;
+      T* dst = rings + ((long long)l * L + i) * D;
+      if (VEC) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (sl >= 0) v = reinterpret_cast<const uint4*>(src)[ch];
+        reinterpret_cast<uint4*>(dst)[ch] = v;
+      } else {
+        dst[ch] = sl >= 0 ? src[ch] : from_f<T>(0.f);
+      }
+    }
+  }
   for (int idx = tid; idx < C * D; idx += nt) {
     const int cp = idx / D, d = idx % D;
-    const long long f = h - cp;
-    diag[cp * SD + d] = (f >= 0 && f <= last) ? to_f(raw[(f % C) * D + d]) : 0.f;
+    diag[cp * SD + d] = rslot[cp] >= 0 ? to_f(raw[rslot[cp] * D + d]) : 0.f;
   }
   __syncthreads();
+  const int wslot = (h - R >= 0 && h - R <= last && L > 0) ? (int)((h - R) % L) : -1;
 
   for (int l = 0; l < a.n_layers; ++l) {
     T* ring = L > 0 ? reinterpret_cast<T*>(a.ring) + ((long long)l * a.BH + bh) * L * D : nullptr;
+    const T* lring = rings + (long long)l * L * D;
     // window rows (tied K = V)
     for (int idx = tid; idx < W * D; idx += nt) {
       const int i = idx / D, d = idx % D;
       const long long u = h - R - L + i;
       float x = 0.f;
       if (u >= 0 && u <= last) {
-        if (i < L) x = to_f(ring[(u % L) * D + d]);
+        if (i < L) x = a.preload ? to_f(lring[i * D + d]) : to_f(ring[slot[i] * D + d]);
         else if (i == L) x = diag[R * SD + d];
         else x = diag[(L + R - i) * SD + d];
       }
@@ -73,10 +112,11 @@ __global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
       const long long u = h - R - L + i, t = h - c;
       float s = neg_inf();
       if (u >= 0 && u <= last && t >= 0 && t <= last) {
-        float acc = 0.f;
+        // four independent partial sums: the dependent FMA chain was the step's longest latency
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 16
-        for (int d = 0; d < D; ++d) acc = fmaf(diag[c * SD + d], win[i * SD + d], acc);
-        s = acc * a.scale_log2;
+        for (int d = 0; d < D; ++d) acc[d & 3] = fmaf(diag[c * SD + d], win[i * SD + d], acc[d & 3]);
+        s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale_log2;
       }
       P[c * W + i] = s;
     }
@@ -103,15 +143,17 @@ __global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
     // values, block rule, rounding as the offline stack stores them
     for (int idx = tid; idx < C * D; idx += nt) {
       const int c = idx / D, d = idx % D;
-      float y = 0.f;
-      for (int i = 0; i < W; ++i) y = fmaf(P[c * W + i], win[i * SD + d], y);
+      float y4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+      for (int i = 0; i < W; ++i) y4[i & 3] = fmaf(P[c * W + i], win[i * SD + d], y4[i & 3]);
+      const float y = (y4[0] + y4[1]) + (y4[2] + y4[3]);
       const float o = to_f(from_f<T>(y));
       ndiag[c * SD + d] = to_f(from_f<T>(0.5f * (diag[c * SD + d] + o)));
     }
     __syncthreads();
     // X_l(h-R, R) joins this layer's ring (after every read of the ring above)
-    if (L > 0 && h - R >= 0 && h - R <= last)
-      for (int d = tid; d < D; d += nt) ring[((h - R) % L) * D + d] = from_f<T>(diag[R * SD + d]);
+    if (wslot >= 0)
+      for (int d = tid; d < D; d += nt) ring[wslot * D + d] = from_f<T>(diag[R * SD + d]);
     for (int idx = tid; idx < C * D; idx += nt) diag[(idx / D) * SD + idx % D] = ndiag[(idx / D) * SD + idx % D];
     __syncthreads();
   }
@@ -121,9 +163,11 @@ __global__ void __launch_bounds__(256) llsa_stream_step_kernel(StreamArgs a) {
   }
 }
 
-inline size_t stream_smem_bytes(int D, int L, int R) {
+// shared memory of the step kernel: working set, plus (preload) every layer's ring rows
+inline size_t stream_smem_bytes(int D, int L, int R, int n_layers = 0, size_t elem = 4) {
   const int C = R + 1, W = L + R + 1, SD = D + 1;
-  return sizeof(float) * ((size_t)W * SD + 2 * (size_t)C * SD + (size_t)C * W);
+  const size_t base = sizeof(float) * ((size_t)W * SD + 2 * (size_t)C * SD + (size_t)C * W) + sizeof(int) * (W + C) + 32;
+  return base + (size_t)n_layers * L * D * elem;
 }
 
 }  // namespace sattn
