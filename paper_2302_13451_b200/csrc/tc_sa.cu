@@ -366,6 +366,31 @@ __global__ void __launch_bounds__(320, 1)
   trace_cta(a.trace, 1);
 }
 
+__device__ __forceinline__ float dot8_bf16(uint4 a, uint4 b) {
+  const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
+  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&b);
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 u = __bfloat1622float2(x[i]), v = __bfloat1622float2(y[i]);
+    s = fmaf(u.x, v.x, s);
+    s = fmaf(u.y, v.y, s);
+  }
+  return s;
+}
+// 64 fp32 of one row -> bf16 (x sc) -> 128 contiguous bytes in global memory
+__device__ __forceinline__ void store_row_bf16(bf16* dst, const float* v, float sc) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    d[c] = make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
+                      pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc));
+}
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
+  tc::tmem_ld_wait();
+}
 // ------------------------------------------------------------------------------------------
 // backward K1 (query-major): delta_t = sum_u P_tu dP_tu, dQ_t = scale * sum_u dS_tu K_u.
 // Persistent, warp-specialised like the forward.  Per tile (128 queries, TMEM buffer b):
@@ -844,6 +869,339 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// backward K2, block-ring variant (SATTN_K2=ring): the key-major kernel above with its query window
+// staged as 128-row blocks.  A CTA sweeps a contiguous range of key tiles, so consecutive
+// tiles' windows [u0 - R, u0 - R + NQ) share a block: each tile loads one new Q block and one
+// dO block (not the NQ-row windows), and a 3-slot block ring holds the current tile's two
+// blocks plus the next one in flight.  K and V get their own 2-slot rings (released after S
+// and dP), LSE*log2e / delta windows a 2-slot ring (released after the dS phase).  The
+// NQ-wide MMAs are issued as N = 128 + (NQ - 128) column pieces over the two blocks.
+// ------------------------------------------------------------------------------------------
+template <int CW> struct DkvRCfg {
+  static constexpr int NQ = nk_of(CW);
+  static constexpr int NQ2 = NQ - kM;                    // rows taken from the second block
+  static constexpr int NB = NQ2 > 0 ? 2 : 1;            // blocks per tile window
+  static constexpr int KB = kM * 128;
+  static constexpr int BLK = 2 * KB;                    // [Q block | dO block]
+  static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
+  static constexpr int RW = 2 * NQP * 4;                // LSE*log2e | delta window
+  static constexpr int SMEM = 1024 + 3 * BLK + 2 * KB + 2 * KB + 2 * KB /* staging */ + 2 * RW + 512;
+  static constexpr int THREADS = 320;
+};
+
+// Block bookkeeping of a CTA's tile sequence (identical in the producer and the MMA issuer):
+// tile k's window uses blocks kt and kt+1 of its head; a tile that continues the previous one
+// (same head, next key tile) reuses the previous tile's second block as its first.
+struct BlkSeq {
+  int k, n;          // next tile, next block number to load
+  int pbh, pkt, ps;  // previous tile's head, key tile, second block number
+  __device__ void init() { k = 0; n = 0; pbh = -1; pkt = -1; ps = -1; }
+  // blocks of tile k (global tile g): first f, second s (-1 if NB == 1); new blocks to load in
+  // [nl0, nl1); advances to tile k + 1
+  __device__ void next(int g, int ntq, int nb, int& f, int& s, int& nl0, int& nl1) {
+    const int bh = g / ntq, kt = g % ntq;
+    const bool cont = nb == 2 && bh == pbh && kt == pkt + 1;
+    nl0 = n;
+    if (cont) { f = ps; s = n++; }
+    else { f = n++; s = nb == 2 ? n++ : -1; }
+    nl1 = n;
+    pbh = bh; pkt = kt; ps = s; ++k;
+  }
+};
+
+template <int CW>
+__global__ void __launch_bounds__(320, 1)
+    sa_bwd_dkdv_ring_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                        const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
+                        const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel,
+                        TcArgs a) {
+  using C = DkvRCfg<CW>;
+  constexpr int NQ = C::NQ, NQ2 = C::NQ2, NB = C::NB;
+  static_assert(NQ + 64 <= 256 && NQ >= kM && NQ <= 2 * kM, "TMEM layout / two-block window");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* blk0 = smem;                             // [Q | dO] x 3 block slots
+  uint8_t* k0 = blk0 + 3 * C::BLK;                  // K x 2
+  uint8_t* v0 = k0 + 2 * C::KB;                     // V x 2
+  uint8_t* obuf0 = v0 + 2 * C::KB;                  // staging x 2 (one per warpgroup)
+  uint8_t* rw0 = obuf0 + 2 * C::KB;                 // LSE / delta windows x 2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rw0 + 2 * C::RW);
+  uint64_t* bfull = bars;             // [3]
+  uint64_t* bempty = bfull + 3;       // [3]
+  uint64_t* kfull = bempty + 3;       // [2]
+  uint64_t* kempty = kfull + 2;       // [2]
+  uint64_t* vfull = kempty + 2;       // [2]
+  uint64_t* vempty = vfull + 2;       // [2]
+  uint64_t* rfull = vempty + 2;       // [2]
+  uint64_t* rempty = rfull + 2;       // [2] (128)
+  uint64_t* sfull = rempty + 2;       // [2]
+  uint64_t* xfree = sfull + 2;        // [2] (128)
+  uint64_t* dpfull = xfree + 2;       // [2]
+  uint64_t* pdsfull = dpfull + 2;     // [2] (128)
+  uint64_t* kvfull = pdsfull + 2;     // [2]
+  uint64_t* kvfree = kvfull + 2;      // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, W = a.L + a.R + 1;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int G = gridDim.x;
+  const int g_begin = (int)((long long)blockIdx.x * ntiles / G);
+  const int ntile_me = (int)((long long)(blockIdx.x + 1) * ntiles / G) - g_begin;
+
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < 3; ++i) { tc::mbar_init(&bfull[i], 1); tc::mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&kfull[i], 1); tc::mbar_init(&kempty[i], 1);
+      tc::mbar_init(&vfull[i], 1); tc::mbar_init(&vempty[i], 1);
+      tc::mbar_init(&rfull[i], 1); tc::mbar_init(&rempty[i], 128);
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t DV = tbase + NQ, DK = tbase + 256 + NQ;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      BlkSeq sq;
+      sq.init();
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = g_begin + k;
+        const int bh = g / ntq, kt = g % ntq, u0 = kt * kM;
+        int f, s2, nl0, nl1;
+        sq.next(g, ntq, NB, f, s2, nl0, nl1);
+        trace_at(a.trace, 0, k);
+        // new window blocks (block b of this head = frames [128 b - R, 128 b - R + 128))
+        for (int n = nl0; n < nl1; ++n) {
+          const int sl = n % 3;
+          if (n >= 3) tc::mbar_wait(&bempty[sl], ((n / 3) - 1) & 1);
+          const int b = (n == f) ? kt : kt + 1;
+          uint8_t* d = blk0 + sl * C::BLK;
+          tc::mbar_expect_tx(&bfull[sl], C::BLK);
+          tc::tma_load_3d(d, &tmQ, &bfull[sl], 0, b * kM - a.R, bh);
+          tc::tma_load_3d(d + C::KB, &tmdO, &bfull[sl], 0, b * kM - a.R, bh);
+        }
+        const int s = k & 1;
+        if (k >= 2) tc::mbar_wait(&kempty[s], ((k - 2) >> 1) & 1);
+        tc::mbar_expect_tx(&kfull[s], C::KB);
+        tc::tma_load_3d(k0 + s * C::KB, &tmK, &kfull[s], 0, u0, bh);
+        if (k >= 2) tc::mbar_wait(&vempty[s], ((k - 2) >> 1) & 1);
+        tc::mbar_expect_tx(&vfull[s], C::KB);
+        tc::tma_load_3d(v0 + s * C::KB, &tmV, &vfull[s], 0, u0, bh);
+        if (k >= 2) tc::mbar_wait(&rempty[s], ((k - 2) >> 1) & 1);
+        const int na = (u0 - a.R) & ~3;
+        tc::mbar_expect_tx(&rfull[s], C::RW);
+        tc::tma_load_3d(rw0 + s * C::RW, &tmL2, &rfull[s], na, bh, 0);
+        tc::tma_load_3d(rw0 + s * C::RW + C::NQP * 4, &tmDel, &rfull[s], na, bh, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS1 = tc::idesc_bf16(kM, kM, 0, 0);
+      constexpr uint32_t idS2 = tc::idesc_bf16(kM, NQ2 > 0 ? NQ2 : 16, 0, 0);
+      constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
+      BlkSeq qs, qd, qk;                               // block sequences seen by S, dP, kv
+      qs.init(); qd.init(); qk.init();
+      int sf = 0, ss = 0, df = 0, ds2 = 0, kf = 0, ks2 = 0, krel2 = 0;   // current tiles' block numbers
+      int ns = 0, ndp = 0, nkv = 0;
+      auto blk = [&](int n) { return tc::smem_u32(blk0 + (n % 3) * C::BLK); };
+      bool s_ready = false, d_ready = false, k_ready = false;            // block numbers fetched
+      while (nkv < ntile_me) {
+        if (!s_ready && ns < ntile_me) { int a0, a1; qs.next(g_begin + ns, ntq, NB, sf, ss, a0, a1); s_ready = true; }
+        if (!d_ready && ndp < ns) { int a0, a1; qd.next(g_begin + ndp, ntq, NB, df, ds2, a0, a1); d_ready = true; }
+        if (!k_ready && nkv < ndp) {
+          int a0, a1; qk.next(g_begin + nkv, ntq, NB, kf, ks2, a0, a1);
+          // the second block is released with this tile unless the next tile continues the head
+          const int g = g_begin + nkv, gn = g + 1;
+          krel2 = (NB == 2) && !(nkv + 1 < ntile_me && gn / ntq == g / ntq && gn % ntq == g % ntq + 1);
+          k_ready = true;
+        }
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&kfull[ns & 1]), (ns >> 1) & 1);
+        if (k_ready && nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
+          tc::tc_fence_after();
+          const int b = nkv & 1;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t bf = blk(kf), bs = NB == 2 ? blk(ks2) : bf;
+#pragma unroll
+          for (int j = 0; j < NQ / 16; ++j) {
+            const uint32_t dO = (j < kM / 16 ? bf : bs) + C::KB + 2048 * (j % (kM / 16));
+            tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO), idG, j > 0);
+          }
+#pragma unroll
+          for (int j = 0; j < NQ / 16; ++j) {
+            const uint32_t q = (j < kM / 16 ? bf : bs) + 2048 * (j % (kM / 16));
+            tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q), idG, j > 0);
+          }
+          tc::mma_commit(&kvfull[b]);
+          tc::mma_commit(&bempty[kf % 3]);
+          if (krel2) tc::mma_commit(&bempty[ks2 % 3]);
+          ++nkv;
+          k_ready = false;
+          continue;
+        }
+        if (d_ready && ndp < ns && (m & 4) && tc::mbar_test(tc::smem_u32(&vfull[ndp & 1]), (ndp >> 1) & 1)) {
+          tc::tc_fence_after();
+          const int b = ndp & 1;
+          const uint32_t v = tc::smem_u32(v0 + (ndp & 1) * C::KB);
+          const uint32_t dO1 = blk(df) + C::KB, dO2 = (NB == 2 ? blk(ds2) : blk(df)) + C::KB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j) {
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO1 + 32 * j), idS1,
+                         j > 0);
+            if (NQ2 > 0)
+              tc::mma_bf16(tbase + b * 256 + kM, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO2 + 32 * j),
+                           idS2, j > 0);
+          }
+          tc::mma_commit(&dpfull[b]);
+          tc::mma_commit(&vempty[ndp & 1]);
+          ++ndp;
+          d_ready = false;
+          continue;
+        }
+        if (s_ready && ns < ntile_me && ns < nkv + 2 && (m & 8) &&
+            tc::mbar_test(tc::smem_u32(&bfull[sf % 3]), (sf / 3) & 1) &&
+            (NB == 1 || tc::mbar_test(tc::smem_u32(&bfull[ss % 3]), (ss / 3) & 1))) {
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t kk = tc::smem_u32(k0 + (ns & 1) * C::KB);
+          const uint32_t q1 = blk(sf), q2 = NB == 2 ? blk(ss) : q1;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j) {
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q1 + 32 * j), idS1,
+                         j > 0);
+            if (NQ2 > 0)
+              tc::mma_bf16(tbase + b * 256 + kM, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q2 + 32 * j),
+                           idS2, j > 0);
+          }
+          tc::mma_commit(&sfull[b]);
+          tc::mma_commit(&kempty[ns & 1]);
+          ++ns;
+          s_ready = false;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    uint8_t* ostage = obuf0 + wg * C::KB;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = g_begin + k;
+      const int bh = g / ntq, u0 = (g % ntq) * kM;
+      const int b = wg, use = k >> 1, s = k & 1;
+      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
+      const float* sL2 = reinterpret_cast<const float*>(rw0 + s * C::RW) + sh;
+      const float* sDel = sL2 + C::NQP;
+      tc::mbar_wait(&rfull[s], (k >> 1) & 1);
+      const bool tr = (tid == 64) || (tid == 192);
+      if (tr) trace_at(a.trace, 1, k);
+      const uint32_t x = tbase + lanes + b * 256;
+      const int c0 = 32 * q4;
+      tc::mbar_wait(&sfull[b], use & 1);
+      if (tr) trace_at(a.trace, 2, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      if (tr) trace_at(a.trace, 3, k);
+      tc::mbar_wait(&dpfull[b], use & 1);
+      if (tr) trace_at(a.trace, 4, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CW];
+#pragma unroll
+      for (int j = 0; j < CW / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      }
+      tc::mbar_arrive(&rempty[s]);                     // LSE / delta window consumed
+      tmem_write_row<CW, NQ>(x, q4, p);
+      tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[b]);
+      if (tr) trace_at(a.trace, 5, k);
+      // dV then dK through one staging tile (TMA stores)
+      tc::mbar_wait(&kvfull[b], use & 1);
+      if (tr) trace_at(a.trace, 6, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float dk[64];
+      {
+        float dv[64];
+        tmem_ld64(DV + lanes, dv);
+        tmem_ld64(DK + lanes, dk);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&kvfree[b]);
+        if (leader) tc::bulk_wait_read0();             // the previous tile's dK store has read the tile
+        tc::named_bar(1 + wg, 128);
+        const uint32_t row = tc::smem_u32(ostage) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tc::st_shared_v4(row + ((c ^ (r & 7)) << 4),
+                           make_uint4(pack_bf16(dv[8 * c], dv[8 * c + 1]), pack_bf16(dv[8 * c + 2], dv[8 * c + 3]),
+                                      pack_bf16(dv[8 * c + 4], dv[8 * c + 5]), pack_bf16(dv[8 * c + 6], dv[8 * c + 7])));
+      }
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+        tc::bulk_commit();
+        tc::bulk_wait_read0();
+      }
+      tc::named_bar(1 + wg, 128);
+      {
+        const uint32_t row = tc::smem_u32(ostage) + r * 128;
+        const float sc = a.scale;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          tc::st_shared_v4(row + ((c ^ (r & 7)) << 4),
+                           make_uint4(pack_bf16(dk[8 * c] * sc, dk[8 * c + 1] * sc), pack_bf16(dk[8 * c + 2] * sc, dk[8 * c + 3] * sc),
+                                      pack_bf16(dk[8 * c + 4] * sc, dk[8 * c + 5] * sc), pack_bf16(dk[8 * c + 6] * sc, dk[8 * c + 7] * sc)));
+      }
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdK, ostage, 0, u0, bh);
+        tc::bulk_commit();
+      }
+      if (tr) trace_at(a.trace, 7, k);
+    }
+    if (leader) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
 // LLSA backward, band keys (channel R), key-major: for a tile of 128 channel-R keys u, every
 // query channel c = 0..R contributes through the band: query (t, c) sees (u, R) iff
 // u in [t + c - R - L, t + c - R]  <=>  t in [u + s_c, u + s_c + L],  s_c = R - c
@@ -1124,31 +1482,6 @@ template <int CW> struct FusCfg {
   static constexpr int THREADS = 384;            // TMA, MMA, 2 x 4 WG warps, 2 row warps
 };
 
-__device__ __forceinline__ float dot8_bf16(uint4 a, uint4 b) {
-  const __nv_bfloat162* x = reinterpret_cast<const __nv_bfloat162*>(&a);
-  const __nv_bfloat162* y = reinterpret_cast<const __nv_bfloat162*>(&b);
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 u = __bfloat1622float2(x[i]), v = __bfloat1622float2(y[i]);
-    s = fmaf(u.x, v.x, s);
-    s = fmaf(u.y, v.y, s);
-  }
-  return s;
-}
-// 64 fp32 of one row -> bf16 (x sc) -> 128 contiguous bytes in global memory
-__device__ __forceinline__ void store_row_bf16(bf16* dst, const float* v, float sc) {
-  uint4* d = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int c = 0; c < 8; ++c)
-    d[c] = make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
-                      pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc));
-}
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float* v) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) tc::tmem_ld16(taddr + 16 * j, v + 16 * j);
-  tc::tmem_ld_wait();
-}
 // carry row r (64 fp32) in smem, float4 s stored at slot s ^ (r & 15) (conflict-free row-per-thread)
 __device__ __forceinline__ float4* carry_at(float* carry, int r, int s) {
   return reinterpret_cast<float4*>(carry + r * 64) + (s ^ (r & 15));
@@ -1755,11 +2088,19 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq,
              tc_args(a));
   }
-  if (!only || only[0] != '1')
-  {
-  cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
-  launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
-             mdoN, mdk, mdv, ml2, mdel, tc_args(a));
+  if (!only || only[0] != '1') {
+    // K2 variant: the two-stage window kernel (default, measured faster) or, with SATTN_K2=ring,
+    // the block-ring sweep (loads hidden, but a longer warpgroup chain: DESIGN.md §10)
+    const char* k2 = getenv("SATTN_K2");
+    if (!(k2 && !strcmp(k2, "ring"))) {
+      cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
+                 mdoN, mdk, mdv, ml2, mdel, tc_args(a));
+    } else {
+      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_ring_tc<CW>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq, mk128,
+                 mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
+    }
   }
   return SATTN_OK;
 }

@@ -228,3 +228,27 @@ def test_sa_fused_backward_full_shape_cta_boundaries(monkeypatch):
         G = oracle.sa.sa_backward(q, k, v, do, L, R)
         for name, got, ref in (("dQ", dq[b, h], G[0]), ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
             assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
+
+
+# The block-ring K2 (SATTN_K2=ring): a contiguous key-tile sweep per CTA with 128-row Q/dO
+# blocks shared by consecutive tiles; block reuse and release at head changes are what these
+# shapes exercise (several heads per CTA range, ragged ends, W from 1 to 49).
+RING = [((1, 2, 129, 64), 0, 0), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16), ((1, 3, 777, 64), 32, 8),
+        ((3, 2, 300, 64), 24, 0), ((8, 12, 1750, 64), 32, 8)]
+
+
+@pytest.mark.parametrize("shape,L,R", RING)
+def test_sa_bf16_ring_k2(shape, L, R, monkeypatch):
+    monkeypatch.setenv("SATTN_K2", "ring")
+    s = sattn()
+    B, H = shape[:2]
+    q, k, v = synth.qkv(6, shape, "bf16")
+    do = synth.grad_out(6, shape, "bf16")
+    tq, tk, tv, tdo = (dev(x, "bf16") for x in (q, k, v, do))
+    o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
+    dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
+    heads = [(b, h) for b in range(B) for h in range(H)][:: max(1, (B * H) // 6)]
+    for (b, h) in heads:
+        G = oracle.sa.sa_backward(q[b, h], k[b, h], v[b, h], do[b, h], L, R)
+        for name, got, ref in (("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
+            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
