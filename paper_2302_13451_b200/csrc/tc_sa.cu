@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <utility>
 #include <string>
 
@@ -156,6 +157,16 @@ __device__ __forceinline__ void tmem_write_row(uint32_t pa, int q4, const float*
   }
   for (int c = 0; c < NK / 2; c += 4)
     if (c < c0 || c >= c0 + CW / 2) tc::tmem_st4(pa + c, 0u, 0u, 0u, 0u);
+}
+
+// 64 fp32 values of row r (registers) -> scaled bf16 -> row r of a 128-row x 128-byte tile (128B swizzle)
+__device__ __forceinline__ void tmem_row64_to_smem_sw128_regs(const float* v, float sc, uint8_t* tile, int r) {
+  const uint32_t row = tc::smem_u32(tile) + r * 128;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    tc::st_shared_v4(row + ((c ^ (r & 7)) << 4),
+                     make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
+                                pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc)));
 }
 
 // 64 fp32 TMEM columns of this thread's row -> scaled bf16 -> row r of a 128-row x 128-byte
@@ -909,7 +920,7 @@ struct BlkSeq {
   }
 };
 
-template <int CW>
+template <int CW, bool COOP>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dkdv_ring_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                         const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -958,9 +969,10 @@ __global__ void __launch_bounds__(320, 1)
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&kfull[i], 1); tc::mbar_init(&kempty[i], 1);
       tc::mbar_init(&vfull[i], 1); tc::mbar_init(&vempty[i], 1);
-      tc::mbar_init(&rfull[i], 1); tc::mbar_init(&rempty[i], 128);
-      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
-      tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
+      constexpr int NW = COOP ? 256 : 128;   // consumers per tile: both warpgroups (COOP) or one
+      tc::mbar_init(&rfull[i], 1); tc::mbar_init(&rempty[i], NW);
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], NW); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], NW); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], NW);
     }
     tc::fence_mbar_init();
   }
@@ -1095,6 +1107,116 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
     }
+  } else if (COOP) {
+    // Both warpgroups work on every tile: warpgroup `half` owns strip chunks [NC0 half, ...) of
+    // each row (the two warps of a TMEM lane quadrant split the row), so the P and dS phases take
+    // half as long; the dV (half 0) / dK (half 1) epilogue of tile k-1 runs after tile k's dS,
+    // while the tensor core works on tile k-1's dV/dK MMAs and on S(k+1).
+    const int half = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    uint8_t* ostage = obuf0 + half * C::KB;
+    constexpr int NC = CW / 8, NC0 = (NC + 1) / 2;     // strip chunks, chunks of half 0
+    const int c0 = 32 * q4;
+    auto epilogue = [&](int kp) {   // dV (half 0) or dK (half 1) rows of tile kp
+      const int gp = g_begin + kp;
+      const int bhp = gp / ntq, u0p = (gp % ntq) * kM;
+      tc::mbar_wait(&kvfull[kp & 1], (kp >> 1) & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float v[64];
+      tmem_ld64((half ? DK : DV) + lanes, v);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&kvfree[kp & 1]);
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + half, 128);
+      tmem_row64_to_smem_sw128_regs(v, half ? a.scale : 1.f, ostage, r);
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + half, 128);
+      if (leader) {
+        tc::tma_store_3d(half ? &tmdK : &tmdV, ostage, 0, u0p, bhp);
+        tc::bulk_commit();
+      }
+    };
+    // the tile body for one half, with its chunk range known at compile time (no spills)
+    auto tile = [&](int k, auto J0c, auto J1c) {
+      constexpr int J0 = decltype(J0c)::value, J1 = decltype(J1c)::value, NJ = J1 - J0;
+      const int g = g_begin + k;
+      const int u0 = (g % ntq) * kM;
+      const int b = k & 1, use = k >> 1, s = k & 1;
+      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
+      const float* sL2 = reinterpret_cast<const float*>(rw0 + s * C::RW) + sh + c0 + 8 * J0;
+      const float* sDel = sL2 + C::NQP;
+      const bool tr = (tid == 64);
+      tc::mbar_wait(&rfull[s], (k >> 1) & 1);
+      if (tr) trace_at(a.trace, 1, k);
+      const uint32_t x = tbase + lanes + b * 256;
+      tc::mbar_wait(&sfull[b], use & 1);
+      if (tr) trace_at(a.trace, 2, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[8 * NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) tc::tmem_ld8(x + c0 + 8 * (J0 + j), p + 8 * j);
+      tc::tmem_ld_wait();
+      const int lo = lane - 8 * J0, hi = lane + W - 8 * J0;   // band columns of this row, in local indices
+#pragma unroll
+      for (int i = 0; i < 8 * NJ; ++i)
+        p[i] = (i >= lo && i < hi) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      if (tr) trace_at(a.trace, 3, k);
+      tc::mbar_wait(&dpfull[b], use & 1);
+      if (tr) trace_at(a.trace, 4, k);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[8 * NJ];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * (J0 + j), dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[8 * j + e]);
+      }
+      tc::mbar_arrive(&rempty[s]);
+      // the packed P / dS columns overlap the other half's fp32 dP columns: both halves of every
+      // row must have read dP first
+      tc::tc_fence_before();
+      tc::named_bar(3, 256);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int pc = 16 * q4 + 4 * (J0 + j);
+        tc::tmem_st4(x + pc, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
+                     pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
+        tc::tmem_st4(x + NQ / 2 + pc, pack_bf16(ds[8 * j], ds[8 * j + 1]), pack_bf16(ds[8 * j + 2], ds[8 * j + 3]),
+                     pack_bf16(ds[8 * j + 4], ds[8 * j + 5]), pack_bf16(ds[8 * j + 6], ds[8 * j + 7]));
+      }
+      // this half's share of the row's zero columns (half 0 before the strip, half 1 after it)
+      {
+        const int pc0 = 16 * q4;
+        const int zlo = J0 ? pc0 + CW / 2 : 0, zhi = J0 ? NQ / 2 : pc0;
+        for (int c = zlo; c < zhi; c += 4) {
+          tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
+          tc::tmem_st4(x + NQ / 2 + c, 0u, 0u, 0u, 0u);
+        }
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[b]);
+      if (tr) trace_at(a.trace, 5, k);
+      if (k >= 1) epilogue(k - 1);
+      if (tr) trace_at(a.trace, 7, k);
+    };
+    for (int k = 0; k < ntile_me; ++k) {
+      if (half) tile(k, std::integral_constant<int, NC0>{}, std::integral_constant<int, NC>{});
+      else tile(k, std::integral_constant<int, 0>{}, std::integral_constant<int, NC0>{});
+    }
+    if (ntile_me > 0) epilogue(ntile_me - 1);
+    if (leader) tc::bulk_wait0();
   } else {
     const int wg = (warp - 2) >> 2;
     const int q4 = warp & 3;
@@ -2092,13 +2214,17 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
     // K2 variant: the two-stage window kernel (default, measured faster) or, with SATTN_K2=ring,
     // the block-ring sweep (loads hidden, but a longer warpgroup chain: DESIGN.md §10)
     const char* k2 = getenv("SATTN_K2");
-    if (!(k2 && !strcmp(k2, "ring"))) {
+    if (k2 && !strcmp(k2, "coop")) {
+      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
+                 mk128, mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
+    } else if (!(k2 && !strcmp(k2, "ring"))) {
       cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
       launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
                  mdoN, mdk, mdv, ml2, mdel, tc_args(a));
     } else {
-      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_ring_tc<CW>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq, mk128,
+      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_ring_tc<CW, false>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq, mk128,
                  mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
     }
   }

@@ -237,9 +237,7 @@ RING = [((1, 2, 129, 64), 0, 0), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 3
         ((3, 2, 300, 64), 24, 0), ((8, 12, 1750, 64), 32, 8)]
 
 
-@pytest.mark.parametrize("shape,L,R", RING)
-def test_sa_bf16_ring_k2(shape, L, R, monkeypatch):
-    monkeypatch.setenv("SATTN_K2", "ring")
+def _ring_check(shape, L, R):
     s = sattn()
     B, H = shape[:2]
     q, k, v = synth.qkv(6, shape, "bf16")
@@ -252,3 +250,14 @@ def test_sa_bf16_ring_k2(shape, L, R, monkeypatch):
         G = oracle.sa.sa_backward(q[b, h], k[b, h], v[b, h], do[b, h], L, R)
         for name, got, ref in (("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
             assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
+    dq2, dk2, dv2 = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
+    assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
+
+
+@pytest.mark.parametrize("variant", ["ring", "coop"])
+@pytest.mark.parametrize("shape,L,R", RING)
+def test_sa_bf16_k2_variants(shape, L, R, variant, monkeypatch):
+    # SATTN_K2=ring: block-ring sweep; SATTN_K2=coop: the same with both warpgroups on every
+    # tile (column halves of each row, deferred dV / dK epilogue)
+    monkeypatch.setenv("SATTN_K2", variant)
+    _ring_check(shape, L, R)
