@@ -87,25 +87,32 @@ __global__ void __launch_bounds__(256, 2) llsa_bwd_stair(StairArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // ---- stage: rows h - c of channel c for h in [h0, h0 + 16)  (zero outside [0, T))
-  const int nrows = ((DX ? 2 : 3) * C + 2 * R) * kStF;
-  for (int idx = tid; idx < nrows * 8; idx += blockDim.x) {
-    const int ch16 = idx & 7, r = (idx >> 3) % kStF, sl = (idx >> 3) / kStF;   // slot = tensor-channel
+  // one warp per (tensor, channel) slot: the slot's plane base and smem tile are computed once,
+  // the lanes then cover its 16 rows x 8 16-byte chunks (4 cp.async each)
+  const int nslot = (DX ? 2 : 3) * C + 2 * R;
+  for (int sl = warp; sl < nslot; sl += blockDim.x >> 5) {
     int tsr, c;
     if (sl < C) { tsr = 0; c = sl; }
     else if (sl < 2 * C) { tsr = 3; c = sl - C; }
     else if (sl < 2 * C + R) { tsr = 1; c = sl - 2 * C; }
     else if (sl < 2 * C + 2 * R) { tsr = 2; c = sl - 2 * C - R; }
     else { tsr = 4; c = sl - 2 * C - 2 * R; }
-    const int f = h0 + r - c;
-    const bool ok = f >= 0 && f < T;
     const bf16* base = tsr == 0 ? a.Q : tsr == 1 ? a.K : tsr == 2 ? a.V : tsr == 3 ? a.dO : a.dQ;
     const long long cs = tsr >= 3 ? a.plane : a.in_cs;
-    const bf16* src = base + c * cs + ((long long)bh * T + (ok ? f : 0)) * 64 + ch16 * 8;
-    uint8_t* dst = (tsr == 0 ? sQ : tsr == 1 ? sK : tsr == 2 ? sV : tsr == 3 ? sD : sG) + c * kStTile + r * kStRS +
-                   ch16 * 16;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                 "l"(src), "r"(ok ? 16 : 0)
-                 : "memory");
+    const bf16* plane = base + c * cs + (long long)bh * T * 64;
+    const uint32_t tile = (uint32_t)__cvta_generic_to_shared(
+        (tsr == 0 ? sQ : tsr == 1 ? sK : tsr == 2 ? sV : tsr == 3 ? sD : sG) + c * kStTile);
+    const int ch16 = lane & 7;
+#pragma unroll
+    for (int j = 0; j < kStF / 4; ++j) {
+      const int r = (lane >> 3) + 4 * j;
+      const int f = h0 + r - c;
+      const bool ok = f >= 0 && f < T;
+      const bf16* src = plane + (long long)(ok ? f : 0) * 64 + ch16 * 8;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(tile + r * kStRS + ch16 * 16), "l"(src),
+                   "r"(ok ? 16 : 0)
+                   : "memory");
+    }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int idx = tid; idx < C * kStF; idx += blockDim.x) {
