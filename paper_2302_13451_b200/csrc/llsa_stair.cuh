@@ -206,12 +206,10 @@ __global__ void __launch_bounds__(256, 2) llsa_bwd_stair(StairArgs a) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int c = g + 8 * hh, t = h - c;
-          if (c < C && t >= 0 && t < T) {
-            __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(a.dQ + c * a.plane + ((long long)bh * T + t) * 64 +
-                                                                    8 * j + 2 * t4);
-            const float2 cur = __bfloat1622float2(
-                *reinterpret_cast<const __nv_bfloat162*>(sG + c * kStTile + i * kStRS + 16 * j + 4 * t4));
-            *dst = __floats2bfloat162_rn(fmaf(acc[2 * hh], a.scale, cur.x), fmaf(acc[2 * hh + 1], a.scale, cur.y));
+          if (c < C && t >= 0 && t < T) {   // dQ row (t, c) = row i of channel c's staged tile, in place
+            __nv_bfloat162* g2 = reinterpret_cast<__nv_bfloat162*>(sG + c * kStTile + i * kStRS + 16 * j + 4 * t4);
+            const float2 cur = __bfloat1622float2(*g2);
+            *g2 = __floats2bfloat162_rn(fmaf(acc[2 * hh], a.scale, cur.x), fmaf(acc[2 * hh + 1], a.scale, cur.y));
           }
         }
       }
@@ -234,14 +232,33 @@ __global__ void __launch_bounds__(256, 2) llsa_bwd_stair(StairArgs a) {
         const int cp = g;                                 // rows c' = g (rows g + 8 are padding)
         const int u = h - cp;
         if (cp < R && u >= 0 && u < T) {
-          const long long off = cp * a.plane + ((long long)bh * T + u) * 64 + 8 * j + 2 * t4;
-          *reinterpret_cast<__nv_bfloat162*>(a.dV + off) = __floats2bfloat162_rn(dv[0], dv[1]);
-          *reinterpret_cast<__nv_bfloat162*>(a.dK + off) =
-              __floats2bfloat162_rn(dk[0] * a.scale, dk[1] * a.scale);
+          // the staircase key (u, c') is horizon h's alone: its K / V rows (row i of tile c', read
+          // only by this warp, above) take dK / dV in place
+          const int o = cp * kStTile + i * kStRS + 16 * j + 4 * t4;
+          *reinterpret_cast<__nv_bfloat162*>(sV + o) = __floats2bfloat162_rn(dv[0], dv[1]);
+          *reinterpret_cast<__nv_bfloat162*>(sK + o) = __floats2bfloat162_rn(dk[0] * a.scale, dk[1] * a.scale);
         }
       }
     }
     __syncwarp();
+  }
+  if (DX) return;
+  // ---- write the staged dQ (all channels) and the staircase dK / dV rows: 16-byte stores
+  __syncthreads();
+  for (int sl = warp; sl < C + 2 * R; sl += blockDim.x >> 5) {
+    const int tsr = sl < C ? 0 : sl < C + R ? 1 : 2;
+    const int c = tsr == 0 ? sl : tsr == 1 ? sl - C : sl - C - R;
+    const uint8_t* tile = (tsr == 0 ? sG : tsr == 1 ? sK : sV) + c * kStTile;
+    bf16* plane = (tsr == 0 ? a.dQ : tsr == 1 ? a.dK : a.dV) + c * a.plane + (long long)bh * T * 64;
+    const int ch16 = lane & 7;
+#pragma unroll
+    for (int j = 0; j < kStF / 4; ++j) {
+      const int r = (lane >> 3) + 4 * j;
+      const int f = h0 + r - c;
+      if (f >= 0 && f < T)
+        *reinterpret_cast<uint4*>(plane + (long long)f * 64 + ch16 * 8) =
+            *reinterpret_cast<const uint4*>(tile + r * kStRS + ch16 * 16);
+    }
   }
 }
 
