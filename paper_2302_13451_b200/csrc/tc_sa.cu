@@ -69,6 +69,8 @@ struct TcArgs {
                                                  // band (LLSA staircase, from the stair pre-pass); null for SA
   int dq_split;                                  // K1: dQ MMA on bf16 dS hi + lo (LLSA, whose dQ is rounded twice)
   int mma_order;                                 // fused backward: MMA issue priority (tuning)
+  int nch;                                       // K1: channels in one launch (LLSA band pass: C; SA: 1)
+  int bcast;                                     // K1: Q is one plane read as every channel (LLSA layer 1)
   float* ws_hand;                                // fused backward: per-CTA dQ hand-off rows [grid][48][64] fp32
 };
 
@@ -445,8 +447,12 @@ __global__ void __launch_bounds__(320, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
   const int ntq = (T + kM - 1) / kM;
-  const int ntiles = ntq * a.BH;
+  // tiles: (channel c, head bh, query tile) with c slowest; SA has one channel.  LLSA runs every
+  // channel's band pass in one launch: channel c's queries see channel-R keys shifted by R - c.
+  const int nch = a.nch > 0 ? a.nch : 1;
+  const int ntiles = ntq * a.BH * nch;
   const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int tpc = ntq * a.BH;                            // tiles per channel
 
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
@@ -470,16 +476,23 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     if (lane == 0) {
       for (int k = 0; k < ntile_me; ++k) {
-        const int g = blockIdx.x + k * gridDim.x;
+        const int g0 = blockIdx.x + k * gridDim.x;
+        const int c = g0 / tpc, g = g0 % tpc;
         const int bh = g / ntq, t0 = (g % ntq) * kM;
+        const int ksh = a.kshift - c;                    // LLSA: R - c (a.kshift = R); SA: 0
         const int st = k % NS;
         uint8_t* b0 = stage0 + st * C::STAGE;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         tc::mbar_expect_tx(&full[st], 2 * C::QB + 2 * C::KB);
-        tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
-        tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
-        tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - a.kshift, bh);
-        tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - a.kshift, bh);
+        if (nch > 1) {   // LLSA: [C][BH][T][64] maps
+          tc::tma_load_4d(b0, &tmQ, &full[st], 0, t0, bh, a.bcast ? 0 : c);
+          tc::tma_load_4d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh, c);
+        } else {
+          tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
+          tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
+        }
+        tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - ksh, bh);
+        tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - ksh, bh);
       }
     }
   } else if (warp == 1) {
@@ -549,14 +562,18 @@ __global__ void __launch_bounds__(320, 1)
     // LSE (and the staircase rowsum) of this warpgroup's next tile are loaded one tile ahead
     auto row_of = [&](int k, const float* src, int stride, float mul) -> float {
       if (k >= ntile_me || !src) return 0.f;
-      const int g = blockIdx.x + k * gridDim.x;
+      const int g0 = blockIdx.x + k * gridDim.x;
+      const int c = g0 / tpc, g = g0 % tpc;
       const int t = (g % ntq) * kM + r;
-      return t < T ? src[(long long)(g / ntq) * stride + t] * mul : 0.f;
+      return t < T ? src[((long long)c * a.BH + g / ntq) * stride + t] * mul : 0.f;
     };
     float lse_next = row_of(wg, a.LSEin, T, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
     for (int k = wg; k < ntile_me; k += 2) {
-      const int g = blockIdx.x + k * gridDim.x;
+      const int g0 = blockIdx.x + k * gridDim.x;
+      const int c = g0 / tpc, g = g0 % tpc;
       const int bh = g / ntq, t0 = (g % ntq) * kM;
+      const int ksh = a.kshift - c;
+      const long long cbh = (long long)c * a.BH + bh;    // row of the [C][BH][Tp] workspaces
       const int t = t0 + r;
       const bool row_ok = t < T;
       const int b = wg, use = k >> 1;
@@ -572,7 +589,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
-      const int key0 = t0 - a.L - a.kshift + 32 * q4;
+      const int key0 = t0 - a.L - ksh + 32 * q4;
       {
         const int lo = max(lane, -key0), hi = min(lane + W, T - key0);
 #pragma unroll
@@ -622,8 +639,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_arrive(&dsfull[b]);
       // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
       if (t < a.Tp) {
-        a.ws_del[(long long)bh * a.Tp + t] = row_ok ? delta : 0.f;
-        a.ws_l2[(long long)bh * a.Tp + t] = row_ok ? lse2 : 0.f;
+        a.ws_del[cbh * a.Tp + t] = row_ok ? delta : 0.f;
+        a.ws_l2[cbh * a.Tp + t] = row_ok ? lse2 : 0.f;
       }
       // dQ epilogue
       tc::mbar_wait(&dqfull[b], use & 1);
@@ -637,7 +654,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::fence_proxy_async_smem();
       tc::named_bar(1 + wg, 128);
       if (leader) {
-        tc::tma_store_3d(&tmdQ, ostage, 0, t0, bh);
+        if (nch > 1) tc::tma_store_4d(&tmdQ, ostage, 0, t0, bh, c);
+        else tc::tma_store_3d(&tmdQ, ostage, 0, t0, bh);
         tc::bulk_commit();
       }
     }
@@ -2269,23 +2287,28 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(llsa_bwd_stair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     llsa_bwd_stair<true><<<sgrid, 256, smem, st>>>(sa);
   }
-  // (1) query-major band pass per channel c: SA dQ kernel with R := 0 and keys shifted by R - c
-  cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
-  for (int c = 0; c < C; ++c) {
+  // (1) query-major band pass of every channel in one launch: the SA dQ kernel with R := 0 and
+  //     channel c's keys shifted by R - c (tiles ordered channel-major)
+  {
+    cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
     CUtensorMap mq, mk, mv, mdo, mdq;
-    if (!make_map(&mq, Q + a.in_cs * c, a.T, a.BH, kM) || !make_map(&mk, Kr, a.T, a.BH, NK) ||
-        !make_map(&mv, Vr, a.T, a.BH, NK) || !make_map(&mdo, dO + plane * c, a.T, a.BH, kM) ||
-        !make_map(&mdq, dQ + plane * c, a.T, a.BH, kM))
+    if (!make_map4(&mq, Q, a.T, a.BH, bc ? 1 : C, kM) || !make_map(&mk, Kr, a.T, a.BH, NK) ||
+        !make_map(&mv, Vr, a.T, a.BH, NK) || !make_map4(&mdo, dO, a.T, a.BH, C, kM) ||
+        !make_map4(&mdq, dQ, a.T, a.BH, C, kM))
       return SATTN_ECUDA;
     TcArgs t = tc_args(a);
     t.R = 0;
-    t.kshift = R - c;
-    t.LSEin = a.LSE + (long long)c * a.BH * a.T;
-    t.ws_del = ws_del + (long long)c * a.BH * Tp;
-    t.ws_l2 = ws_l2 + (long long)c * a.BH * Tp;
-    t.ws_dx = ws_dx + (long long)c * a.BH * Tp;
+    t.kshift = R;
+    t.nch = C;
+    t.bcast = bc ? 1 : 0;
+    t.LSEin = a.LSE;
+    t.ws_del = ws_del;
+    t.ws_l2 = ws_l2;
+    t.ws_dx = ws_dx;
     t.dq_split = 1;
-    launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq, t);
+    const int tiles = (a.T + kM - 1) / kM * a.BH * C;
+    launch_pdl(sa_bwd_dq_tc<CW>, dim3(tiles < num_sms() ? tiles : num_sms()), dim3(DqCfg<CW>::THREADS),
+               DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq, t);
   }
   // (2) key-major band pass: dK, dV of channel R accumulated over the C query channels
   {
@@ -2366,7 +2389,7 @@ sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-int tc_llsa_backward_launches(int R) { return (R + 1) + 3; }
+int tc_llsa_backward_launches(int R) { (void)R; return 4; }
 void tc_set_trace(void* p) { g_trace = static_cast<long long*>(p); }
 const char* tc_last_error() { return g_tc_err.c_str(); }
 
