@@ -196,7 +196,7 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
   if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true))
     return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA backward needs bf16, D=64, 1 <= R <= 8, L <= 48"
-                                         : "tensor-core SA backward needs bf16, D=64, L+R+1 <= 49");
+                                         : "tensor-core SA backward needs bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);

@@ -2232,7 +2232,10 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
     // K2 variant: the two-stage window kernel (default, measured faster) or, with SATTN_K2=ring,
     // the block-ring sweep (loads hidden, but a longer warpgroup chain: DESIGN.md §10)
     const char* k2 = getenv("SATTN_K2");
-    if (k2 && !strcmp(k2, "coop")) {
+    // bands too wide for the two-stage kernel's shared memory (W > 49: NQ = 192) take the
+    // block-ring kernel with the column-split warpgroups (its registers hold half a row)
+    constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
+    if (wide || (k2 && !strcmp(k2, "coop"))) {
       cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
       launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
                  mk128, mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
@@ -2338,9 +2341,10 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
 bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward) {
   if (llsa || dtype != SATTN_BF16 || D != 64) return false;
   const int W = L + R + 1;
-  // forward: TMEM (NK + 64 <= 256 per buffer) -> CW <= 96; backward: smem of the dK/dV
-  // kernel's two stages + staging -> CW <= 80
-  return W + 31 <= (backward ? 80 : 96);
+  // TMEM (NK + 64 <= 256 per buffer) -> CW <= 96, i.e. W <= 65, forward and backward (the
+  // backward takes the block-ring dK/dV kernel beyond CW = 80)
+  (void)backward;
+  return W + 31 <= 96;
 }
 
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st) {

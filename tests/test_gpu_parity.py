@@ -234,7 +234,7 @@ def test_sa_fused_backward_full_shape_cta_boundaries(monkeypatch):
 # blocks shared by consecutive tiles; block reuse and release at head changes are what these
 # shapes exercise (several heads per CTA range, ragged ends, W from 1 to 49).
 RING = [((1, 2, 129, 64), 0, 0), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16), ((1, 3, 777, 64), 32, 8),
-        ((3, 2, 300, 64), 24, 0), ((8, 12, 1750, 64), 32, 8)]
+        ((3, 2, 300, 64), 24, 0), ((8, 12, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 32), ((1, 2, 300, 64), 40, 24)]
 
 
 def _ring_check(shape, L, R):
