@@ -305,7 +305,10 @@ def run_gpu(args):
     hour = None
     if not args.no_hour:
         torch.cuda.empty_cache()
-        hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
+        try:
+            hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
+        except Exception as e:   # the headline line must not depend on this sub-measurement
+            hour = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     stream_lat = None
     if not args.no_stream:
