@@ -199,6 +199,20 @@ __global__ void __launch_bounds__(320, 1)
       const int g = blockIdx.x + kt * gridDim.x;
       const int bh = g / nht, h0 = (g % nht) * kHT;
       const int c = 4 * ii + q4;                         // output channel of this warp
+      if (c >= C) {
+        // padding rows of the last item (C = 9 channels in items of 4): no scores, softmax or
+        // epilogue, but the same barrier sequence so the arrivals of consecutive items never mix
+        // (their TMEM rows hold garbage that the PV MMA turns into garbage O rows, never stored)
+        tc::mbar_wait(&sfull[b], use & 1);
+        tc::tc_fence_after();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&pfull[b]);
+        tc::mbar_wait(&ofull[b], use & 1);
+        tc::tc_fence_after();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tfree[b]);
+        continue;
+      }
       const int h = h0 + i, t = h - c;
       const uint8_t* hb = hstage0 + (kt & 1) * Cf::HSTAGE;
       tc::mbar_wait(&hfull[kt & 1], (kt >> 1) & 1);
