@@ -11,7 +11,8 @@ Modules
   sa       AA / MAA / SA forward+backward as dense masked attention (Eq. 1-13)
   llsa     LLSA forward+backward, gather form of Eq. 14-15 (+ flattened-mask form)
   stack    n-layer tied-QKV stack with the X_{l+1} = (X_l + Y_l)/2 rule (G12)
-  stream   per-frame incremental LLSA recurrence over a ring of channel-R frames
+  stream   per-frame incremental LLSA recurrence over a ring of channel-R frames, and the
+           incremental SA stack (infer_sa: latency n_layers x R)
   latency  structural receptive-field propagation and Table-3 latency arithmetic
   counts   score-element counts of P:L87 / P:L337-342
 

@@ -133,3 +133,24 @@ def test_llsa_extra_compute_ratio():
     # interior frames: exactly (R+1) * W
     interior = sum(len(oll.window_slots(t, c, T, L, R)) for t in range(50, 150) for c in range(R + 1))
     assert interior == 100 * (R + 1) * (L + R + 1)
+
+
+# ---- infer_sa (NEXT-2): the SA stack run incrementally; latency n_layers x R (Table 3)
+@pytest.mark.parametrize("L,R,n,T", [(3, 1, 2, 16), (4, 2, 3, 40), (0, 3, 2, 25), (5, 0, 3, 20), (6, 2, 1, 9)])
+def test_sa_stream_online_equals_offline(L, R, n, T):
+    x = synth.normal(4, "X", (2, 3, T, 4))
+    y_off = stack.stack_forward(x, L, R, n, "sa")[0]
+    y_on, emitted_at = stream.sa_stream_all(x, L, R, n)
+    np.testing.assert_allclose(y_on, y_off, atol=1e-12, rtol=0)
+    # frame t is emitted at push t + n R (latency builds up with depth), the tail at flush
+    np.testing.assert_array_equal(emitted_at, np.minimum(np.arange(T) + n * R, T))
+
+
+def test_sa_stream_state_is_bounded():
+    L, R, n, T = 4, 2, 3, 80
+    st = stream.SAStream(L, R, n)
+    peak = 0
+    for h in range(T):
+        st.push(synth.normal(5, "X", (1, 1, 4), offset=4 * h))
+        peak = max(peak, st.state_frames())
+    assert peak <= n * (L + R + 1)
