@@ -446,13 +446,14 @@ def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
 
 
 def run_stream(sattn, dev, n_steps=2000, warm=200):
-    """Incremental LLSA inference (infer_llsa): per-frame step latency, 12 layers,
+    """Incremental LLSA (infer_llsa) and SA (infer_sa) inference: per-frame step latency, 12 layers,
     H=12, D=64, (L,R)=(32,8), bf16, one kernel launch per frame for all layers.
     device = CUDA-event time of the step; host = ABI call + synchronize round trip."""
     import torch
     res = {}
-    for nb in (1, 64):
-        st = sattn.LLSAStream(nb, H, D, L, R, NL, dtype=torch.bfloat16, device=dev)
+    for kind, nb in (("llsa", 1), ("llsa", 64), ("sa", 1), ("sa", 64)):
+        cls = sattn.LLSAStream if kind == "llsa" else sattn.SAStream
+        st = cls(nb, H, D, L, R, NL, dtype=torch.bfloat16, device=dev)
         xs = torch.randn(warm + n_steps, nb, H, D, device=dev).to(torch.bfloat16)
         y = torch.empty(nb, H, D, device=dev, dtype=torch.bfloat16)
         for i in range(warm):
@@ -468,13 +469,14 @@ def run_stream(sattn, dev, n_steps=2000, warm=200):
             torch.cuda.synchronize()
             host_us.append((time.perf_counter() - t0) * 1e6)
         dev_us = [a.elapsed_time(b) * 1e3 for a, b in ev]
-        res[f"B{nb}"] = {"device_p50_us": round(float(np.percentile(dev_us, 50)), 2),
+        res[f"B{nb}" if kind == "llsa" else f"sa_B{nb}"] = {"device_p50_us": round(float(np.percentile(dev_us, 50)), 2),
                          "device_p99_us": round(float(np.percentile(dev_us, 99)), 2),
                          "host_p50_us": round(float(np.percentile(host_us, 50)), 2),
                          "host_p99_us": round(float(np.percentile(host_us, 99)), 2),
                          "streams": nb, "steps": n_steps}
         del st
-    res["config"] = f"{NL} layers, H={H}, D={D}, (L,R)=({L},{R}), bf16, one launch per frame"
+    res["config"] = (f"{NL} layers, H={H}, D={D}, (L,R)=({L},{R}), bf16, one launch per frame; B1/B64 = infer_llsa "
+                     f"(latency R = {R} frames), sa_B1/sa_B64 = infer_sa (latency {NL}R = {NL * R} frames)")
     return res
 
 

@@ -136,6 +136,25 @@ sattn_status llsa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, vo
 sattn_status llsa_stream_reset(sattn_stream* s);
 void llsa_stream_destroy(sattn_stream* s);
 
+/* ---------------- incremental SA inference (infer_sa; NEXT-2) ----------
+ * The SA stack of sattn_stack_forward(SATTN_MODE_SA) run frame by frame: layer l
+ * can emit frame t only once its input holds t + R, so after frame h arrives
+ * layer l computes t = h - (l+1) R and the stack emits X_n(h - n R) — latency
+ * n_layers x R frames (Table 3's infer_sa; compare llsa_stream_*).
+ * State: per layer a ring of its last L+R+1 input frames.  sa_stream_step
+ * ingests x_new [B][H][D] for frame h (one kernel launch for all layers) and,
+ * once h >= n_layers R, writes X_n(h - n R) to y_out [B][H][D] and sets
+ * *out_frame = h - n R (else -1, y_out untouched).  sa_stream_flush runs the
+ * remaining n R steps with windows clipped at the last frame and writes frames
+ * T - nR .. T-1 (those >= 0) to y_tail [n R][B][H][D]; *n_out = number written.
+ * Ownership and threading as for llsa_stream_*; the handle type is shared and
+ * sattn_stream_destroy / llsa_stream_destroy free either kind.                  */
+sattn_status sa_stream_create(const sattn_desc* desc, int n_layers, sattn_stream** out);
+sattn_status sa_stream_step(sattn_stream* s, const void* x_new, void* y_out, int64_t* out_frame, void* stream);
+sattn_status sa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void* stream);
+sattn_status sa_stream_reset(sattn_stream* s);
+void sa_stream_destroy(sattn_stream* s);
+
 /* ---------------- misc ---------------------------------------------------------*/
 const char* sattn_last_error(void);      /* thread-local message of the last failure */
 const char* sattn_version(void);

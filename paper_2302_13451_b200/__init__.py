@@ -58,6 +58,11 @@ EXPORTS = {
     "llsa_stream_flush": (_I, [_P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
     "llsa_stream_reset": (_I, [_P]),
     "llsa_stream_destroy": (None, [_P]),
+    "sa_stream_create": (_I, [_PD, _I, ctypes.POINTER(_P)]),
+    "sa_stream_step": (_I, [_P, _P, _P, ctypes.POINTER(ctypes.c_int64), _P]),
+    "sa_stream_flush": (_I, [_P, _P, ctypes.POINTER(ctypes.c_int32), _P]),
+    "sa_stream_reset": (_I, [_P]),
+    "sa_stream_destroy": (None, [_P]),
     "sattn_last_error": (ctypes.c_char_p, []),
     "sattn_version": (ctypes.c_char_p, []),
     "sattn_launch_count": (ctypes.c_int64, []),
@@ -258,6 +263,48 @@ class LLSAStream:
         h = getattr(self, "_h", None)
         if h is not None and _lib is not None:
             _lib.llsa_stream_destroy(h)
+            self._h = None
+
+
+class SAStream:
+    """Incremental SA inference (infer_sa): the SA stack frame by frame, latency n_layers x R
+    (one kernel launch per frame for all layers)."""
+
+    def __init__(self, B, H, D, L, R, n_layers, dtype=torch.float32, scale=None, device="cuda"):
+        self.B, self.H, self.D, self.L, self.R, self.n_layers = B, H, D, L, R, n_layers
+        self.dtype, self.device = dtype, torch.device(device)
+        code = F32 if dtype == torch.float32 else BF16
+        d = make_desc(B, H, 1, D, L, R, code, scale)
+        h = ctypes.c_void_p()
+        _check(lib().sa_stream_create(ctypes.byref(d), n_layers, ctypes.byref(h)), "sa_stream_create")
+        self._h = h
+
+    def step(self, x):
+        """x [B,H,D] -> (frame index, y [B,H,D]) or None while h < n_layers R."""
+        fr = ctypes.c_int64(-1)
+        y = torch.empty((self.B, self.H, self.D), device=self.device, dtype=self.dtype)
+        _check(lib().sa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "sa_stream_step")
+        return None if fr.value < 0 else (fr.value, y)
+
+    def step_into(self, x, y):
+        fr = ctypes.c_int64(-1)
+        _check(lib().sa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "sa_stream_step")
+        return fr.value
+
+    def flush(self):
+        n_tail = max(self.n_layers * self.R, 1)
+        tail = torch.empty((n_tail, self.B, self.H, self.D), device=self.device, dtype=self.dtype)
+        n = ctypes.c_int32(0)
+        _check(lib().sa_stream_flush(self._h, _ptr(tail), ctypes.byref(n), _stream()), "sa_stream_flush")
+        return tail[: n.value]
+
+    def reset(self):
+        _check(lib().sa_stream_reset(self._h), "sa_stream_reset")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.sa_stream_destroy(h)
             self._h = None
 
 

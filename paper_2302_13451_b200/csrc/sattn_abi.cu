@@ -414,6 +414,7 @@ struct sattn_stream {
   bool closed;
   void* raw;
   void* ring;
+  int mode;          // SATTN_MODE_LLSA (llsa_stream_*) or SATTN_MODE_SA (sa_stream_*)
 };
 
 namespace {
@@ -445,9 +446,107 @@ sattn_status stream_launch(sattn_stream* s, const void* x, void* y, long long h,
     return after_launch("llsa_stream_step");
   });
 }
+sattn_status sa_stream_launch(sattn_stream* s, const void* x, void* y, long long h, long long last, cudaStream_t st) {
+  SAStreamArgs a{};
+  a.x_new = x;
+  a.ring = s->ring;
+  a.y_out = y;
+  a.h = h;
+  a.last = last;
+  a.n_layers = s->n_layers;
+  a.L = s->d.L;
+  a.R = s->d.R;
+  a.BH = (int)(s->d.B * s->d.H);
+  a.scale_log2 = eff_scale(&s->d) * kLog2e;
+  size_t smem = sa_stream_smem_bytes((int)s->d.D, a.L, a.R, a.n_layers, elem_size(s->d.dtype));
+  a.preload = 1;
+  if (smem > 160 * 1024) {
+    a.preload = 0;
+    smem = sa_stream_smem_bytes((int)s->d.D, a.L, a.R);
+  }
+  if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
+  return dispatch(s->d.D, s->d.dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
+    constexpr int D = decltype(dc)::value;
+    using T = decltype(tv);
+    set_smem(sa_stream_step_kernel<D, T>, smem);
+    sa_stream_step_kernel<D, T><<<a.BH, 128, smem, st>>>(a);
+    return after_launch("sa_stream_step");
+  });
+}
 }  // namespace
 
 extern "C" {
+
+sattn_status sa_stream_create(const sattn_desc* d, int n_layers, sattn_stream** out) {
+  if (!out) return fail(SATTN_EARG, "out is NULL");
+  *out = nullptr;
+  sattn_desc dd = *d;
+  dd.T = 1;
+  sattn_status r = validate(&dd);
+  if (r != SATTN_OK) return r;
+  if (n_layers < 1) return fail(SATTN_EARG, "n_layers must be >= 1");
+  sattn_stream* s = new (std::nothrow) sattn_stream{};
+  if (!s) return fail(SATTN_ECUDA, "out of host memory");
+  s->d = dd;
+  s->n_layers = n_layers;
+  s->mode = SATTN_MODE_SA;
+  const size_t ring_b = (size_t)n_layers * d->B * d->H * (d->L + d->R + 1) * d->D * elem_size(d->dtype);
+  cudaError_t e = cudaMalloc(&s->ring, ring_b);
+  if (e == cudaSuccess) e = cudaMemset(s->ring, 0, ring_b);
+  if (e != cudaSuccess) {
+    cudaFree(s->ring);
+    delete s;
+    return fail(SATTN_ECUDA, "stream state allocation: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return SATTN_OK;
+}
+
+sattn_status sa_stream_step(sattn_stream* s, const void* x_new, void* y_out, int64_t* out_frame, void* stream) {
+  if (!s || !x_new || !y_out) return fail(SATTN_EARG, "NULL pointer");
+  if (s->mode != SATTN_MODE_SA) return fail(SATTN_EARG, "not an SA stream handle");
+  if (s->closed) return fail(SATTN_ESTATE, "stream already flushed (call sa_stream_reset)");
+  const long long h = s->h, lat = (long long)s->n_layers * s->d.R;
+  sattn_status r = sa_stream_launch(s, x_new, y_out, h, h, (cudaStream_t)stream);
+  if (r != SATTN_OK) return r;
+  s->h = h + 1;
+  s->n_in = h + 1;
+  if (out_frame) *out_frame = h >= lat ? h - lat : -1;
+  return SATTN_OK;
+}
+
+sattn_status sa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void* stream) {
+  if (!s || !y_tail) return fail(SATTN_EARG, "NULL pointer");
+  if (s->mode != SATTN_MODE_SA) return fail(SATTN_EARG, "not an SA stream handle");
+  if (s->closed) return fail(SATTN_ESTATE, "stream already flushed");
+  s->closed = true;
+  const long long T = s->n_in, lat = (long long)s->n_layers * s->d.R;
+  const size_t frame_b = s->d.B * s->d.H * s->d.D * elem_size(s->d.dtype);
+  int cnt = 0;
+  for (long long h = T; h < T + lat; ++h) {
+    if (h - lat < 0) continue;
+    sattn_status r = sa_stream_launch(s, nullptr, static_cast<char*>(y_tail) + cnt * frame_b, h, T - 1,
+                                      (cudaStream_t)stream);
+    if (r != SATTN_OK) return r;
+    ++cnt;
+  }
+  if (n_out) *n_out = cnt;
+  return SATTN_OK;
+}
+
+sattn_status sa_stream_reset(sattn_stream* s) {
+  if (!s) return fail(SATTN_EARG, "NULL handle");
+  s->h = s->n_in = 0;
+  s->closed = false;
+  return SATTN_OK;
+}
+
+void sa_stream_destroy(sattn_stream* s) {
+  if (!s) return;
+  cudaFree(s->raw);
+  cudaFree(s->ring);
+  delete s;
+}
 
 sattn_status llsa_stream_create(const sattn_desc* d, int n_layers, sattn_stream** out) {
   if (!out) return fail(SATTN_EARG, "out is NULL");
@@ -461,6 +560,7 @@ sattn_status llsa_stream_create(const sattn_desc* d, int n_layers, sattn_stream*
   if (!s) return fail(SATTN_ECUDA, "out of host memory");
   s->d = dd;
   s->n_layers = n_layers;
+  s->mode = SATTN_MODE_LLSA;
   const size_t es = elem_size(d->dtype);
   const size_t BH = d->B * d->H;
   const size_t raw_b = BH * (d->R + 1) * d->D * es;
@@ -481,6 +581,7 @@ sattn_status llsa_stream_create(const sattn_desc* d, int n_layers, sattn_stream*
 
 sattn_status llsa_stream_step(sattn_stream* s, const void* x_new, void* y_out, int64_t* out_frame, void* stream) {
   if (!s || !x_new || !y_out) return fail(SATTN_EARG, "NULL pointer");
+  if (s->mode != SATTN_MODE_LLSA) return fail(SATTN_EARG, "not an LLSA stream handle");
   if (s->closed) return fail(SATTN_ESTATE, "stream already flushed (call llsa_stream_reset)");
   const long long h = s->h;
   sattn_status r = stream_launch(s, x_new, y_out, h, h, (cudaStream_t)stream);

@@ -171,3 +171,146 @@ inline size_t stream_smem_bytes(int D, int L, int R, int n_layers = 0, size_t el
 }
 
 }  // namespace sattn
+
+namespace sattn {
+
+// ------------------------------------------------------------------------------------------
+// One incremental SA step (infer_sa).  CTA = one (batch, head).
+// After frame h arrives, layer l (0-based) computes its output at t_l = h - (l+1) R from the
+// window [t_l - L, t_l + R] of its input; the newest window frame t_l + R = h - l R is the one
+// the layer below produced in this same step (layer 0: x_h), the older ones come from the
+// layer's ring of its last L + R + 1 input frames.  X_{l+1}(t_l) = (X_l(t_l) + Y_l(t_l)) / 2
+// (G12), rounded like the offline stack; the stack emits X_n(h - n R): latency n R frames.
+// ------------------------------------------------------------------------------------------
+struct SAStreamArgs {
+  const void* x_new;   // [BH][D] or nullptr (flush step)
+  void* ring;          // [n_layers][BH][L+R+1][D], slot = frame mod (L+R+1)
+  void* y_out;         // [BH][D] or nullptr
+  long long h, last;   // step and last valid frame
+  int n_layers, L, R, BH;
+  float scale_log2;
+  int preload;         // 1: every layer's ring rows are staged into shared memory at the start
+};
+
+template <int D, typename T>
+__global__ void __launch_bounds__(128) sa_stream_step_kernel(SAStreamArgs a) {
+  constexpr int SD = D + 1;
+  extern __shared__ float sm[];
+  const int L = a.L, R = a.R, W = L + R + 1;
+  float* win = sm;                   // [W][SD]
+  float* cur = win + W * SD;         // [SD] newest input frame of the current layer
+  float* P = cur + SD;               // [W]
+  T* rings = reinterpret_cast<T*>(reinterpret_cast<uintptr_t>(P + W + 3) & ~uintptr_t(15));   // [n][W-1][D]
+  const int bh = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const long long h = a.h, last = a.last;
+  const int NR = W;
+
+  // newest input of layer 0: x_h
+  bool cur_ok = a.x_new != nullptr && h <= last;
+  if (cur_ok) {
+    const T* x = reinterpret_cast<const T*>(a.x_new) + (long long)bh * D;
+    for (int d = tid; d < D; d += nt) cur[d] = to_f(x[d]);
+  }
+  // ring slot of frame u = (h mod NR) + (u - h) mod NR: one 64-bit modulo per step, not per element
+  const int hm = (int)(h % NR);
+  auto slot_of = [&](long long u) { int sl = (hm + (int)((u - h) % NR)) % NR; return sl < 0 ? sl + NR : sl; };
+  // stage every layer's ring rows: window rows i in [0, W-1) of layer l (frames t_l - L + i),
+  // 16-byte copies when rows are 16-byte multiples
+  if (a.preload) {
+    constexpr bool VEC = (D * sizeof(T)) % 16 == 0;
+    constexpr int PER = VEC ? (int)(D * sizeof(T) / 16) : D;
+    const int n = a.n_layers * (W - 1) * PER;
+    for (int idx = tid; idx < n; idx += nt) {
+      const int ch = idx % PER, i = (idx / PER) % (W - 1), l = idx / (PER * (W - 1));
+      const long long u = h - (long long)(l + 1) * R - L + i;
+      const bool ok = u >= 0 && u <= last;
+      const T* src = reinterpret_cast<const T*>(a.ring) + (((long long)l * a.BH + bh) * NR + (ok ? slot_of(u) : 0)) * D;
+      T* dst = rings + ((long long)l * (W - 1) + i) * D;
+      if (VEC) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = reinterpret_cast<const uint4*>(src)[ch];
+        reinterpret_cast<uint4*>(dst)[ch] = v;
+      } else {
+        dst[ch] = ok ? src[ch] : from_f<T>(0.f);
+      }
+    }
+  }
+  __syncthreads();
+  for (int l = 0; l < a.n_layers; ++l) {
+    T* ring = reinterpret_cast<T*>(a.ring) + ((long long)l * a.BH + bh) * NR * D;
+    const long long fn = h - (long long)l * R;          // this layer's newest input frame (= cur)
+    const long long t = fn - R;                          // the frame it computes
+    const bool run = t >= 0 && t <= last;
+    if (run) {
+      for (int idx = tid; idx < W * D; idx += nt) {
+        const int i = idx / D, d = idx % D;
+        const long long u = t - L + i;
+        float x = 0.f;
+        if (u >= 0 && u <= last) {
+          if (i == W - 1) x = cur[d];                    // u = t + R = fn
+          else x = a.preload ? to_f(rings[((long long)l * (W - 1) + i) * D + d]) : to_f(ring[slot_of(u) * D + d]);
+        }
+        win[i * SD + d] = x;
+      }
+    }
+    __syncthreads();
+    // the newest frame joins the ring (its slot held frame fn - W, outside every later window)
+    if (cur_ok && fn >= 0) {
+      const int sl = slot_of(fn);
+      for (int d = tid; d < D; d += nt) ring[sl * D + d] = from_f<T>(cur[d]);
+    }
+    if (run) {
+      // scores (log2 domain) of the query X_l(t) = window row L
+      for (int i = tid; i < W; i += nt) {
+        const long long u = t - L + i;
+        float s = neg_inf();
+        if (u >= 0 && u <= last) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 16
+          for (int d = 0; d < D; ++d) acc[d & 3] = fmaf(win[L * SD + d], win[i * SD + d], acc[d & 3]);
+          s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * a.scale_log2;
+        }
+        P[i] = s;
+      }
+      __syncthreads();
+      if (tid < 32) {
+        float m = neg_inf();
+        for (int i = tid; i < W; i += 32) m = fmaxf(m, P[i]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        float sum = 0.f;
+        for (int i = tid; i < W; i += 32) {
+          const float e = exp2f(P[i] - m);
+          P[i] = e;
+          sum += e;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const float inv = 1.f / sum;
+        for (int i = tid; i < W; i += 32) P[i] *= inv;
+      }
+      __syncthreads();
+      // value sum and the block rule; the result is the next layer's newest input frame
+      for (int d = tid; d < D; d += nt) {
+        float y4[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int i = 0; i < W; ++i) y4[i & 3] = fmaf(P[i], win[i * SD + d], y4[i & 3]);
+        const float o = to_f(from_f<T>((y4[0] + y4[1]) + (y4[2] + y4[3])));
+        cur[d] = to_f(from_f<T>(0.5f * (win[L * SD + d] + o)));
+      }
+    }
+    cur_ok = run;
+    __syncthreads();
+  }
+  const long long te = h - (long long)a.n_layers * R;
+  if (a.y_out && cur_ok && te >= 0 && te <= last) {
+    T* y = reinterpret_cast<T*>(a.y_out) + (long long)bh * D;
+    for (int d = tid; d < D; d += nt) y[d] = from_f<T>(cur[d]);
+  }
+}
+
+inline size_t sa_stream_smem_bytes(int D, int L, int R, int n_layers = 0, size_t elem = 4) {
+  const int W = L + R + 1, SD = D + 1;
+  return sizeof(float) * ((size_t)W * SD + SD + W) + 32 + (size_t)n_layers * (W - 1) * D * elem;
+}
+
+}  // namespace sattn

@@ -98,3 +98,33 @@ def test_stream_matches_oracle_recurrence_and_offline(dt, tol, n):
         assert np.abs(host(ys) - Y_or).max() <= tol * mag
     y_off, _ = s.stack_forward(tx, L, R, n, s.MODE_LLSA)
     assert np.abs(host(ys) - host(y_off[R])).max() <= tol * mag
+
+
+@pytest.mark.parametrize("dt,tol,n", [(torch.float32, 1e-5, 12), (torch.bfloat16, 2e-2, 2), (torch.bfloat16, 2e-2, 12)])
+def test_sa_stream_matches_oracle_recurrence_and_offline(dt, tol, n):
+    # infer_sa (NEXT-2): frame t leaves the n-layer SA stack at push t + n R (latency n R),
+    # against the oracle's own SA recurrence (fp32 at 12 layers, bf16 at 2) and the offline GPU
+    # SA stack (same rounding points) — gates as for the LLSA stream above
+    s = sattn()
+    B, H, T, D, L, R = 1, 2, 200, 64, 32, 8
+    x = synth.normal(7, "X", (B, H, T, D))
+    xr = synth.round_to(x, "f32" if dt == torch.float32 else "bf16")
+    tx = dev(xr, dt)
+    st = s.SAStream(B, H, D, L, R, n, dtype=dt)
+    ys = torch.full((B, H, T, D), float("nan"), device="cuda", dtype=dt)
+    first = None
+    for h in range(T):
+        r = st.step(tx[:, :, h].contiguous())
+        if r is not None:
+            ys[:, :, r[0]] = r[1]
+            first = h if first is None else first
+    tail = st.flush()
+    assert tail.shape[0] == min(n * R, T)
+    ys[:, :, T - tail.shape[0]:] = tail.permute(1, 2, 0, 3)
+    assert first == (n * R if n * R < T else None)      # first emission after n R + 1 pushes
+    Y_or, _ = oracle.stream.sa_stream_all(xr, L, R, n)
+    mag = max(1.0, float(np.abs(Y_or).max()))
+    if dt == torch.float32 or n <= 2:
+        assert np.abs(host(ys) - Y_or).max() <= tol * mag
+    y_off, _ = s.stack_forward(tx, L, R, n, s.MODE_SA)
+    assert np.abs(host(ys) - host(y_off)).max() <= tol * mag
