@@ -310,6 +310,14 @@ def run_gpu(args):
         except Exception as e:   # the headline line must not depend on this sub-measurement
             hour = {"error": f"{type(e).__name__}: {e}"[:300]}
 
+    enc = None
+    if not args.no_encoder and world == 1:
+        torch.cuda.empty_cache()
+        try:
+            enc = run_encoder(args, dev)
+        except Exception as e:
+            enc = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     stream_lat = None
     if not args.no_stream:
         stream_lat = run_stream(sattn, dev)
@@ -331,7 +339,7 @@ def run_gpu(args):
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
            "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa,
-           "hour": hour, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
+           "hour": hour, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
 
@@ -443,6 +451,47 @@ def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
             "workload": f"hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), {n_layers} layers x (SA fwd + bwd), "
                         f"time-sharded x{world} (halo exchange {'NCCL P2P' if world > 1 else 'none'}), eager calls",
             "frames_per_rank": t1 - t0}
+
+
+def run_encoder(args, dev):
+    """NEXT-3: a 12-layer wav2vec2/HuBERT-base encoder (d=768, H=12, FFN 3072, post-LN, bf16)
+    training step (forward + backward, no optimizer) at B=8, T=1750, with the repo's SA
+    attention vs the same layers with masked acausal attention (torch SDPA + band mask).
+    Everything but the attention is torch / cuBLAS."""
+    import torch
+    from paper_2302_13451_b200 import encoder
+    out = {}
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn(B, T, 768, device=dev, generator=g).to(torch.bfloat16)
+    dy = torch.randn(B, T, 768, device=dev, generator=g).to(torch.bfloat16)
+    for name, cls in (("sa", encoder.SAEncoderLayer), ("maa", encoder.MaskedEncoderLayer)):
+        torch.manual_seed(0)
+        layers = torch.nn.Sequential(*[cls(L=L, R=R) for _ in range(NL)]).to(dev).to(torch.bfloat16)
+
+        def step():
+            xi = x.detach().requires_grad_(True)
+            layers(xi).backward(dy)
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        torch.cuda.reset_peak_memory_stats()
+        k = 3
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k):
+            step()
+        a1.record()
+        torch.cuda.synchronize()
+        ms = a0.elapsed_time(a1) / k
+        out[name] = {"ms_per_step": round(ms, 3), "frames_per_s": round(B * T / (ms / 1e3), 1),
+                     "peak_mem_gb": round(torch.cuda.max_memory_allocated() / 2**30, 2)}
+        del layers
+        torch.cuda.empty_cache()
+    out["speedup_vs_maa"] = round(out["maa"]["ms_per_step"] / out["sa"]["ms_per_step"], 3)
+    out["workload"] = (f"{NL} x wav2vec2-base encoder layer (d=768, H=12, FFN 3072, post-LN), B={B}, T={T}, "
+                       f"(L,R)=({L},{R}), bf16, fwd+bwd (no optimizer); projections/FFN/LN are torch (cuBLAS)")
+    return out
 
 
 def run_stream(sattn, dev, n_steps=2000, warm=200):
@@ -596,6 +645,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
     ap.add_argument("--no-hour", action="store_true")
+    ap.add_argument("--no-encoder", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
