@@ -120,3 +120,50 @@ def sa_backward_tsharded(q, k, v, o, lse, do, L: int, R: int, group=None, align:
     dq, dk, dv = attn_bwd(q_e, k_e, v_e, o_e, lse_e.squeeze(-1).contiguous(), do_e, L, R)
     sl = slice(nl, nl + T_loc)
     return dq[..., sl, :].contiguous(), dk[..., sl, :].contiguous(), dv[..., sl, :].contiguous()
+
+
+# ------------------------------------------------------------------ deep halo (NEXT-4)
+# A whole n-layer stack on a time shard with ONE exchange instead of one per layer: an output
+# frame t of the stack depends on input frames [t - n (L + R), t + n R] (each SA layer reaches
+# L back and R ahead; an LLSA layer's band reaches L + R back, reading G6), so a
+# slab extended by that deep halo reproduces the local rows exactly; the backward's dX_0(u)
+# reaches dY over [u - n R, u + n L] and the activations around them, so twice the forward
+# halo on both sides (SURVEY §8(c) time-sharding pins: per-layer margins L + R forward and
+# 2 (L + R) backward, times n_layers).  The trade: recompute of the halo frames in every layer
+# against n - 1 fewer exchanges (for the hour-long stream at 8 ranks: 480 of 22,500 frames).
+
+def _stack_fwd_default(x, L, R, n, mode):
+    import paper_2302_13451_b200 as s
+    return s.stack_forward(x, L, R, n, mode)[0]
+
+
+def _stack_bwd_default(x, dy, L, R, n, mode):
+    import paper_2302_13451_b200 as s
+    _, saved = s.stack_forward(x, L, R, n, mode)
+    return s.stack_backward(x, saved, dy, L, R, n, mode)
+
+
+def stack_forward_tsharded(x, L: int, R: int, n_layers: int, mode: int = 0, group=None, align: int = 128,
+                           stack_fwd=None):
+    """x: this rank's slab [B, H, T_loc, D].  Returns this rank's rows of the n-layer stack
+    output (SA: [B, H, T_loc, D]; LLSA mode 1: [C, B, H, T_loc, D])."""
+    stack_fwd = stack_fwd or _stack_fwd_default
+    T_loc = x.shape[-2]
+    back = n_layers * (L + R) if mode == 1 else n_layers * L
+    hl, hr = _halo(back, align, T_loc, group), _halo(n_layers * R, align, T_loc, group)
+    x_e, nl = exchange_halo(x, hl, hr, group)
+    y = stack_fwd(x_e, L, R, n_layers, mode)
+    return y[..., nl:nl + T_loc, :].contiguous()
+
+
+def stack_backward_tsharded(x, dy, L: int, R: int, n_layers: int, mode: int = 0, group=None, align: int = 128,
+                            stack_bwd=None):
+    """x: this rank's input slab [B, H, T_loc, D]; dy: its rows of dL/dY (SA [B, H, T_loc, D],
+    LLSA [C, B, H, T_loc, D]).  Returns this rank's rows of dL/dX_0."""
+    stack_bwd = stack_bwd or _stack_bwd_default
+    T_loc = x.shape[-2]
+    h = _halo(2 * n_layers * (L + R), align, T_loc, group)
+    x_e, nl = exchange_halo(x, h, h, group)
+    dy_e, _ = exchange_halo(dy, h, h, group)
+    dx = stack_bwd(x_e, dy_e, L, R, n_layers, mode)
+    return dx[..., nl:nl + T_loc, :].contiguous()

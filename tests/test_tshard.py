@@ -79,3 +79,39 @@ def test_shard_bounds_cover_and_align():
         assert b[0][0] == 0 and b[-1][1] == T
         assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
         assert all(t0 % align == 0 for t0, _ in b)
+
+
+def _stack_worker(rank, world, port, T, L, R, n, mode, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2302_13451_b200 import tshard
+    from oracle import stack as ostack
+    mname = "llsa" if mode == 1 else "sa"
+    x = synth.normal(8, "X", (1, 2, T, 4))
+    dy = synth.normal(9, "dY", ((R + 1,) if mode == 1 else ()) + (1, 2, T, 4))
+    fwd = lambda xe, L_, R_, n_, m_: torch.from_numpy(ostack.stack_forward(xe.numpy(), L_, R_, n_, mname)[0])  # noqa
+    bwd = lambda xe, dye, L_, R_, n_, m_: torch.from_numpy(  # noqa: E731
+        ostack.stack_backward(xe.numpy(), dye.numpy(), L_, R_, n_, mname))
+    t0, t1 = tshard.shard_bounds(T, world, rank, 1)
+    xl = torch.from_numpy(x[..., t0:t1, :].copy())
+    dyl = torch.from_numpy(dy[..., t0:t1, :].copy())
+    y = tshard.stack_forward_tsharded(xl, L, R, n, mode, align=1, stack_fwd=fwd)
+    dx = tshard.stack_backward_tsharded(xl, dyl, L, R, n, mode, align=1, stack_bwd=bwd)
+    Y = ostack.stack_forward(x, L, R, n, mname)[0]
+    DX = ostack.stack_backward(x, dy, L, R, n, mname)
+    out[rank] = max(float(np.abs(y.numpy() - Y[..., t0:t1, :]).max()),
+                    float(np.abs(dx.numpy() - DX[..., t0:t1, :]).max()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T,L,R,n,mode", [(2, 60, 3, 1, 2, 0), (3, 90, 2, 2, 3, 0), (2, 64, 3, 2, 2, 1),
+                                                 (3, 96, 2, 1, 2, 1)])
+def test_deep_halo_stack_equals_unsharded(world, T, L, R, n, mode):
+    # NEXT-4: the n-layer stack (SA and LLSA) on time shards with one deep-halo exchange per
+    # stack reproduces the unsharded stack rows, forward and backward (CPU oracle stack injected)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_stack_worker, args=(world, _free_port(), T, L, R, n, mode, out), nprocs=world, join=True)
+    assert sorted(out.keys()) == list(range(world))
+    assert max(out.values()) < 1e-12, dict(out)
