@@ -18,7 +18,7 @@
 
 namespace sattn {
 
-constexpr int kStF = 16;          // horizons per CTA
+constexpr int kStF = 8;           // horizons per CTA
 constexpr int kStRS = 144;        // padded row stride (bytes)
 constexpr int kStTile = kStF * kStRS + 16;   // one channel's rows (+ skew)
 
@@ -69,7 +69,7 @@ __device__ __forceinline__ float st_ex2(float x) {
 }
 
 template <bool DX>
-__global__ void __launch_bounds__(256, 2) llsa_bwd_stair(StairArgs a) {
+__global__ void __launch_bounds__(256, 3) llsa_bwd_stair(StairArgs a) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int R = a.R, C = R + 1, T = a.T;
   const int h0 = blockIdx.x * kStF, bh = blockIdx.y;
