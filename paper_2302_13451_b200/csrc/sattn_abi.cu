@@ -594,6 +594,7 @@ sattn_status llsa_stream_step(sattn_stream* s, const void* x_new, void* y_out, i
 
 sattn_status llsa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void* stream) {
   if (!s || !y_tail) return fail(SATTN_EARG, "NULL pointer");
+  if (s->mode != SATTN_MODE_LLSA) return fail(SATTN_EARG, "not an LLSA stream handle");
   if (s->closed) return fail(SATTN_ESTATE, "stream already flushed");
   s->closed = true;
   const long long T = s->n_in, R = s->d.R;

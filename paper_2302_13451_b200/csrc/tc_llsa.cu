@@ -36,6 +36,7 @@ constexpr int kRmax = 8;
 struct LlsaArgs {
   int T, L, R, C, BH;
   int bcast;                     // inputs are one plane read as every channel (layer 1)
+  int skew;                      // stair K/V and item Q staged by one skewed 4-D box each (see map_skew)
   float scale, scale_log2;
   float* LSE;                    // [C][BH][T]
   bf16* O;                       // [C][BH][T][64] (direct stores of the first tile)
@@ -122,15 +123,24 @@ __global__ void __launch_bounds__(320, 1)
         tc::mbar_expect_tx(&hfull[hs], 2 * Cf::BB + 2 * R * Cf::SB);
         tc::tma_load_4d(hb, &tmKb, &hfull[hs], 0, h0 - R - L, bh, chan(R));
         tc::tma_load_4d(hb + Cf::BB, &tmVb, &hfull[hs], 0, h0 - R - L, bh, chan(R));
-        for (int cp = 0; cp < R; ++cp) {
-          tc::tma_load_4d(hb + 2 * Cf::BB + cp * Cf::SB, &tmKs, &hfull[hs], 0, h0 - cp, bh, chan(cp));
-          tc::tma_load_4d(hb + 2 * Cf::BB + (kRmax + cp) * Cf::SB, &tmVs, &hfull[hs], 0, h0 - cp, bh, chan(cp));
+        if (a.skew) {   // rows (h0 - c' + i, c') for all c' < R: one box each for K and V
+          tc::tma_load_4d(hb + 2 * Cf::BB, &tmKs, &hfull[hs], 0, h0, 0, bh);
+          tc::tma_load_4d(hb + 2 * Cf::BB + kRmax * Cf::SB, &tmVs, &hfull[hs], 0, h0, 0, bh);
+        } else {
+          for (int cp = 0; cp < R; ++cp) {
+            tc::tma_load_4d(hb + 2 * Cf::BB + cp * Cf::SB, &tmKs, &hfull[hs], 0, h0 - cp, bh, chan(cp));
+            tc::tma_load_4d(hb + 2 * Cf::BB + (kRmax + cp) * Cf::SB, &tmVs, &hfull[hs], 0, h0 - cp, bh, chan(cp));
+          }
         }
         for (int ii = 0; ii < NI; ++ii, ++k) {
           const int qs = k % Cf::NSQ;
           if (k >= Cf::NSQ) tc::mbar_wait(&qempty[qs], ((k - Cf::NSQ) / Cf::NSQ) & 1);
           uint8_t* qb = qstage0 + qs * Cf::QB;
           tc::mbar_expect_tx(&qfull[qs], Cf::QB);
+          if (a.skew) {   // rows (h0 - c + i, c) of the item's 4 channels (channels >= C zero-filled)
+            tc::tma_load_4d(qb, &tmQ, &qfull[qs], 0, h0, 4 * ii, bh);
+            continue;
+          }
           for (int w = 0; w < 4; ++w) {
             const int c = 4 * ii + w;
             // channels >= C: a box entirely past the end of the sequence (zero-filled)
@@ -409,6 +419,23 @@ int num_sms() {
   return n;
 }
 
+// [C][BH][T][64] bf16 viewed so that box row i of channel c is frame y + i - c: dims
+// (64, T + R, C, BH) with the channel stride skewed by one frame, (BH T - 1) x 128 B.  One box
+// {64, rows, nch, 1} at (0, y, c0, bh) then stages the LLSA staircase diagonal (or an item's
+// channel rows) in a single TMA copy.  Coordinates past the frame bounds of the diagonal read
+// neighbouring planes (finite data); the kernel masks those slots (P = 0).
+bool map_skew(CUtensorMap* m, const void* base, int T, int BH, int C, int R, int rows, int nch) {
+  EncodeTiledFn enc = encoder();
+  if (!enc || (long long)BH * T - 1 < (long long)T + R) return false;
+  cuuint64_t dims[4] = {64, (cuuint64_t)(T + R), (cuuint64_t)C, (cuuint64_t)BH};
+  cuuint64_t strides[3] = {128, ((cuuint64_t)BH * T - 1) * 128, (cuuint64_t)T * 128};
+  cuuint32_t box[4] = {64, (cuuint32_t)rows, (cuuint32_t)nch, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NB>
 sattn_status launch(const AttnArgs& a, cudaStream_t st) {
   using Cf = LCfg<NB>;
@@ -419,7 +446,17 @@ sattn_status launch(const AttnArgs& a, cudaStream_t st) {
       !map4(&mvb, a.V, a.T, a.BH, Cin, NB) || !map4(&mks, a.K, a.T, a.BH, Cin, kHT) ||
       !map4(&mvs, a.V, a.T, a.BH, Cin, kHT) || !map4(&mo, a.Out, a.T, a.BH, C, kHT))
     return SATTN_ECUDA;
+  // skewed single-box staging of the staircase and of each item's Q rows (dense inputs only:
+  // a broadcast plane would need a negative channel stride); falls back to per-channel boxes
+  bool skew = a.in_cs != 0 && !getenv("SATTN_LLSA_NOSKEW");
+  if (skew) {
+    CUtensorMap sq, sk, sv;
+    skew = map_skew(&sq, a.Q, a.T, a.BH, C, a.R, kHT, 4) && map_skew(&sk, a.K, a.T, a.BH, C, a.R, kHT, a.R) &&
+           map_skew(&sv, a.V, a.T, a.BH, C, a.R, kHT, a.R);
+    if (skew) { mq = sq; mks = sk; mvs = sv; }
+  }
   LlsaArgs la{};
+  la.skew = skew ? 1 : 0;
   la.T = a.T; la.L = a.L; la.R = a.R; la.C = C; la.BH = a.BH;
   la.bcast = a.in_cs == 0;
   la.scale = a.scale; la.scale_log2 = a.scale_log2;
