@@ -3,7 +3,7 @@
 d_k = 64, N_T = 1000 frames, H in {8, 16} heads, receptive field W = A + B + 1 = 10 ... 490 in
 steps of 10 (look-back B = ceil((W-1)/2), look-ahead A = floor((W-1)/2)), 5 repeats, mean.
 For each point: peak device memory of one SA forward + backward through the C ABI (bf16; the
-tensor-core kernels for W <= 49, the CUDA-core kernels beyond) per training vector (frame),
+tensor-core kernels for W <= 65, the CUDA-core kernels beyond) per training vector (frame),
 and its time; next to masked acausal attention (MAA) as PyTorch computes it (dense T x T scores,
 boolean band mask, softmax, autograd), which is what the paper compares against.  Writes
 profiles/r1/fig5.json and prints a markdown table.  Inputs are synthetic (iid N(0,1))."""
@@ -64,7 +64,7 @@ def run(H, B=8):
         m_sa, t_sa = measure(sa)
         m_maa, t_maa = measure(maa)
         frames = B * T
-        rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 49 else "ffma",
+        rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 65 else "ffma",
                      "sa_bytes_per_frame": m_sa / frames, "maa_bytes_per_frame": m_maa / frames,
                      "sa_ms": t_sa, "maa_ms": t_maa})
         del mask
