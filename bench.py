@@ -233,7 +233,10 @@ def run_gpu(args):
         for l in range(NL):
             for j, src in enumerate((Qs, Ks, Vs, dOs)):
                 hin[l][j].copy_(src[l])
-        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        # H2D on copy stream(s) (layers alternate when more than one), D2H on another
+        n_in = int(os.environ.get("SATTN_E2E_H2D_STREAMS", "1"))   # 2-3 measured no faster (PCIe-bound)
+        s_ins = [torch.cuda.Stream(dev) for _ in range(n_in)]
+        s_out = torch.cuda.Stream(dev)
         ev = lambda: torch.cuda.Event()  # noqa: E731
         # two device buffer sets, alternating by step: the H2D of step i+1 need not wait for
         # step i's compute to release its inputs
@@ -248,6 +251,7 @@ def run_gpu(args):
             q_, k_, v_, do_, o_, lse_, dq_, dk_, dv_ = sets[p_]
             landed = []
             for l in range(NL):
+                s_in = s_ins[l % n_in]
                 with torch.cuda.stream(s_in):
                     if used[p_][l] is not None:
                         s_in.wait_event(used[p_][l])
@@ -276,7 +280,8 @@ def run_gpu(args):
         n_e2e = max(2, min(args.steps, 5))
         a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
         a0.record(stream)
-        s_in.wait_event(a0)          # the first copies start after the start event
+        for s_in in s_ins:
+            s_in.wait_event(a0)      # the first copies start after the start event
         for _ in range(n_e2e):
             e2e_step()
         for d in drained[0] + drained[1]:   # the end event follows every copy of the last steps
@@ -291,8 +296,8 @@ def run_gpu(args):
         el = 2 * B * H * T * D
         e2e = {"value": round(world * B * T * n_e2e / (e_ms / 1e3), 1), "unit": UNIT,
                "h2d_bytes_per_step": 4 * NL * el, "d2h_bytes_per_step": 3 * NL * el, "steps": n_e2e,
-               "pipeline": "layer-granular H2D / compute / D2H on three streams (CUDA events), two device "
-                           "buffer sets alternating by step"}
+               "pipeline": f"layer-granular H2D ({n_in} copy streams) / compute / D2H streams (CUDA events), two "
+                           "device buffer sets alternating by step"}
         del hin, hout, sets
 
     # ---------------- LLSA step (same shape, C = R+1 channels), reported alongside
