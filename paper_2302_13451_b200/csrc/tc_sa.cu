@@ -898,6 +898,251 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// backward K2 with M = 64 sub-tiles (SATTN_K2=m64): the 128-key tile of sa_bwd_dkdv_tc as two
+// 64-key halves whose accumulators share TMEM columns.  An M = 64 tcgen05 accumulator uses 16
+// of each TMEM subpartition's 32 lanes; half A (keys u0 .. u0+63) sits at lane offset 0, half
+// B (keys u0+64 ..) at lane offset 16 of the same columns, so a warp's lanes 0-15 / 16-31 hold
+// one row of each half.  A half's query window is 63 + W -> NQH = 16-rounded columns (112 for
+// (32,8)) instead of 176 for the full tile: 36 % less MMA work and TMEM per key, which leaves
+// room for three S/dP buffers (3 x NQH + dV 64 + dK 64 <= 512).
+// ------------------------------------------------------------------------------------------
+template <int CW> struct M64Cfg {
+  static constexpr int NQ = nk_of(CW);                       // the stage's query window (both halves)
+  static constexpr int NQH = ((CW - 32 + 63) + 15) / 16 * 16;   // one half's window: 63 + W, W <= CW - 31
+  static constexpr int CWH = (CW - 16 + 7) / 8 * 8;           // strip of a 16-row group: 16 + W - 1
+  static constexpr int NX = 3;
+  static_assert(64 + NQH <= NQ + 16 && NX * NQH + 128 <= 512, "window / TMEM layout");
+};
+
+template <int CW>
+__global__ void __launch_bounds__(320, 1)
+    sa_bwd_dkdv_m64_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                       const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
+                       const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel, TcArgs a) {
+  using C = DkvCfg<CW>;
+  using M = M64Cfg<CW>;
+  constexpr int NS = C::NS, NQH = M::NQH, CWH = M::CWH, NX = M::NX;
+  constexpr uint32_t LB = 16u << 16;                 // TMEM lane offset of half B
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage0 = smem;                       // [K | V | Q | dO | LSE | delta]
+  uint8_t* obuf0 = smem + NS * C::STAGE;        // per warpgroup: [dV | dK] staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * C::KB);
+  uint64_t* full = bars;              // [NS]
+  uint64_t* empty = full + NS;        // [NS]
+  uint64_t* sfull = empty + NS;       // [NX]
+  uint64_t* xfree = sfull + NX;       // [NX] (128)
+  uint64_t* dpfull = xfree + NX;      // [NX]
+  uint64_t* pdsfull = dpfull + NX;    // [NX] (128)
+  uint64_t* kvfull = pdsfull + NX;    // [2] (by warpgroup)
+  uint64_t* kvfree = kvfull + 2;      // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, W = a.L + a.R + 1;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NX; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128);
+    }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128); }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t DV = tbase + NX * NQH, DK = DV + 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / ntq, u0 = (g % ntq) * kM;
+        const int st = k % NS;
+        uint8_t* b0 = stage0 + st * C::STAGE;
+        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
+        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
+        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
+        const int na = (u0 - a.R) & ~3;
+        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], na, bh, 0);
+        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], na, bh, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(64, NQH, 0, 0);
+      constexpr uint32_t idG = tc::idesc_bf16(64, kD, 0, 1);
+      constexpr uint32_t H64 = 64 * 128;            // 64 rows of a 128-byte-row smem tile (8 swizzle atoms)
+      int ns = 0, ndp = 0, nkv = 0;
+      while (nkv < ntile_me) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv % NX]), (nkv / NX) & 1,
+                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp % NX]), (ndp / NX) & 1,
+                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
+        if (nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
+          tc::tc_fence_after();
+          const int st = nkv % NS;
+          const uint32_t x = tbase + (nkv % NX) * NQH;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t q = base + 2 * C::KB, dO = q + C::QB;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {                // half A (lanes 0-15), half B (lanes 16-31)
+            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
+#pragma unroll
+            for (int j = 0; j < NQH / 16; ++j)
+              tc::mma_bf16_ts(DV | lo, (x + 8 * j) | lo, tc::desc_mnmajor_sw128(dO + roff + 2048 * j), idG, j > 0);
+#pragma unroll
+            for (int j = 0; j < NQH / 16; ++j)
+              tc::mma_bf16_ts(DK | lo, (x + NQH / 2 + 8 * j) | lo, tc::desc_mnmajor_sw128(q + roff + 2048 * j), idG,
+                              j > 0);
+          }
+          tc::mma_commit(&kvfull[nkv & 1]);
+          tc::mma_commit(&empty[st]);
+          ++nkv;
+          continue;
+        }
+        if (ndp < ns && (m & 4)) {
+          tc::tc_fence_after();
+          const int st = ndp % NS;
+          const uint32_t x = tbase + (ndp % NX) * NQH;
+          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
+          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(x | lo, tc::desc_kmajor_sw128(v + roff + 32 * j), tc::desc_kmajor_sw128(dO + roff + 32 * j),
+                           idS, j > 0);
+          }
+          tc::mma_commit(&dpfull[ndp % NX]);
+          ++ndp;
+          continue;
+        }
+        if (ns < ntile_me && ns < nkv + NX && (m & 8)) {
+          tc::tc_fence_after();
+          const uint32_t x = tbase + (ns % NX) * NQH;
+          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
+          const uint32_t kk = base, q = base + 2 * C::KB;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(x | lo, tc::desc_kmajor_sw128(kk + roff + 32 * j), tc::desc_kmajor_sw128(q + roff + 32 * j),
+                           idS, j > 0);
+          }
+          tc::mma_commit(&sfull[ns % NX]);
+          ++ns;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int hb = lane >> 4, rr = 16 * q4 + (lane & 15);   // half, row within the half
+    const int r = 64 * hb + rr;                               // key row within the 128-key tile
+    const int l16 = lane & 15;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    uint8_t* ostage = obuf0 + wg * 2 * C::KB;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, u0 = (g % ntq) * kM;
+      const int xb = k % NX, use = k / NX, st = k % NS;
+      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
+      // this half's window starts 64 query rows into the stage window for half B
+      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB) + sh + 64 * hb;
+      const float* sDel = sL2 + C::NQP;
+      tc::mbar_wait(&full[st], (k / NS) & 1);
+      const uint32_t x = tbase + lanes + xb * NQH;
+      const int c0 = 16 * q4;
+      tc::mbar_wait(&sfull[xb], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CWH];
+#pragma unroll
+      for (int j = 0; j < CWH / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CWH; ++i)
+        p[i] = (i >= l16 && i < l16 + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[xb]);
+      tc::mbar_wait(&dpfull[xb], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CWH];
+#pragma unroll
+      for (int j = 0; j < CWH / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      }
+      // packed P^T (columns [0, NQH/2)) and dS^T ([NQH/2, NQH)) of this row: the strip at packed
+      // column 8 q4, zeros elsewhere
+      {
+        const int pc0 = 8 * q4;
+#pragma unroll
+        for (int j = 0; j < CWH / 8; ++j) {
+          tc::tmem_st4(x + pc0 + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
+                       pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
+          tc::tmem_st4(x + NQH / 2 + pc0 + 4 * j, pack_bf16(ds[8 * j], ds[8 * j + 1]),
+                       pack_bf16(ds[8 * j + 2], ds[8 * j + 3]), pack_bf16(ds[8 * j + 4], ds[8 * j + 5]),
+                       pack_bf16(ds[8 * j + 6], ds[8 * j + 7]));
+        }
+        for (int c = 0; c < NQH / 2; c += 4)
+          if (c < pc0 || c >= pc0 + CWH / 2) {
+            tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
+            tc::tmem_st4(x + NQH / 2 + c, 0u, 0u, 0u, 0u);
+          }
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[xb]);
+      // dV / dK rows (row r of the 128-key tile)
+      tc::mbar_wait(&kvfull[k & 1], (k >> 1) & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + wg, 128);
+      tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+      tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&kvfree[k & 1]);
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+        tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
+        tc::bulk_commit();
+      }
+    }
+    if (leader) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
 // backward K2, block-ring variant (SATTN_K2=ring): the key-major kernel above with its query window
 // staged as 128-row blocks.  A CTA sweeps a contiguous range of key tiles, so consecutive
 // tiles' windows [u0 - R, u0 - R + NQ) share a block: each tile loads one new Q block and one
@@ -2235,7 +2480,11 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
     // bands too wide for the two-stage kernel's shared memory (W > 49: NQ = 192) take the
     // block-ring kernel with the column-split warpgroups (its registers hold half a row)
     constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
-    if (wide || (k2 && !strcmp(k2, "coop"))) {
+    if (!wide && k2 && !strcmp(k2, "m64")) {
+      cudaFuncSetAttribute(sa_bwd_dkdv_m64_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_m64_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128,
+                 mv128, mdoN, mdk, mdv, ml2, mdel, tc_args(a));
+    } else if (wide || (k2 && !strcmp(k2, "coop"))) {
       cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
       launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
                  mk128, mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
