@@ -1587,6 +1587,305 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// backward K2, block ring + M = 64 halves (SATTN_K2=rm64): the query window as 128-row blocks
+// shared by consecutive tiles of a contiguous sweep (3-slot ring, loads well ahead), K and V
+// through one 3-slot ring in load order K(0) V(0) K(1) V(1) ... (K freed by S, V by dP), the
+// 128-key tile as two M = 64 halves at TMEM lane offsets 0 / 16 (three S/dP buffers), and the
+// two-tile [dV | dK] staging per warpgroup of the original K2.
+// ------------------------------------------------------------------------------------------
+template <int CW> struct RM64Cfg {
+  static constexpr int NQ = nk_of(CW);
+  static constexpr int NQH = ((CW - 32 + 63) + 15) / 16 * 16;   // a half's window
+  static constexpr int NB2 = NQH > 64 ? NQH - 64 : 0;           // half B rows taken from the second block
+  static constexpr int NB = NB2 > 0 ? 2 : 1;
+  static constexpr int CWH = (CW - 16 + 7) / 8 * 8;
+  static constexpr int NX = 3;
+  static constexpr int KB = kM * 128;
+  static constexpr int BLK = 2 * KB;                             // [Q block | dO block]
+  static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
+  static constexpr int RW = 2 * NQP * 4;
+  static constexpr int SMEM = 1024 + 3 * BLK + 3 * KB + 4 * KB + 2 * RW + 512;
+  static constexpr int THREADS = 320;
+  static_assert(SMEM <= 232448 && NX * NQH + 128 <= 512 && NQH <= 128, "smem / TMEM layout");
+};
+
+template <int CW>
+__global__ void __launch_bounds__(320, 1)
+    sa_bwd_dkdv_rm64_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                        const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
+                        const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel,
+                        TcArgs a) {
+  using C = RM64Cfg<CW>;
+  constexpr int NQH = C::NQH, NB2 = C::NB2, NB = C::NB, CWH = C::CWH, NX = C::NX;
+  constexpr uint32_t LB = 16u << 16;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* blk0 = smem;                             // [Q | dO] x 3 block slots
+  uint8_t* kv0 = blk0 + 3 * C::BLK;                 // K / V x 3 (load order K0 V0 K1 V1 ...)
+  uint8_t* obuf0 = kv0 + 3 * C::KB;                 // per warpgroup [dV | dK]
+  uint8_t* rw0 = obuf0 + 4 * C::KB;                 // LSE / delta windows x 2
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rw0 + 2 * C::RW);
+  uint64_t* bfull = bars;             // [3]
+  uint64_t* bempty = bfull + 3;       // [3]
+  uint64_t* kvf = bempty + 3;         // [3] K/V slot landed
+  uint64_t* kve = kvf + 3;            // [3] K/V slot free
+  uint64_t* rfull = kve + 3;          // [2]
+  uint64_t* rempty = rfull + 2;       // [2] (128)
+  uint64_t* sfull = rempty + 2;       // [NX]
+  uint64_t* xfree = sfull + NX;       // [NX] (128)
+  uint64_t* dpfull = xfree + NX;      // [NX]
+  uint64_t* pdsfull = dpfull + NX;    // [NX] (128)
+  uint64_t* kvfull = pdsfull + NX;    // [2] by warpgroup
+  uint64_t* kvfree = kvfull + 2;      // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, W = a.L + a.R + 1;
+  const int ntq = (T + kM - 1) / kM;
+  const int ntiles = ntq * a.BH;
+  const int G = gridDim.x;
+  const int g_begin = (int)((long long)blockIdx.x * ntiles / G);
+  const int ntile_me = (int)((long long)(blockIdx.x + 1) * ntiles / G) - g_begin;
+
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
+    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < 3; ++i) {
+      tc::mbar_init(&bfull[i], 1); tc::mbar_init(&bempty[i], 1);
+      tc::mbar_init(&kvf[i], 1); tc::mbar_init(&kve[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&rfull[i], 1); tc::mbar_init(&rempty[i], 128);
+      tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
+    }
+    for (int i = 0; i < NX; ++i) {
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&pdsfull[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+  const uint32_t DV = tbase + NX * NQH, DK = DV + 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      BlkSeq sq;
+      sq.init();
+      auto kv_load = [&](int item, const CUtensorMap* map, int u0, int bh) {   // item 2k = K(k), 2k+1 = V(k)
+        const int sl = item % 3;
+        if (item >= 3) tc::mbar_wait(&kve[sl], ((item / 3) - 1) & 1);
+        tc::mbar_expect_tx(&kvf[sl], C::KB);
+        tc::tma_load_3d(kv0 + sl * C::KB, map, &kvf[sl], 0, u0, bh);
+      };
+      for (int k = 0; k < ntile_me; ++k) {
+        const int g = g_begin + k;
+        const int bh = g / ntq, kt = g % ntq, u0 = kt * kM;
+        int f, s2, nl0, nl1;
+        sq.next(g, ntq, NB, f, s2, nl0, nl1);
+        for (int n = nl0; n < nl1; ++n) {
+          const int sl = n % 3;
+          if (n >= 3) tc::mbar_wait(&bempty[sl], ((n / 3) - 1) & 1);
+          const int b = (n == f) ? kt : kt + 1;
+          uint8_t* d = blk0 + sl * C::BLK;
+          tc::mbar_expect_tx(&bfull[sl], C::BLK);
+          tc::tma_load_3d(d, &tmQ, &bfull[sl], 0, b * kM - a.R, bh);
+          tc::tma_load_3d(d + C::KB, &tmdO, &bfull[sl], 0, b * kM - a.R, bh);
+        }
+        kv_load(2 * k, &tmK, u0, bh);
+        kv_load(2 * k + 1, &tmV, u0, bh);
+        const int s = k & 1;
+        if (k >= 2) tc::mbar_wait(&rempty[s], ((k - 2) >> 1) & 1);
+        const int na = (u0 - a.R) & ~3;
+        tc::mbar_expect_tx(&rfull[s], C::RW);
+        tc::tma_load_3d(rw0 + s * C::RW, &tmL2, &rfull[s], na, bh, 0);
+        tc::tma_load_3d(rw0 + s * C::RW + C::NQP * 4, &tmDel, &rfull[s], na, bh, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idA = tc::idesc_bf16(64, NQH, 0, 0);              // half A: one block
+      constexpr uint32_t idB1 = tc::idesc_bf16(64, NB2 > 0 ? 64 : NQH, 0, 0);   // half B: rows 64.. of block f
+      constexpr uint32_t idB2 = tc::idesc_bf16(64, NB2 > 0 ? NB2 : 16, 0, 0);   // ... and rows 0.. of block s
+      constexpr uint32_t idG = tc::idesc_bf16(64, kD, 0, 1);
+      constexpr uint32_t H64 = 64 * 128;
+      BlkSeq qs, qd, qk;
+      qs.init(); qd.init(); qk.init();
+      int sf = 0, ss = 0, df = 0, ds2 = 0, kf = 0, ks2 = 0, krel2 = 0;
+      int ns = 0, ndp = 0, nkv = 0;
+      auto blk = [&](int n) { return tc::smem_u32(blk0 + (n % 3) * C::BLK); };
+      auto kvs = [&](int item) { return tc::smem_u32(kv0 + (item % 3) * C::KB); };
+      bool s_ready = false, d_ready = false, k_ready = false;
+      // S^T or dP^T of both halves: A rows (K or V) 0..63 / 64..127, B = the half's query window
+      auto sdp = [&](uint32_t x, uint32_t arows, uint32_t bf, uint32_t bs, uint32_t boff) {
+#pragma unroll
+        for (int j = 0; j < kD / 16; ++j) {
+          tc::mma_bf16(x, tc::desc_kmajor_sw128(arows + 32 * j), tc::desc_kmajor_sw128(bf + boff + 32 * j), idA, j > 0);
+          tc::mma_bf16(x | LB, tc::desc_kmajor_sw128(arows + H64 + 32 * j),
+                       tc::desc_kmajor_sw128(bf + boff + H64 + 32 * j), idB1, j > 0);
+          if (NB2 > 0)
+            tc::mma_bf16((x + 64) | LB, tc::desc_kmajor_sw128(arows + H64 + 32 * j),
+                         tc::desc_kmajor_sw128(bs + boff + 32 * j), idB2, j > 0);
+        }
+      };
+      while (nkv < ntile_me) {
+        if (!s_ready && ns < ntile_me) { int a0, a1; qs.next(g_begin + ns, ntq, NB, sf, ss, a0, a1); s_ready = true; }
+        if (!d_ready && ndp < ns) { int a0, a1; qd.next(g_begin + ndp, ntq, NB, df, ds2, a0, a1); d_ready = true; }
+        if (!k_ready && nkv < ndp) {
+          int a0, a1; qk.next(g_begin + nkv, ntq, NB, kf, ks2, a0, a1);
+          const int g = g_begin + nkv, gn = g + 1;
+          krel2 = (NB == 2) && !(nkv + 1 < ntile_me && gn / ntq == g / ntq && gn % ntq == g % ntq + 1);
+          k_ready = true;
+        }
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv % NX]), (nkv / NX) & 1,
+                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp % NX]), (ndp / NX) & 1,
+                                          tc::smem_u32(&kvf[(2 * ns) % 3]), ((2 * ns) / 3) & 1);
+        if (k_ready && nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
+          tc::tc_fence_after();
+          const uint32_t x = tbase + (nkv % NX) * NQH;
+          const uint32_t bf = blk(kf), bs = NB == 2 ? blk(ks2) : bf;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t lo = h ? LB : 0u;
+#pragma unroll
+            for (int j = 0; j < NQH / 16; ++j) {   // K-step j: window rows 64 h + 16 j
+              const int row = 64 * h + 16 * j;
+              const uint32_t bb = row < kM ? bf + 128 * row : bs + 128 * (row - kM);
+              tc::mma_bf16_ts(DV | lo, (x + 8 * j) | lo, tc::desc_mnmajor_sw128(bb + C::KB), idG, j > 0);
+            }
+#pragma unroll
+            for (int j = 0; j < NQH / 16; ++j) {
+              const int row = 64 * h + 16 * j;
+              const uint32_t bb = row < kM ? bf + 128 * row : bs + 128 * (row - kM);
+              tc::mma_bf16_ts(DK | lo, (x + NQH / 2 + 8 * j) | lo, tc::desc_mnmajor_sw128(bb), idG, j > 0);
+            }
+          }
+          tc::mma_commit(&kvfull[nkv & 1]);
+          tc::mma_commit(&bempty[kf % 3]);
+          if (krel2) tc::mma_commit(&bempty[ks2 % 3]);
+          ++nkv;
+          k_ready = false;
+          continue;
+        }
+        if (d_ready && ndp < ns && (m & 4) &&
+            tc::mbar_test(tc::smem_u32(&kvf[(2 * ndp + 1) % 3]), ((2 * ndp + 1) / 3) & 1)) {
+          tc::tc_fence_after();
+          const uint32_t x = tbase + (ndp % NX) * NQH;
+          sdp(x, kvs(2 * ndp + 1), blk(df), NB == 2 ? blk(ds2) : blk(df), C::KB);
+          tc::mma_commit(&dpfull[ndp % NX]);
+          tc::mma_commit(&kve[(2 * ndp + 1) % 3]);
+          ++ndp;
+          d_ready = false;
+          continue;
+        }
+        if (s_ready && ns < ntile_me && ns < nkv + NX && (m & 8) &&
+            tc::mbar_test(tc::smem_u32(&bfull[sf % 3]), (sf / 3) & 1) &&
+            (NB == 1 || tc::mbar_test(tc::smem_u32(&bfull[ss % 3]), (ss / 3) & 1))) {
+          tc::tc_fence_after();
+          const uint32_t x = tbase + (ns % NX) * NQH;
+          sdp(x, kvs(2 * ns), blk(sf), NB == 2 ? blk(ss) : blk(sf), 0);
+          tc::mma_commit(&sfull[ns % NX]);
+          tc::mma_commit(&kve[(2 * ns) % 3]);
+          ++ns;
+          s_ready = false;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int hb = lane >> 4, rr = 16 * q4 + (lane & 15);
+    const int r = 64 * hb + rr;
+    const int l16 = lane & 15;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const bool leader = q4 == 2 && lane == 0;
+    uint8_t* ostage = obuf0 + wg * 2 * C::KB;
+    for (int k = wg; k < ntile_me; k += 2) {
+      const int g = g_begin + k;
+      const int bh = g / ntq, u0 = (g % ntq) * kM;
+      const int xb = k % NX, use = k / NX, s = k & 1;
+      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
+      const float* sL2 = reinterpret_cast<const float*>(rw0 + s * C::RW) + sh + 64 * hb;
+      const float* sDel = sL2 + C::NQP;
+      tc::mbar_wait(&rfull[s], (k >> 1) & 1);
+      const uint32_t x = tbase + lanes + xb * NQH;
+      const int c0 = 16 * q4;
+      tc::mbar_wait(&sfull[xb], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[CWH];
+#pragma unroll
+      for (int j = 0; j < CWH / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < CWH; ++i)
+        p[i] = (i >= l16 && i < l16 + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[xb]);
+      tc::mbar_wait(&dpfull[xb], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float ds[CWH];
+#pragma unroll
+      for (int j = 0; j < CWH / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + c0 + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
+      }
+      tc::mbar_arrive(&rempty[s]);
+      {
+        const int pc0 = 8 * q4;
+#pragma unroll
+        for (int j = 0; j < CWH / 8; ++j) {
+          tc::tmem_st4(x + pc0 + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
+                       pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
+          tc::tmem_st4(x + NQH / 2 + pc0 + 4 * j, pack_bf16(ds[8 * j], ds[8 * j + 1]),
+                       pack_bf16(ds[8 * j + 2], ds[8 * j + 3]), pack_bf16(ds[8 * j + 4], ds[8 * j + 5]),
+                       pack_bf16(ds[8 * j + 6], ds[8 * j + 7]));
+        }
+        for (int c = 0; c < NQH / 2; c += 4)
+          if (c < pc0 || c >= pc0 + CWH / 2) {
+            tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
+            tc::tmem_st4(x + NQH / 2 + c, 0u, 0u, 0u, 0u);
+          }
+      }
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pdsfull[xb]);
+      tc::mbar_wait(&kvfull[k & 1], (k >> 1) & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + wg, 128);
+      tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+      tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&kvfree[k & 1]);
+      tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (leader) {
+        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+        tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
+        tc::bulk_commit();
+      }
+    }
+    if (leader) tc::bulk_wait0();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
 // LLSA backward, band keys (channel R), key-major: for a tile of 128 channel-R keys u, every
 // query channel c = 0..R contributes through the band: query (t, c) sees (u, R) iff
 // u in [t + c - R - L, t + c - R]  <=>  t in [u + s_c, u + s_c + L],  s_c = R - c
@@ -2480,7 +2779,11 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
     // bands too wide for the two-stage kernel's shared memory (W > 49: NQ = 192) take the
     // block-ring kernel with the column-split warpgroups (its registers hold half a row)
     constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
-    if (!wide && k2 && !strcmp(k2, "m64")) {
+    if (!wide && k2 && !strcmp(k2, "rm64")) {
+      cudaFuncSetAttribute(sa_bwd_dkdv_rm64_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, RM64Cfg<CW>::SMEM);
+      launch_pdl(sa_bwd_dkdv_rm64_tc<CW>, dim3(grid), dim3(RM64Cfg<CW>::THREADS), RM64Cfg<CW>::SMEM, st, mq, mk128,
+                 mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
+    } else if (!wide && k2 && !strcmp(k2, "m64")) {
       cudaFuncSetAttribute(sa_bwd_dkdv_m64_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
       launch_pdl(sa_bwd_dkdv_m64_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128,
                  mv128, mdoN, mdk, mdv, ml2, mdel, tc_args(a));

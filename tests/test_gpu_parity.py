@@ -254,7 +254,7 @@ def _ring_check(shape, L, R):
     assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
 
 
-@pytest.mark.parametrize("variant", ["ring", "coop", "m64"])
+@pytest.mark.parametrize("variant", ["ring", "coop", "m64", "rm64"])
 @pytest.mark.parametrize("shape,L,R", RING)
 def test_sa_bf16_k2_variants(shape, L, R, variant, monkeypatch):
     # SATTN_K2=ring: block-ring sweep; SATTN_K2=coop: the same with both warpgroups on every
