@@ -82,6 +82,27 @@ sattn_status sa_backward(const sattn_desc* desc, const void* Q, const void* K, c
                          const void* O, const float* LSE, const void* dO,
                          void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------- SA with the stored band (NEXT-4) ----------
+ * The paper keeps z_t and a_t as N_T x (A+B+1) matrices; the calls
+ * above keep only LSE [B][H][T] and recompute a_t.  These keep a_t instead:
+ * sa_p_ld(desc): row stride (elements) of the band, W = L+R+1 rounded up to a
+ *   multiple of 8 (16-byte rows); 0 if desc is invalid.
+ * sa_forward_p: as sa_forward, and also writes P [B][H][T][ld] (desc->dtype),
+ *   P[t][j] = a_{t, t-L+j} (Eq. 5) for j < W, exactly 0 where t-L+j is
+ *   outside [0, T-1] (G2) and for j >= W.  Runs on the CUDA-core kernels
+ *   (desc->impl = SATTN_IMPL_TC -> SATTN_EUNSUPPORTED).
+ * sa_backward_p: gradients of <dO, O> with a_t read from P instead of
+ *   recomputed (Eq. 7-13); P must come from sa_forward_p on the same inputs.
+ *   ws >= sa_backward_p_workspace(desc) bytes (delta_t = dO_t . O_t, fp32).
+ *   Deterministic (no atomics).                                               */
+int64_t sa_p_ld(const sattn_desc* desc);
+sattn_status sa_forward_p(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                          void* O, float* LSE, void* P, void* stream);
+size_t sa_backward_p_workspace(const sattn_desc* desc);
+sattn_status sa_backward_p(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                           const void* O, const void* P, const void* dO,
+                           void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------- LLSA: Eq. 14-16 -------------------------------
  * Output (t, c) attends the Eq. 14 slots read in the Fig. 3(c) convention (G6):
  * anchor s = t-(R-c); slots (u, R) for u in [s-L, s] and (s+j, R-j), j=1..R,

@@ -108,3 +108,60 @@ def aa_forward(Q, K, V, scale: float | None = None):
     for idx in _heads(Q):
         O[idx], _, _ = attention_fwd(Q[idx], np.asarray(K)[idx], np.asarray(V)[idx], full, _scale(D, scale))
     return O
+
+
+# ---------------------------------------------------------------------------
+# The paper's stored band (NEXT-4).  The paper keeps z_t and a_t
+# as N_T x (A+B+1) matrices; the build's stored-band mode keeps a_t.
+# ---------------------------------------------------------------------------
+
+def sa_band_probs(Q, K, L: int, R: int, scale: float | None = None):
+    """a_t of Eq. 5 stored in the band layout: A[..., t, j] = a_{t, t-L+j},
+    j in [0, W), W = L+R+1; 0 where t-L+j is outside [0, T-1] (G2).  Taken from the dense
+    definition (attention_fwd's a), entry by entry."""
+    Q, K = (np.asarray(x, dtype=np.float64) for x in (Q, K))
+    T, D = Q.shape[-2:]
+    W = L + R + 1
+    s = _scale(D, scale)
+    mask = band_mask(T, L, R)
+    A = np.zeros(Q.shape[:-1] + (W,))
+    for idx in _heads(Q):
+        _, _, a = attention_fwd(Q[idx], K[idx], K[idx], mask, s)
+        for t in range(T):
+            for j in range(W):
+                u = t - L + j
+                if 0 <= u < T:
+                    A[idx + (t, j)] = a[t, u]
+    return A
+
+
+def sa_backward_band(A, Q, K, V, dO, L: int, R: int, scale: float | None = None):
+    """SA gradients from a stored band A (layout of sa_band_probs), Eq. 7-13 written in
+    the band index j (key u = n - L + j), one shifted slice per j:
+      dv_u  = sum_n a_{n,u-n+L} dy_n                  Eq. 7-8 (index condition per G3)
+      da_nj = dy_n . v_{n-L+j}                        Eq. 9's dl/da
+      dz_nj = a_nj (da_nj - sum_j' a_nj' da_nj')      softmax Jacobian (Eq. 9)
+      dq_n  = s sum_j dz_nj k_{n-L+j}                 Eq. 10
+      dk_u  = s sum_n dz_{n,u-n+L} q_n                Eq. 11-13
+    """
+    A, Q, K, V, dO = (np.asarray(x, dtype=np.float64) for x in (A, Q, K, V, dO))
+    T, D = Q.shape[-2:]
+    W = L + R + 1
+    s = _scale(D, scale)
+    A = A[..., :W]
+    da = np.zeros(A.shape)
+    for j in range(W):                      # key u = n - L + j, valid rows n
+        n0, n1 = max(0, L - j), min(T, T + L - j)
+        if n0 < n1:
+            da[..., n0:n1, j] = np.einsum("...nd,...nd->...n", dO[..., n0:n1, :], V[..., n0 - L + j:n1 - L + j, :])
+    dz = A * (da - (A * da).sum(axis=-1, keepdims=True))
+    dQ, dK, dV = np.zeros_like(Q), np.zeros_like(K), np.zeros_like(V)
+    for j in range(W):
+        n0, n1 = max(0, L - j), min(T, T + L - j)
+        if n0 >= n1:
+            continue
+        u0, u1 = n0 - L + j, n1 - L + j
+        dQ[..., n0:n1, :] += s * dz[..., n0:n1, j, None] * K[..., u0:u1, :]
+        dK[..., u0:u1, :] += s * dz[..., n0:n1, j, None] * Q[..., n0:n1, :]
+        dV[..., u0:u1, :] += A[..., n0:n1, j, None] * dO[..., n0:n1, :]
+    return dQ, dK, dV

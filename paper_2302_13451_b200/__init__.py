@@ -14,7 +14,7 @@ import os
 import torch
 
 __all__ = [
-    "SattnError", "lib", "sa_forward", "sa_backward", "llsa_forward", "llsa_backward",
+    "SattnError", "lib", "sa_forward", "sa_backward", "sa_forward_p", "sa_backward_p", "llsa_forward", "llsa_backward",
     "stack_forward", "stack_backward", "LLSAStream", "SAFunction", "LLSAFunction", "launch_count",
     "MODE_SA", "MODE_LLSA", "IMPL_AUTO", "IMPL_FFMA", "IMPL_TC",
 ]
@@ -46,6 +46,10 @@ EXPORTS = {
     "sa_forward": (_I, [_PD, _P, _P, _P, _P, _P, _P]),
     "sa_backward_workspace": (_SZ, [_PD]),
     "sa_backward": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "sa_p_ld": (ctypes.c_int64, [_PD]),
+    "sa_forward_p": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P]),
+    "sa_backward_p_workspace": (_SZ, [_PD]),
+    "sa_backward_p": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "llsa_forward": (_I, [_PD, _P, _P, _P, _P, _P, _P]),
     "llsa_backward_workspace": (_SZ, [_PD]),
     "llsa_backward": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -157,6 +161,34 @@ def sa_backward(q, k, v, o, lse, do, L: int, R: int, scale=None, impl="auto", ws
         ws = torch.empty(nws, device=q.device, dtype=torch.uint8)
     _check(lib().sa_backward(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(do),
                              _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), nws, _stream()), "sa_backward")
+    return dq, dk, dv
+
+
+def sa_forward_p(q, k, v, L: int, R: int, scale=None, impl="auto"):
+    """SA forward that also stores the band of probabilities (the paper's a_t):
+    -> (o, lse, p) with p [B, H, T, ld] in q's dtype, p[..., t, j] = a_{t, t-L+j} for
+    j < W = L+R+1, zero outside the clipped window and in the padding j >= W."""
+    _same(q, k, v)
+    d = _desc_from(q, L, R, scale, impl)
+    o = torch.empty_like(q)
+    lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
+    ld = int(lib().sa_p_ld(ctypes.byref(d)))
+    p = torch.empty(tuple(q.shape[:-1]) + (ld,), device=q.device, dtype=q.dtype)
+    _check(lib().sa_forward_p(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(p), _stream()),
+           "sa_forward_p")
+    return o, lse, p
+
+
+def sa_backward_p(q, k, v, o, p, do, L: int, R: int, scale=None, impl="auto", ws=None):
+    """SA backward from the stored band p of sa_forward_p (no score recompute) -> (dq, dk, dv)."""
+    _same(q, k, v, o, do)
+    d = _desc_from(q, L, R, scale, impl)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    nws = lib().sa_backward_p_workspace(ctypes.byref(d))
+    if ws is None or ws.numel() < nws:
+        ws = torch.empty(nws, device=q.device, dtype=torch.uint8)
+    _check(lib().sa_backward_p(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(p), _ptr(do),
+                               _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), nws, _stream()), "sa_backward_p")
     return dq, dk, dv
 
 

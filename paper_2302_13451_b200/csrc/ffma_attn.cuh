@@ -48,6 +48,8 @@ struct AttnArgs {
   void* Out; float* LSEout;                     // forward outputs
   void* dQ; void* dK; void* dV;                 // backward outputs (dense)
   float* delta;                                 // backward workspace [C][BH][T]
+  void* P;                                      // SA banded probabilities [BH][T][ldp] (PST kernels)
+  int ldp;
   int T, L, R, BH;
   float scale, scale_log2;
   long long in_cs, out_cs;
@@ -100,7 +102,10 @@ __device__ __forceinline__ float pair_sum(float x) { return x + __shfl_xor_sync(
 // --------------------------------------------------------------------------------------------
 // forward: O, LSE
 // --------------------------------------------------------------------------------------------
-template <int D, bool LLSA, typename E>
+// PST (SA only, the paper's stored band, NEXT-4 / P:L342): also write a_t into
+// P[bh][t][j] = a_{t, t-L+j}, j in [0, ldp), zero outside the clipped window, by a second
+// pass over the window once the row's LSE is known.
+template <int D, bool LLSA, typename E, bool PST = false>
 __global__ void __launch_bounds__(32 * kNW) fwd_ffma(AttnArgs a) {
   constexpr int HD = D / 2, SD = Smem<D>::SD;
   extern __shared__ __align__(16) float smem[];
@@ -197,12 +202,37 @@ __global__ void __launch_bounds__(32 * kNW) fwd_ffma(AttnArgs a) {
     store_vec<HD>(orow, acc);
     if (half == 0) a.LSEout[((long long)c * a.BH + bh) * T + t] = (m + log2f(l)) * kLn2;
   }
+  if constexpr (PST && !LLSA) {
+    const float lse2 = m + log2f(l);
+    E* prow = reinterpret_cast<E*>(a.P) + ((long long)bh * T + t) * a.ldp;
+    // entries outside the clipped window (sequence edges, padding j >= W): zero
+    if (active)
+      for (int j = half; j < a.ldp; j += 2) {
+        const int u = t - L + j;
+        if (u < 0 || u >= T || j > L + R) prow[j] = from_f<E>(0.f);
+      }
+    const bool single = uhi - ulo + 1 <= kRB;   // sK still holds the whole union
+    for (int b0 = ulo; b0 <= uhi; b0 += kRB) {
+      const int nr = min(kRB, uhi - b0 + 1);
+      if (!single) {
+        __syncthreads();
+        stage_rows<D, E>(sK, kplane, b0, nr);
+        __syncthreads();
+      }
+      const int r0 = max(b0, wlo), r1 = min(b0 + nr - 1, whi);
+      for (int r = r0; r <= r1; ++r) {
+        const float sc = pair_sum(dot<HD>(q, sK + (r - b0) * SD + hoff));
+        if (active && half == (r & 1) && r >= my_lo && r <= my_hi) prow[r - my_lo] = from_f<E>(exp2f(sc - lse2));
+      }
+    }
+  }
 }
 
 // --------------------------------------------------------------------------------------------
 // backward 1 (query-major): delta_t = dO_t . O_t and dQ_t = scale * sum_u dS_tu k_u
 // --------------------------------------------------------------------------------------------
-template <int D, bool LLSA, typename E>
+// PST (SA only): P_tu read from the stored band a.P instead of exp2(z - LSE) (no q . k)
+template <int D, bool LLSA, typename E, bool PST = false>
 __global__ void __launch_bounds__(32 * kNW) bwd_dq_ffma(AttnArgs a) {
   constexpr int HD = D / 2, SD = Smem<D>::SD;
   extern __shared__ __align__(16) float smem[];
@@ -229,7 +259,8 @@ __global__ void __launch_bounds__(32 * kNW) bwd_dq_ffma(AttnArgs a) {
     for (int i = 0; i < HD; ++i) { q[i] *= a.scale_log2; dq[i] = 0.f; }
     const float delta = pair_sum(dot<HD>(dout, o));
     if (active && half == 0) a.delta[((long long)c * a.BH + bh) * T + t] = delta;
-    const float lse2 = a.LSE[((long long)c * a.BH + bh) * T + tc] * kLog2e;
+    const float lse2 = PST ? 0.f : a.LSE[((long long)c * a.BH + bh) * T + tc] * kLog2e;
+    const E* prow = PST ? reinterpret_cast<const E*>(a.P) + ((long long)bh * T + tc) * a.ldp : nullptr;
 
     const int my_lo = t + lo_off, my_hi = t + hi_off;
     const int tw = t0 + warp * 16;
@@ -250,16 +281,18 @@ __global__ void __launch_bounds__(32 * kNW) bwd_dq_ffma(AttnArgs a) {
 #pragma unroll
         for (int k = 0; k < kCH; ++k) {
           const int ro = (min(r + k, r1) - b0) * SD + hoff;
-          s[k] = dot<HD>(q, sK + ro);
+          s[k] = PST ? 0.f : dot<HD>(q, sK + ro);
           dp[k] = dot<HD>(dout, sV + ro);
         }
 #pragma unroll
         for (int k = 0; k < kCH; ++k) {
-          s[k] = pair_sum(s[k]);
+          if (!PST) s[k] = pair_sum(s[k]);
           dp[k] = pair_sum(dp[k]);
           const int row = r + k;
           const bool v = row <= r1 && row >= my_lo && row <= my_hi;
-          const float p = v ? exp2f(s[k] - lse2) : 0.f;
+          float p;
+          if constexpr (PST) p = v ? to_f(prow[row - my_lo]) : 0.f;
+          else p = v ? exp2f(s[k] - lse2) : 0.f;
           const float ds = p * (dp[k] - delta);
           const float* kr = sK + (min(row, r1) - b0) * SD + hoff;
 #pragma unroll
@@ -295,13 +328,16 @@ __global__ void __launch_bounds__(32 * kNW) bwd_dq_ffma(AttnArgs a) {
 // --------------------------------------------------------------------------------------------
 // backward 2 (key-major): dK_u = scale * sum_n dS_nu q_n,  dV_u = sum_n P_nu dO_n
 // --------------------------------------------------------------------------------------------
-template <int D, typename E>
+// pst >= 0: P_nu is the stored band value pst (PST kernels), no q . k
+template <int D, typename E, bool PST = false>
 __device__ __forceinline__ void dkdv_row(const float* qr, const float* dor, float lse2, float delta, bool valid,
-                                         const float* k, const float* v, float* dk, float* dv, float scale_log2) {
+                                         const float* k, const float* v, float* dk, float* dv, float scale_log2,
+                                         float pst = 0.f) {
   constexpr int HD = D / 2;
-  const float s = pair_sum(dot<HD>(qr, k)) * scale_log2;
   const float dp = pair_sum(dot<HD>(dor, v));
-  const float p = valid ? exp2f(s - lse2) : 0.f;
+  float p;
+  if constexpr (PST) p = valid ? pst : 0.f;
+  else p = valid ? exp2f(pair_sum(dot<HD>(qr, k)) * scale_log2 - lse2) : 0.f;
   const float ds = p * (dp - delta);
 #pragma unroll
   for (int i = 0; i < HD; ++i) {
@@ -310,7 +346,8 @@ __device__ __forceinline__ void dkdv_row(const float* qr, const float* dor, floa
   }
 }
 
-template <int D, bool LLSA, typename E>
+// PST (SA only): P_nu = a.P[n][u - n + L] (the stored band, read along its diagonal)
+template <int D, bool LLSA, typename E, bool PST = false>
 __global__ void __launch_bounds__(32 * kNW) bwd_dkdv_ffma(AttnArgs a) {
   constexpr int HD = D / 2, SD = Smem<D>::SD;
   extern __shared__ __align__(16) float smem[];
@@ -354,7 +391,7 @@ __global__ void __launch_bounds__(32 * kNW) bwd_dkdv_ffma(AttnArgs a) {
         stage_rows<D, E>(sQ, qplane, b0, nr);
         stage_rows<D, E>(sD, dplane, b0, nr);
         for (int i = tid; i < nr; i += blockDim.x) {
-          sL[i] = lse[b0 + i] * kLog2e;
+          if (!PST) sL[i] = lse[b0 + i] * kLog2e;
           sE[i] = del[b0 + i];
         }
         __syncthreads();
@@ -362,7 +399,12 @@ __global__ void __launch_bounds__(32 * kNW) bwd_dkdv_ffma(AttnArgs a) {
         for (int r = r0; r <= r1; ++r) {
           const bool valid = r >= my_lo && r <= my_hi;
           const int ro = (r - b0) * SD + hoff;
-          dkdv_row<D, E>(sQ + ro, sD + ro, sL[r - b0], sE[r - b0], valid, k, v, dk, dv, a.scale_log2);
+          if constexpr (PST) {
+            const float pv = valid ? to_f(reinterpret_cast<const E*>(a.P)[((long long)bh * T + r) * a.ldp + (uc - r + L)]) : 0.f;
+            dkdv_row<D, E, true>(sQ + ro, sD + ro, 0.f, sE[r - b0], valid, k, v, dk, dv, a.scale_log2, pv);
+          } else {
+            dkdv_row<D, E>(sQ + ro, sD + ro, sL[r - b0], sE[r - b0], valid, k, v, dk, dv, a.scale_log2);
+          }
         }
       }
     }

@@ -144,6 +144,38 @@ sattn_status ffma_backward(const sattn_desc* d, bool llsa, const AttnArgs& a, cu
   });
 }
 
+// SA with the stored band (NEXT-4): the PST instances of the CUDA-core kernels
+int64_t p_ld(const sattn_desc* d) { return ((int64_t)d->L + d->R + 1 + 7) & ~int64_t(7); }
+
+sattn_status ffma_forward_p(const sattn_desc* d, const AttnArgs& a, cudaStream_t st) {
+  return dispatch(d->D, d->dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
+    constexpr int D = decltype(dc)::value;
+    using T = decltype(tv);
+    const size_t smem = fwd_smem_bytes<D>();
+    set_smem(fwd_ffma<D, false, T, true>, smem);
+    dim3 grid((unsigned)((a.T + kQT - 1) / kQT), 1u, (unsigned)a.BH);
+    fwd_ffma<D, false, T, true><<<grid, 32 * kNW, smem, st>>>(a);
+    return after_launch("fwd_ffma_p");
+  });
+}
+
+sattn_status ffma_backward_p(const sattn_desc* d, const AttnArgs& a, cudaStream_t st) {
+  return dispatch(d->D, d->dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
+    constexpr int D = decltype(dc)::value;
+    using T = decltype(tv);
+    dim3 grid((unsigned)((a.T + kQT - 1) / kQT), 1u, (unsigned)a.BH);
+    const size_t s1 = fwd_smem_bytes<D>();
+    set_smem(bwd_dq_ffma<D, false, T, true>, s1);
+    bwd_dq_ffma<D, false, T, true><<<grid, 32 * kNW, s1, st>>>(a);
+    sattn_status r = after_launch("bwd_dq_ffma_p");
+    if (r != SATTN_OK) return r;
+    const size_t s2 = dkdv_smem_bytes<D>();
+    set_smem(bwd_dkdv_ffma<D, false, T, true>, s2);
+    bwd_dkdv_ffma<D, false, T, true><<<grid, 32 * kNW, s2, st>>>(a);
+    return after_launch("bwd_dkdv_ffma_p");
+  });
+}
+
 bool tc_ok(const sattn_desc* d, bool llsa, bool backward) {
   if (llsa)
     return backward ? tc_llsa_bwd_supported(d->dtype, (int)d->D, d->L, d->R)
@@ -302,6 +334,43 @@ sattn_status llsa_backward(const sattn_desc* d, const void* Q, const void* K, co
   sattn_status r = validate(d);
   if (r != SATTN_OK) return r;
   return attn_backward(d, true, Q, K, V, O, LSE, dO, dQ, dK, dV, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int64_t sa_p_ld(const sattn_desc* d) { return validate(d) == SATTN_OK ? p_ld(d) : 0; }
+
+sattn_status sa_forward_p(const sattn_desc* d, const void* Q, const void* K, const void* V, void* O, float* LSE,
+                          void* P, void* stream) {
+  sattn_status r = validate(d);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !O || !LSE || !P) return fail(SATTN_EARG, "NULL tensor pointer");
+  if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE) || !aligned16(P))
+    return fail(SATTN_EARG, "tensor pointers must be 16-byte aligned");
+  if (d->impl == SATTN_IMPL_TC) return fail(SATTN_EUNSUPPORTED, "stored-band SA runs on the CUDA-core kernels");
+  AttnArgs a = make_args(d, false);
+  a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE; a.P = P; a.ldp = (int)p_ld(d);
+  return ffma_forward_p(d, a, (cudaStream_t)stream);
+}
+
+size_t sa_backward_p_workspace(const sattn_desc* d) {
+  return validate(d) == SATTN_OK ? (size_t)d->B * d->H * ((d->T + 3) & ~3LL) * sizeof(float) : 0;
+}
+
+sattn_status sa_backward_p(const sattn_desc* d, const void* Q, const void* K, const void* V, const void* O,
+                           const void* P, const void* dO, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,
+                           void* stream) {
+  sattn_status r = validate(d);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !O || !P || !dO || !dQ || !dK || !dV || !ws) return fail(SATTN_EARG, "NULL pointer");
+  const void* ps[] = {Q, K, V, O, P, dO, dQ, dK, dV, ws};
+  for (const void* p : ps)
+    if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
+  if (ws_bytes < sa_backward_p_workspace(d))
+    return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, sa_backward_p_workspace(d));
+  if (d->impl == SATTN_IMPL_TC) return fail(SATTN_EUNSUPPORTED, "stored-band SA runs on the CUDA-core kernels");
+  AttnArgs a = make_args(d, false);
+  a.Q = Q; a.K = K; a.V = V; a.O = O; a.dO = dO; a.P = const_cast<void*>(P); a.ldp = (int)p_ld(d);
+  a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
+  return ffma_backward_p(d, a, (cudaStream_t)stream);
 }
 
 size_t sattn_stack_saved_bytes(const sattn_desc* d, int mode, int n_layers) {

@@ -1,0 +1,83 @@
+"""GPU parity of the stored-band mode (sa_forward_p / sa_backward_p; NEXT-4, the paper's
+N_T x (A+B+1) a_t matrix) against the oracle (oracle.sa.sa_band_probs,
+sa_backward_band, sa_forward / sa_backward).  Gates as tests/test_gpu_parity.py."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from test_gpu_parity import TOL, dev, excess, host, maxerr, sattn
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    ((1, 1, 16, 4), 3, 1, "f32"), ((2, 3, 37, 4), 0, 0, "f32"), ((2, 3, 37, 4), 0, 5, "f32"),
+    ((2, 3, 37, 4), 5, 0, "f32"), ((1, 2, 129, 64), 32, 8, "f32"), ((1, 2, 300, 64), 200, 150, "f32"),
+    ((1, 1, 1, 8), 3, 2, "f32"), ((1, 2, 65, 2), 1, 1, "f32"), ((1, 1, 200, 32), 0, 63, "f32"),
+    ((2, 2, 1750, 64), 32, 8, "bf16"), ((1, 2, 300, 64), 32, 16, "bf16"), ((1, 3, 777, 64), 32, 32, "bf16"),
+    ((1, 2, 130, 16), 7, 3, "bf16"),
+]
+
+
+def _ld(L, R):
+    return (L + R + 1 + 7) // 8 * 8
+
+
+@pytest.mark.parametrize("shape,L,R,dt", CASES)
+def test_sa_stored_band(shape, L, R, dt):
+    s = sattn()
+    q, k, v = synth.qkv(11, shape, dt)
+    do = synth.grad_out(11, shape, dt)
+    tq, tk, tv, tdo = (dev(x, dt) for x in (q, k, v, do))
+    W = L + R + 1
+    o, lse, p = s.sa_forward_p(tq, tk, tv, L, R)
+    assert p.shape == tuple(shape[:-1]) + (_ld(L, R),) and p.dtype == tq.dtype
+    O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
+    A = oracle.sa.sa_band_probs(q, k, L, R)
+    assert excess(o, O, dt) <= 0, ("O", maxerr(o, O))
+    assert maxerr(lse, LSE) <= TOL[dt], ("LSE", maxerr(lse, LSE))
+    # the band: entries within the gate; exact zeros outside the clipped window and in the padding
+    ph = host(p)
+    assert maxerr(p[..., :W], A) <= (TOL[dt] if dt == "f32" else 4e-3), ("P", maxerr(p[..., :W], A))
+    assert (ph[..., W:] == 0).all()
+    t = np.arange(shape[2])[:, None]
+    u = t - L + np.arange(W)[None, :]
+    assert (ph[..., :W][..., (u < 0) | (u >= shape[2])] == 0).all()
+    # backward from the GPU's own band
+    dq, dk, dv = s.sa_backward_p(tq, tk, tv, o, p, tdo, L, R)
+    G = oracle.sa.sa_backward(q, k, v, do, L, R)
+    for name, got, ref in (("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
+        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
+    # backward from the oracle's band (rounded to the tensor dtype): the band-form oracle
+    pa = torch.zeros_like(p)
+    pa[..., :W] = dev(A, dt)
+    o_ref = dev(O, dt)
+    dq2, dk2, dv2 = s.sa_backward_p(tq, tk, tv, o_ref, pa, tdo, L, R)
+    Ar = host(pa)[..., :W]
+    G2 = oracle.sa.sa_backward_band(Ar, q, k, v, do, L, R)
+    for name, got, ref in (("dQ", dq2, G2[0]), ("dK", dk2, G2[1]), ("dV", dv2, G2[2])):
+        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
+
+
+def test_sa_stored_band_errors():
+    s = sattn()
+    q = torch.zeros(1, 1, 16, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(s.SattnError):
+        s.sa_forward_p(q, q, q, 3, 1, impl="tc")
+    with pytest.raises(s.SattnError):
+        s.sa_forward_p(q.cpu(), q.cpu(), q.cpu(), 3, 1)
+
+
+def test_sa_stored_band_deterministic():
+    s = sattn()
+    shape, L, R = (2, 2, 600, 64), 32, 8
+    q, k, v = (dev(x, "bf16") for x in synth.qkv(12, shape, "bf16"))
+    do = dev(synth.grad_out(12, shape, "bf16"), "bf16")
+    o, lse, p = s.sa_forward_p(q, k, v, L, R)
+    r1 = s.sa_backward_p(q, k, v, o, p, do, L, R)
+    r2 = s.sa_backward_p(q, k, v, o, p, do, L, R)
+    for a, b in zip(r1, r2):
+        assert torch.equal(a, b)
+    o2, _ = s.sa_forward(q, k, v, L, R, impl="ffma")
+    assert torch.equal(o, o2)   # the band store does not change the forward's arithmetic
