@@ -307,6 +307,14 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
 
+    band = None
+    if not args.no_band:
+        torch.cuda.empty_cache()
+        try:
+            band = run_band(args, sattn, dev, rnd, barrier, world, stream, hbm)
+        except Exception as e:
+            band = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     hour = None
     if not args.no_hour:
         torch.cuda.empty_cache()
@@ -343,7 +351,7 @@ def run_gpu(args):
                       "B": B, "H": H, "T": T, "D": D, "L": L, "R": R, "layers": NL, "global_batch": B * world,
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
-           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa,
+           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, "band": band,
            "hour": hour, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
@@ -395,6 +403,73 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
     return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
             "channels": C, "hbm_frac": round(bytes_step / (ms / 1e3) / 1e9 / hbm, 4), "steps": k,
             "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
+
+
+def run_band(args, sattn, dev, rnd, barrier, world, stream, hbm):
+    """NEXT-4: the same 12-layer SA step in the paper's stored-band mode (a_t kept as
+    [B,H,T,ld] bf16 by the forward and read by the backward) instead of LSE + recompute.
+    Algorithmic bytes per head-frame: forward 516 + 2W (the band write), backward
+    Q,K,V,dO + band + dQ,dK,dV = 896 + 2W (no O, no LSE: delta = rowsum(P o dP))."""
+    import ctypes
+    import torch
+    lib = sattn.lib()
+    shp = (B, H, T, D)
+    bf = torch.bfloat16
+    desc = sattn.make_desc(B, H, T, D, L, R, sattn.BF16, impl=args.kernels)
+    pd = ctypes.byref(desc)
+    ld = int(lib.sa_p_ld(pd))
+    Q, K, V, dO = ([rnd(*shp) for _ in range(NL)] for _ in range(4))
+    O = [torch.empty(shp, device=dev, dtype=bf) for _ in range(NL)]
+    LSE = [torch.empty(shp[:-1], device=dev, dtype=torch.float32) for _ in range(NL)]
+    Pb = [torch.empty(shp[:-1] + (ld,), device=dev, dtype=bf) for _ in range(NL)]
+    dQ, dK, dV = ([torch.empty(shp, device=dev, dtype=bf) for _ in range(NL)] for _ in range(3))
+    nws = lib.sa_backward_p_workspace(pd)
+    ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    sp = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+
+    def fwd():
+        for l in range(NL):
+            assert lib.sa_forward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(Pb[l]), sp()) == 0, \
+                lib.sattn_last_error()
+
+    def bwd():
+        for l in reversed(range(NL)):
+            assert lib.sa_backward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(Pb[l]), P(dO[l]), P(dQ[l]), P(dK[l]),
+                                     P(dV[l]), P(ws), nws, sp()) == 0, lib.sattn_last_error()
+
+    fwd(); bwd()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(dev)
+    gF, gB = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gF, stream=cap):
+        fwd()
+    with torch.cuda.graph(gB, stream=cap):
+        bwd()
+    for _ in range(max(3, args.warmup)):
+        gF.replay(); gB.replay()
+    barrier()
+    k = max(2, min(args.steps, 10))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k + 1)]
+    evs[0].record(stream)
+    for i in range(k):
+        gF.replay(); evs[2 * i + 1].record(stream)
+        gB.replay(); evs[2 * i + 2].record(stream)
+    barrier()
+    f_ms = sum(evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(k)) / k
+    b_ms = sum(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]) for i in range(k)) / k
+    ms = f_ms + b_ms
+    W = L + R + 1
+    fb, bb = FWD_BYTES + 2 * W, 896 + 2 * W
+    units = B * H * T
+    return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4), "steps": k,
+            "per_call_ms": {"sa_forward_p": round(f_ms / NL, 4), "sa_backward_p": round(b_ms / NL, 4)},
+            "algorithmic_bytes_per_head_frame": {"forward": fb, "backward": bb},
+            "hbm_frac": {"sa_forward_p": round(fb * units / (f_ms / NL / 1e3) / 1e9 / hbm, 4),
+                         "sa_backward_p": round(bb * units / (b_ms / NL / 1e3) / 1e9 / hbm, 4),
+                         "step": round((fb + bb) * units * NL / (ms / 1e3) / 1e9 / hbm, 4)},
+            "band_bytes_per_layer": units * ld * 2, "lse_bytes_per_layer": units * 4,
+            "workload": "12 layers x (sa_forward_p + sa_backward_p), untied per-layer inputs, stored band bf16"}
 
 
 def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
@@ -650,6 +725,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
     ap.add_argument("--no-hour", action="store_true")
+    ap.add_argument("--no-band", action="store_true")
     ap.add_argument("--no-encoder", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

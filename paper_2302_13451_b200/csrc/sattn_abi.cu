@@ -345,9 +345,16 @@ sattn_status sa_forward_p(const sattn_desc* d, const void* Q, const void* K, con
   if (!Q || !K || !V || !O || !LSE || !P) return fail(SATTN_EARG, "NULL tensor pointer");
   if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE) || !aligned16(P))
     return fail(SATTN_EARG, "tensor pointers must be 16-byte aligned");
-  if (d->impl == SATTN_IMPL_TC) return fail(SATTN_EUNSUPPORTED, "stored-band SA runs on the CUDA-core kernels");
+  const bool tc = d->impl != SATTN_IMPL_FFMA && tc_p_supported(d->dtype, (int)d->D, d->L, d->R, false);
+  if (d->impl == SATTN_IMPL_TC && !tc)
+    return fail(SATTN_EUNSUPPORTED, "tensor-core stored-band forward needs bf16, D=64, L+R+1 <= 64");
   AttnArgs a = make_args(d, false);
   a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE; a.P = P; a.ldp = (int)p_ld(d);
+  if (tc) {
+    r = tc_forward_p(a, (cudaStream_t)stream);
+    if (r != SATTN_OK) return fail(r, "tc_forward_p: %s", tc_last_error());
+    return after_launch("tc_forward_p");
+  }
   return ffma_forward_p(d, a, (cudaStream_t)stream);
 }
 
@@ -366,10 +373,20 @@ sattn_status sa_backward_p(const sattn_desc* d, const void* Q, const void* K, co
     if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
   if (ws_bytes < sa_backward_p_workspace(d))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, sa_backward_p_workspace(d));
-  if (d->impl == SATTN_IMPL_TC) return fail(SATTN_EUNSUPPORTED, "stored-band SA runs on the CUDA-core kernels");
+  const bool tc = d->impl != SATTN_IMPL_FFMA && tc_p_supported(d->dtype, (int)d->D, d->L, d->R, true);
+  if (d->impl == SATTN_IMPL_TC && !tc)
+    return fail(SATTN_EUNSUPPORTED, "tensor-core stored-band backward needs bf16, D=64, L+R+1 <= 49");
   AttnArgs a = make_args(d, false);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.dO = dO; a.P = const_cast<void*>(P); a.ldp = (int)p_ld(d);
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
+  if (tc) {
+    r = tc_backward_p(a, (cudaStream_t)stream);
+    if (r != SATTN_OK) return fail(r, "tc_backward_p: %s", tc_last_error());
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_backward_p launch: %s", cudaGetErrorString(e));
+    return SATTN_OK;
+  }
   return ffma_backward_p(d, a, (cudaStream_t)stream);
 }
 

@@ -11,7 +11,10 @@ bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward);
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
 int tc_backward_launches();
-size_t tc_backward_ws_bytes();   // SA tensor-core backward: CTA hand-off rows (fused sweep)
+size_t tc_backward_ws_bytes();
+bool tc_p_supported(int dtype, int D, int L, int R, bool backward);   // stored-band mode (NEXT-4)
+sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st);
+sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st);   // SA tensor-core backward: CTA hand-off rows (fused sweep)
 const char* tc_last_error();
 void tc_set_trace(void* p);  // debug only
 // tensor-core LLSA forward (tc_llsa.cu)

@@ -72,6 +72,7 @@ struct TcArgs {
   int nch;                                       // K1: channels in one launch (LLSA band pass: C; SA: 1)
   int bcast;                                     // K1: Q is one plane read as every channel (LLSA layer 1)
   float* ws_hand;                                // fused backward: per-CTA dQ hand-off rows [grid][48][64] fp32
+  int ldp;                                       // stored-band mode: row stride of P [BH][T][ldp] (bf16)
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
@@ -186,10 +187,14 @@ __device__ __forceinline__ void tmem_row64_to_smem_sw128(uint32_t taddr, float s
                                 pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc)));
 }
 
-template <int CW>
+// PST: the stored-band mode (NEXT-4) -- the softmax warpgroup also writes its row of
+// a_t (bf16, band layout [BH][T][ldp], zeros outside the clipped window) through the O staging
+// tile and a TMA store (tmP: box (ldp, 128, 1)) before the O epilogue.
+template <int CW, bool PST = false>
 __global__ void __launch_bounds__(320, 1)
     sa_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, TcArgs a) {
+              const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+              const __grid_constant__ CUtensorMap tmP, TcArgs a) {
   using C = FwdCfg<CW>;
   constexpr int NK = C::NK, NQK = C::NQK, NV = C::NV;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -352,6 +357,24 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(&pfull[b]);
       if (tr) trace_at(a.trace, 5, k);
+      if constexpr (PST) {   // a_t row -> staging row r (ldp bf16) -> TMA store (rows >= T clipped)
+        if (leader) tc::bulk_wait_read0();
+        tc::named_bar(1 + wg, 128);
+        const float inv = 1.f / l;
+        const uint32_t prow = tc::smem_u32(ostage) + r * a.ldp * 2;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          const int j = i - lane;   // band index of register i (zero outside [lo, hi) already)
+          if (j >= 0 && j < W) tc::st_shared_u16(prow + 2 * j, __bfloat16_as_ushort(__float2bfloat16_rn(s[i] * inv)));
+        }
+        for (int j = W; j < a.ldp; ++j) tc::st_shared_u16(prow + 2 * j, 0);
+        tc::fence_proxy_async_smem();
+        tc::named_bar(1 + wg, 128);
+        if (leader) {
+          tc::tma_store_3d(&tmP, ostage, 0, t0, bh);
+          tc::bulk_commit();
+        }
+      }
       // epilogue (the other warpgroup runs the next tile's softmax meanwhile)
       tc::mbar_wait(&ofull[b], use & 1);
       if (tr) trace_at(a.trace, 6, k);
@@ -422,7 +445,9 @@ template <int CW> struct DqCfg {
   static constexpr int THREADS = 320;
 };
 
-template <int CW>
+// PST (stored-band mode): tmQ maps the band P [BH][T][ldp] (box (ldp, 128, 1)) and the tile's
+// P rows are staged in the Q slot; no S MMA, no exponentials: the warpgroup reads P from smem.
+template <int CW, bool PST = false>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -483,6 +508,11 @@ __global__ void __launch_bounds__(320, 1)
         const int st = k % NS;
         uint8_t* b0 = stage0 + st * C::STAGE;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
+        if constexpr (PST) {
+          tc::mbar_expect_tx(&full[st], kM * a.ldp * 2 + C::QB + 2 * C::KB);
+          tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
+          tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
+        } else {
         tc::mbar_expect_tx(&full[st], 2 * C::QB + 2 * C::KB);
         if (nch > 1) {   // LLSA: [C][BH][T][64] maps
           tc::tma_load_4d(b0, &tmQ, &full[st], 0, t0, bh, a.bcast ? 0 : c);
@@ -490,6 +520,7 @@ __global__ void __launch_bounds__(320, 1)
         } else {
           tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
           tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
+        }
         }
         tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - ksh, bh);
         tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - ksh, bh);
@@ -500,8 +531,13 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idS = tc::idesc_bf16(kM, NK, 0, 0);
       constexpr uint32_t idQ = tc::idesc_bf16(kM, kD, 0, 1);
       int ns = 0, ndp = 0, ndq = 0;
+      if constexpr (PST) ns = ntile_me;   // no S: dP(k) needs its stage and X_b free (dQ(k-2) issued)
       while (ndq < ntile_me) {
-        const uint32_t m = tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
+        const uint32_t m = PST ? tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
+                                                tc::smem_u32(&tfree[ndq & 1]), ((ndq + 2) >> 1) & 1,
+                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1,
+                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1)
+                               : tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
                                           tc::smem_u32(&tfree[ndq & 1]), ((ndq + 2) >> 1) & 1,   // = (ndq-2)>>1 parity
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
                                           tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
@@ -523,7 +559,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndq;
           continue;
         }
-        if (ndp < ns && (m & 4)) {
+        if (ndp < ns && (m & 4) && (!PST || ndp < ndq + 2)) {
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
@@ -536,7 +572,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndp;
           continue;
         }
-        if (ns < ntile_me && ns < ndq + 2 && (m & 8)) {
+        if (!PST && ns < ntile_me && ns < ndq + 2 && (m & 8)) {
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
@@ -567,7 +603,7 @@ __global__ void __launch_bounds__(320, 1)
       const int t = (g % ntq) * kM + r;
       return t < T ? src[((long long)c * a.BH + g / ntq) * stride + t] * mul : 0.f;
     };
-    float lse_next = row_of(wg, a.LSEin, T, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
+    float lse_next = PST ? 0.f : row_of(wg, a.LSEin, T, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
     for (int k = wg; k < ntile_me; k += 2) {
       const int g0 = blockIdx.x + k * gridDim.x;
       const int c = g0 / tpc, g = g0 % tpc;
@@ -578,14 +614,24 @@ __global__ void __launch_bounds__(320, 1)
       const bool row_ok = t < T;
       const int b = wg, use = k >> 1;
       const float lse2 = lse_next, dx = dx_next;
-      lse_next = row_of(k + 2, a.LSEin, T, kLog2e);
+      if (!PST) lse_next = row_of(k + 2, a.LSEin, T, kLog2e);
       dx_next = row_of(k + 2, a.ws_dx, a.Tp, 1.f);
       const uint32_t x = tbase + lanes + b * 256;
+      float p[CW];
+      if constexpr (PST) {   // P from the staged band rows: register i <-> band index i - lane
+        const int st = k % NS;
+        tc::mbar_wait(&full[st], (k / NS) & 1);
+        const uint32_t prow = tc::smem_u32(stage0 + st * C::STAGE) + r * a.ldp * 2;
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+          const int j = i - lane;
+          p[i] = (j >= 0 && j < W) ? tc::ld_shared_bf16(prow + 2 * j) : 0.f;
+        }
+      } else {
       // P from S
       tc::mbar_wait(&sfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
-      float p[CW];
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
@@ -598,6 +644,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
+      }
       // delta = rowsum(P o dP), then dS from dP
       tc::mbar_wait(&dpfull[b], use & 1);
       __syncwarp();
@@ -640,7 +687,7 @@ __global__ void __launch_bounds__(320, 1)
       // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
       if (t < a.Tp) {
         a.ws_del[cbh * a.Tp + t] = row_ok ? delta : 0.f;
-        a.ws_l2[cbh * a.Tp + t] = row_ok ? lse2 : 0.f;
+        if (!PST) a.ws_l2[cbh * a.Tp + t] = row_ok ? lse2 : 0.f;
       }
       // dQ epilogue
       tc::mbar_wait(&dqfull[b], use & 1);
@@ -685,9 +732,19 @@ template <int CW> struct DkvCfg {
   static constexpr int NS = 2;
   static constexpr int SMEM = 1024 + NS * STAGE + 4 * KB + 512;
   static constexpr int THREADS = 320;
+  // stored-band mode: [P window (NQ rows x PLD bf16) | V | Q | dO | delta] (no K, no LSE)
+  static constexpr int PLD = ((CW - 31) + 7) / 8 * 8;
+  static constexpr int PB = (NQ * PLD * 2 + 1023) / 1024 * 1024;
+  static constexpr int STAGE_P = (PB + KB + 2 * QB + NQP * 4 + 1023) / 1024 * 1024;
+  // wide bands (W > 41): one staging tile per warpgroup (dV, then dK through the same tile)
+  static constexpr bool P1 = 1024 + NS * STAGE_P + 4 * KB + 512 > 232448;
+  static constexpr int SMEM_P = 1024 + NS * STAGE_P + (P1 ? 2 : 4) * KB + 512;
 };
 
-template <int CW>
+// PST (stored-band mode): tmK maps the band P [BH][T][ldp] with box (ldp, NQ, 1); the stage is
+// [P window | V | Q | dO | delta]; no S MMA, no LSE, no exponentials: the warpgroup reads
+// P^T[u][n] = P[n][u - n + L] from the staged rows.
+template <int CW, bool PST = false>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -696,12 +753,16 @@ __global__ void __launch_bounds__(320, 1)
   using C = DkvCfg<CW>;
   constexpr int NQ = C::NQ, NS = C::NS;
   constexpr int DVCOL = 176 <= 256 - 64 ? NQ : 0;   // dV after X_0, dK after X_1
+  constexpr int STG = PST ? C::STAGE_P : C::STAGE;
+  constexpr int OFF_V = PST ? C::PB : C::KB, OFF_Q = OFF_V + C::KB, OFF_DO = OFF_Q + C::QB;
+  constexpr int OFF_L2 = OFF_DO + C::QB, OFF_DEL = PST ? OFF_L2 : OFF_L2 + C::NQP * 4;
   static_assert(NQ + 64 <= 256, "TMEM layout needs NQ <= 192");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;                       // [K | V | Q | dO]
-  uint8_t* obuf0 = smem + NS * C::STAGE;        // per warpgroup: [dV | dK] staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * C::KB);
+  uint8_t* obuf0 = smem + NS * STG;             // per warpgroup: [dV | dK] staging
+  constexpr bool ONE = PST && C::P1;             // one staging tile per warpgroup
+  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + (ONE ? 2 : 4) * C::KB);
   uint64_t* full = bars;              // [NS]
   uint64_t* empty = full + NS;        // [NS]
   uint64_t* sfull = empty + NS;       // [2]
@@ -747,19 +808,24 @@ __global__ void __launch_bounds__(320, 1)
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, u0 = (g % ntq) * kM;
         const int st = k % NS;
-        uint8_t* b0 = stage0 + st * C::STAGE;
+        uint8_t* b0 = stage0 + st * STG;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         trace_at(a.trace, 0, k);
-        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
-        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
-        // LSE*log2e and delta of the NQ query columns (padded workspace rows written by K1;
-        // columns outside [0, T) are zero-filled: their Q / dO rows are zero, so they add nothing)
         const int na = (u0 - a.R) & ~3;   // floor to a multiple of 4 (also for negatives)
-        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], na, bh, 0);
-        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], na, bh, 0);
+        if constexpr (PST) {
+          tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB + 2 * C::QB + C::NQP * 4);
+          tc::tma_load_3d(b0, &tmK, &full[st], 0, u0 - a.R, bh);   // P rows of the query window
+        } else {
+          tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
+          tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
+          // LSE*log2e of the NQ query columns (padded workspace rows written by K1; columns
+          // outside [0, T) are zero-filled: their Q / dO rows are zero, so they add nothing)
+          tc::tma_load_3d(b0 + OFF_L2, &tmL2, &full[st], na, bh, 0);
+        }
+        tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
+        tc::tma_load_3d(b0 + OFF_Q, &tmQ, &full[st], 0, u0 - a.R, bh);
+        tc::tma_load_3d(b0 + OFF_DO, &tmdO, &full[st], 0, u0 - a.R, bh);
+        tc::tma_load_3d(b0 + OFF_DEL, &tmDel, &full[st], na, bh, 0);
       }
     }
   } else if (warp == 1) {
@@ -767,8 +833,13 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idS = tc::idesc_bf16(kM, NQ, 0, 0);
       constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
       int ns = 0, ndp = 0, nkv = 0;
+      if constexpr (PST) ns = ntile_me;   // no S: dP(k) needs its stage and X_b free (dV/dK(k-2) issued)
       while (nkv < ntile_me) {
-        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+        const uint32_t m = PST ? tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
+                                                tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
+                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1,
+                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1)
+                               : tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                           tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,  // = (nkv-1)>>1 parity
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
                                           tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
@@ -776,8 +847,8 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = nkv & 1, st = nkv % NS;
           const uint32_t x = tbase + b * 256;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t q = base + 2 * C::KB, dO = q + C::QB;
+          const uint32_t base = tc::smem_u32(stage0 + st * STG);
+          const uint32_t q = base + OFF_Q, dO = base + OFF_DO;
 #pragma unroll
           for (int j = 0; j < NQ / 16; ++j)
             tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO + 2048 * j), idG, j > 0);
@@ -789,11 +860,11 @@ __global__ void __launch_bounds__(320, 1)
           ++nkv;
           continue;
         }
-        if (ndp < ns && (m & 4)) {
+        if (ndp < ns && (m & 4) && (!PST || ndp < nkv + 2)) {
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
+          const uint32_t base = tc::smem_u32(stage0 + st * STG);
+          const uint32_t v = base + OFF_V, dO = base + OFF_DO;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
@@ -802,11 +873,11 @@ __global__ void __launch_bounds__(320, 1)
           ++ndp;
           continue;
         }
-        if (ns < ntile_me && ns < nkv + 2 && (m & 8)) {
+        if (!PST && ns < ntile_me && ns < nkv + 2 && (m & 8)) {
           tc::tc_fence_after();
           const int b = ns & 1;
-          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
-          const uint32_t kk = base, q = base + 2 * C::KB;
+          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * STG);
+          const uint32_t kk = base, q = base + OFF_Q;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
@@ -824,24 +895,30 @@ __global__ void __launch_bounds__(320, 1)
     const int r = 32 * q4 + lane;
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
-    uint8_t* ostage = obuf0 + wg * 2 * C::KB;  // [dV | dK]
+    uint8_t* ostage = obuf0 + wg * (ONE ? 1 : 2) * C::KB;  // [dV | dK] (ONE: dV, then dK)
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, u0 = (g % ntq) * kM;
       const int b = wg, use = k >> 1, st = k % NS;
       const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);   // column 0 sits `sh` floats into the aligned box
-      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB) + sh;
-      const float* sDel = sL2 + C::NQP;
+      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * STG + OFF_L2) + sh;
+      const float* sDel = reinterpret_cast<const float*>(stage0 + st * STG + OFF_DEL) + sh;
       tc::mbar_wait(&full[st], (k / NS) & 1);   // LSE / delta staged by the producer warp
       const bool tr = (tid == 64) || (tid == 192);
       if (tr) trace_at(a.trace, 1, k);
       const uint32_t x = tbase + lanes + b * 256;
       const int c0 = 32 * q4;
+      float p[CW];
+      if constexpr (PST) {   // column i = query u0 - R + c0 + i; its band index of key u0 + r is lane - i + W - 1
+        uint32_t pw = tc::smem_u32(stage0 + st * STG) + (c0 * a.ldp + lane + W - 1) * 2;
+        const uint32_t step = 2 * (a.ldp - 1);
+#pragma unroll
+        for (int i = 0; i < CW; ++i, pw += step) p[i] = (i >= lane && i < lane + W) ? tc::ld_shared_bf16(pw) : 0.f;
+      } else {
       tc::mbar_wait(&sfull[b], use & 1);
       if (tr) trace_at(a.trace, 2, k);
       __syncwarp();
       tc::tc_fence_after();
-      float p[CW];
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
@@ -850,6 +927,7 @@ __global__ void __launch_bounds__(320, 1)
         p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
+      }
       if (tr) trace_at(a.trace, 3, k);
       tc::mbar_wait(&dpfull[b], use & 1);
       if (tr) trace_at(a.trace, 4, k);
@@ -877,6 +955,28 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_after();
       if (leader) tc::bulk_wait_read0();
       tc::named_bar(1 + wg, 128);
+      if constexpr (ONE) {
+        float dkr[64];
+        tmem_ld64(DK + lanes, dkr);
+        tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&kvfree[b]);
+        tc::fence_proxy_async_smem();
+        tc::named_bar(1 + wg, 128);
+        if (leader) {
+          tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+          tc::bulk_commit();
+          tc::bulk_wait_read0();
+        }
+        tc::named_bar(1 + wg, 128);
+        tmem_row64_to_smem_sw128_regs(dkr, a.scale, ostage, r);
+        tc::fence_proxy_async_smem();
+        tc::named_bar(1 + wg, 128);
+        if (leader) {
+          tc::tma_store_3d(&tmdK, ostage, 0, u0, bh);
+          tc::bulk_commit();
+        }
+      } else {
       tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
       tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
       tc::tc_fence_before();
@@ -887,6 +987,7 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
         tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
         tc::bulk_commit();
+      }
       }
       if (tr) trace_at(a.trace, 7, k);
     }
@@ -2607,6 +2708,28 @@ bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows)
   return true;
 }
 
+// stored band P [BH][T][ldp] bf16 as (ldp, T, BH); box (ldp, rows, 1), no swizzle (row-major
+// [rows][ldp] in shared memory); rows outside [0, T) load as zeros and are clipped on store.
+bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) {
+    g_tc_err = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)ldp, (cuuint64_t)T, (cuuint64_t)BH};
+  cuuint64_t strides[2] = {(cuuint64_t)ldp * 2, (cuuint64_t)T * ldp * 2};
+  cuuint32_t box[3] = {(cuuint32_t)ldp, (cuuint32_t)rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_tc_err = "cuTensorMapEncodeTiled (band) failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
 // padded fp32 workspace rows [BH][Tp] viewed as a 2-D tensor (T, BH); box (rows, 1); no swizzle.
 bool make_map_f32_rows(CUtensorMap* m, const void* base, int T, int Tp, int BH, int box) {
   EncodeTiledFn enc = encoder();
@@ -2670,6 +2793,7 @@ TcArgs tc_args(const AttnArgs& a) {
   t.kshift = 0;
   t.ws_del = a.delta;
   t.ws_l2 = a.delta + (long long)a.BH * t.Tp;
+  t.ldp = a.ldp;
   return t;
 }
 
@@ -2684,7 +2808,7 @@ int num_sms() {
   return n;
 }
 
-template <int CW>
+template <int CW, bool PST = false>
 sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   using C = FwdCfg<CW>;
   TcArgs ta = tc_args(a);
@@ -2693,14 +2817,15 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   ta.ksplit_pf = 0;   // L2 prefetch of later tiles measured slower (18.7 vs 22.6 us, gpurun_out/diag8)
   if (const char* e = getenv("SATTN_FWD_PF")) ta.ksplit_pf = atoi(e);
   if (kM % ta.qsplit || (kM / ta.qsplit) % 8 || C::NK % ta.ksplit || (C::NK / ta.ksplit) % 8) ta.qsplit = ta.ksplit = 1;
-  CUtensorMap mq, mk, mv, mo;
+  CUtensorMap mq, mk, mv, mo, mp;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM / ta.qsplit) || !make_map(&mk, a.K, a.T, a.BH, C::NK / ta.ksplit) ||
       !make_map(&mv, a.V, a.T, a.BH, C::NK / ta.ksplit) || !make_map(&mo, a.Out, a.T, a.BH, kM))
     return SATTN_ECUDA;
-  cudaFuncSetAttribute(sa_fwd_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
+  cudaFuncSetAttribute(sa_fwd_tc<CW, PST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  launch_pdl(sa_fwd_tc<CW>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, ta);
+  launch_pdl(sa_fwd_tc<CW, PST>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, PST ? mp : mo, ta);
   return SATTN_OK;
 }
 
@@ -2926,6 +3051,65 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
 }
 
 int tc_backward_launches() { return sa_bwd_split() ? 2 : 1; }
+
+// ---- stored-band mode (NEXT-4): forward W <= 64 (P staging rows fit the O tile), backward
+// W <= 49 (the P window replaces K in the two-stage K2 stage; for W > 41 with one dV/dK
+// staging tile per warpgroup)
+bool tc_p_supported(int dtype, int D, int L, int R, bool backward) {
+  const int W = L + R + 1;
+  if (dtype != SATTN_BF16 || D != 64 || L < 0 || R < 0) return false;
+  return backward ? cw_of(W) > 0 && cw_of(W) <= 80 : W <= 64;
+}
+
+sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st) {
+  switch (cw_of(a.L + a.R + 1)) {
+    case 32: return fwd_launch<32, true>(a, st);
+    case 48: return fwd_launch<48, true>(a, st);
+    case 64: return fwd_launch<64, true>(a, st);
+    case 72: return fwd_launch<72, true>(a, st);
+    case 80: return fwd_launch<80, true>(a, st);
+    case 96: return fwd_launch<96, true>(a, st);
+  }
+  g_tc_err = "band too wide for the tensor-core stored-band forward";
+  return SATTN_EUNSUPPORTED;
+}
+
+template <int CW>
+sattn_status bwd_p_launch(const AttnArgs& a, cudaStream_t st) {
+  using K2 = DkvCfg<CW>;
+  static_assert(K2::SMEM_P <= 232448, "stored-band K2 stage");
+  constexpr int NK = nk_of(CW);
+  const int Tp = (a.T + 3) & ~3;
+  CUtensorMap mp128, mk, mv, mdo, mdq, mqN, mpN, mv128, mdoN, mdk, mdv, mdel;
+  if (!make_map_p(&mp128, a.P, a.T, a.BH, a.ldp, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) ||
+      !make_map(&mv, a.V, a.T, a.BH, NK) || !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
+      !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, K2::NQ) ||
+      !make_map_p(&mpN, a.P, a.T, a.BH, a.ldp, K2::NQ) || !make_map(&mv128, a.V, a.T, a.BH, kM) ||
+      !make_map(&mdoN, a.dO, a.T, a.BH, K2::NQ) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
+      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, K2::NQP))
+    return SATTN_ECUDA;
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  cudaFuncSetAttribute(sa_bwd_dq_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+  launch_pdl(sa_bwd_dq_tc<CW, true>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mp128, mk, mv, mdo,
+             mdq, tc_args(a));
+  cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K2::SMEM_P);
+  launch_pdl(sa_bwd_dkdv_tc<CW, true>, dim3(grid), dim3(K2::THREADS), K2::SMEM_P, st, mqN, mpN, mv128, mdoN, mdk,
+             mdv, mdel, mdel, tc_args(a));
+  return SATTN_OK;
+}
+
+sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st) {
+  switch (cw_of(a.L + a.R + 1)) {
+    case 32: return bwd_p_launch<32>(a, st);
+    case 48: return bwd_p_launch<48>(a, st);
+    case 64: return bwd_p_launch<64>(a, st);
+    case 72: return bwd_p_launch<72>(a, st);
+    case 80: return bwd_p_launch<80>(a, st);
+  }
+  g_tc_err = "band too wide for the tensor-core stored-band backward";
+  return SATTN_EUNSUPPORTED;
+}
 size_t tc_backward_ws_bytes() { return fused_ws_bytes(); }
 
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {

@@ -16,7 +16,8 @@ CASES = [
     ((2, 3, 37, 4), 5, 0, "f32"), ((1, 2, 129, 64), 32, 8, "f32"), ((1, 2, 300, 64), 200, 150, "f32"),
     ((1, 1, 1, 8), 3, 2, "f32"), ((1, 2, 65, 2), 1, 1, "f32"), ((1, 1, 200, 32), 0, 63, "f32"),
     ((2, 2, 1750, 64), 32, 8, "bf16"), ((1, 2, 300, 64), 32, 16, "bf16"), ((1, 3, 777, 64), 32, 32, "bf16"),
-    ((1, 2, 130, 16), 7, 3, "bf16"),
+    ((1, 2, 130, 16), 7, 3, "bf16"), ((1, 2, 129, 64), 0, 0, "bf16"), ((3, 2, 300, 64), 24, 0, "bf16"),
+    ((1, 3, 777, 64), 16, 8, "bf16"), ((2, 1, 1000, 64), 40, 23, "bf16"), ((1, 1, 5, 64), 2, 2, "bf16"),
 ]
 
 
@@ -24,14 +25,18 @@ def _ld(L, R):
     return (L + R + 1 + 7) // 8 * 8
 
 
+@pytest.mark.parametrize("impl", ["auto", "ffma"])
 @pytest.mark.parametrize("shape,L,R,dt", CASES)
-def test_sa_stored_band(shape, L, R, dt):
+def test_sa_stored_band(shape, L, R, dt, impl):
+    # auto: tensor cores for bf16 D=64 (forward W <= 64, backward W <= 49), CUDA cores otherwise
     s = sattn()
+    if impl == "ffma" and dt == "f32":
+        pytest.skip("fp32 runs on the CUDA-core kernels under auto already")
     q, k, v = synth.qkv(11, shape, dt)
     do = synth.grad_out(11, shape, dt)
     tq, tk, tv, tdo = (dev(x, dt) for x in (q, k, v, do))
     W = L + R + 1
-    o, lse, p = s.sa_forward_p(tq, tk, tv, L, R)
+    o, lse, p = s.sa_forward_p(tq, tk, tv, L, R, impl=impl)
     assert p.shape == tuple(shape[:-1]) + (_ld(L, R),) and p.dtype == tq.dtype
     O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
     A = oracle.sa.sa_band_probs(q, k, L, R)
@@ -45,7 +50,7 @@ def test_sa_stored_band(shape, L, R, dt):
     u = t - L + np.arange(W)[None, :]
     assert (ph[..., :W][..., (u < 0) | (u >= shape[2])] == 0).all()
     # backward from the GPU's own band
-    dq, dk, dv = s.sa_backward_p(tq, tk, tv, o, p, tdo, L, R)
+    dq, dk, dv = s.sa_backward_p(tq, tk, tv, o, p, tdo, L, R, impl=impl)
     G = oracle.sa.sa_backward(q, k, v, do, L, R)
     for name, got, ref in (("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
         assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
@@ -53,7 +58,7 @@ def test_sa_stored_band(shape, L, R, dt):
     pa = torch.zeros_like(p)
     pa[..., :W] = dev(A, dt)
     o_ref = dev(O, dt)
-    dq2, dk2, dv2 = s.sa_backward_p(tq, tk, tv, o_ref, pa, tdo, L, R)
+    dq2, dk2, dv2 = s.sa_backward_p(tq, tk, tv, o_ref, pa, tdo, L, R, impl=impl)
     Ar = host(pa)[..., :W]
     G2 = oracle.sa.sa_backward_band(Ar, q, k, v, do, L, R)
     for name, got, ref in (("dQ", dq2, G2[0]), ("dK", dk2, G2[1]), ("dV", dv2, G2[2])):
@@ -64,7 +69,12 @@ def test_sa_stored_band_errors():
     s = sattn()
     q = torch.zeros(1, 1, 16, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(s.SattnError):
-        s.sa_forward_p(q, q, q, 3, 1, impl="tc")
+        s.sa_forward_p(q.float(), q.float(), q.float(), 3, 1, impl="tc")
+    with pytest.raises(s.SattnError):
+        s.sa_forward_p(q, q, q, 40, 40, impl="tc")        # W = 81 > 64
+    o, lse, p = s.sa_forward_p(q, q, q, 32, 24, impl="tc")
+    with pytest.raises(s.SattnError):
+        s.sa_backward_p(q, q, q, o, p, q, 32, 24, impl="tc")   # W = 57 > 49
     with pytest.raises(s.SattnError):
         s.sa_forward_p(q.cpu(), q.cpu(), q.cpu(), 3, 1)
 
@@ -79,5 +89,8 @@ def test_sa_stored_band_deterministic():
     r2 = s.sa_backward_p(q, k, v, o, p, do, L, R)
     for a, b in zip(r1, r2):
         assert torch.equal(a, b)
-    o2, _ = s.sa_forward(q, k, v, L, R, impl="ffma")
+    o2, _ = s.sa_forward(q, k, v, L, R)
     assert torch.equal(o, o2)   # the band store does not change the forward's arithmetic
+    of, _, pf = s.sa_forward_p(q, k, v, L, R, impl="ffma")
+    assert torch.equal(of, s.sa_forward(q, k, v, L, R, impl="ffma")[0])
+    assert (p.float() - pf.float()).abs().max().item() <= 4e-3   # tensor-core band == CUDA-core band
