@@ -143,16 +143,36 @@ def run_gpu(args):
         if st != 0:
             raise RuntimeError(f"{what}: {lib.sattn_last_error().decode()}")
 
+    # mode "band" (default): the paper's stored a_t -- sa_forward_p keeps the band,
+    # sa_backward_p reads it; mode "lse": LSE + recompute (sa_forward / sa_backward).  Same
+    # outputs (dQ, dK, dV of the same SA layer), different memory / recompute trade-off.
+    band = args.mode == "band"
+    W = L + R + 1
+    Pbs = [torch.empty(shp[:-1] + (int(lib.sa_p_ld(pd)),), device=dev, dtype=bf) for _ in range(NL)] if band else LSEs
+    FB, BB = (FWD_BYTES + 2 * W, 896 + 2 * W) if band else (FWD_BYTES, BWD_BYTES)
+    KF, KB = ("sa_forward_p", "sa_backward_p") if band else ("sa_forward", "sa_backward")
+
+    def fcall(q, k, v, o, lse, pb, sp):
+        if band:
+            check(lib.sa_forward_p(pd, P(q), P(k), P(v), P(o), P(lse), P(pb), sp), KF)
+        else:
+            check(lib.sa_forward(pd, P(q), P(k), P(v), P(o), P(lse), sp), KF)
+
+    def bcall(q, k, v, o, lse, pb, do, dq, dk, dv, sp):
+        if band:
+            check(lib.sa_backward_p(pd, P(q), P(k), P(v), P(o), P(pb), P(do), P(dq), P(dk), P(dv), P(ws), nws, sp), KB)
+        else:
+            check(lib.sa_backward(pd, P(q), P(k), P(v), P(o), P(lse), P(do), P(dq), P(dk), P(dv), P(ws), nws, sp), KB)
+
     def fwd_pass():
         sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         for l in range(NL):
-            check(lib.sa_forward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), sp), "sa_forward")
+            fcall(Qs[l], Ks[l], Vs[l], Os[l], LSEs[l], Pbs[l], sp)
 
     def bwd_pass():
         sp = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
         for l in reversed(range(NL)):
-            check(lib.sa_backward(pd, P(Qs[l]), P(Ks[l]), P(Vs[l]), P(Os[l]), P(LSEs[l]), P(dOs[l]),
-                                  P(dQs[l]), P(dKs[l]), P(dVs[l]), P(ws), nws, sp), "sa_backward")
+            bcall(Qs[l], Ks[l], Vs[l], Os[l], LSEs[l], Pbs[l], dOs[l], dQs[l], dKs[l], dVs[l], sp)
 
     # The step is captured once as two CUDA graphs (forward pass, backward pass) so the timed
     # region measures GPU execution, not Python/ctypes launch overhead; an event between the two
@@ -210,7 +230,7 @@ def run_gpu(args):
     bwd_ms = float(np.mean([a.elapsed_time(b) for a, b in ev["bwd"]])) / NL
     units = B * H * T  # head-frames per launch
     hbm, tc_peak, peak_kind = load_peaks()
-    kern = {"sa_forward": (fwd_ms, FWD_BYTES * units), "sa_backward": (bwd_ms, BWD_BYTES * units)}
+    kern = {KF: (fwd_ms, FB * units), KB: (bwd_ms, BB * units)}
     dom = max(kern, key=lambda k: kern[k][0])
     achieved = kern[dom][1] / (kern[dom][0] / 1e3) / 1e9
     traffic = load_traffic(dom, args.kernels)
@@ -219,7 +239,8 @@ def run_gpu(args):
                 "algorithmic_bytes_per_launch": kern[dom][1],
                 "per_call_ms": {k: round(v[0], 4) for k, v in kern.items()},
                 "step_frac": {k: round(v[0] * NL / ms_per_step, 3) for k, v in kern.items()},
-                "step_hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * NL / (ms_per_step / 1e3) / 1e9 / hbm, 4)}
+                "algorithmic_bytes_per_head_frame": {KF: FB, KB: BB},
+                "step_hbm_frac": round((FB + BB) * units * NL / (ms_per_step / 1e3) / 1e9 / hbm, 4)}
 
     # ---------------- e2e through the public API with host buffers (pinned), H2D + D2H inside
     # Every step copies its inputs (all layers' Q, K, V, dO) from pinned host memory and reads
@@ -240,15 +261,15 @@ def run_gpu(args):
         ev = lambda: torch.cuda.Event()  # noqa: E731
         # two device buffer sets, alternating by step: the H2D of step i+1 need not wait for
         # step i's compute to release its inputs
-        sets = [(Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs),
-                tuple([torch.empty_like(t) for t in ts] for ts in (Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs))]
+        sets = [(Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs, Pbs),
+                tuple([torch.empty_like(t) for t in ts] for ts in (Qs, Ks, Vs, dOs, Os, LSEs, dQs, dKs, dVs, Pbs))]
         used = [[None] * NL for _ in range(2)]      # compute finished reading set p, layer l
         drained = [[None] * NL for _ in range(2)]   # D2H of set p, layer l finished
         par = [0]
 
         def e2e_step():
             p_ = par[0]; par[0] ^= 1
-            q_, k_, v_, do_, o_, lse_, dq_, dk_, dv_ = sets[p_]
+            q_, k_, v_, do_, o_, lse_, dq_, dk_, dv_, pb_ = sets[p_]
             landed = []
             for l in range(NL):
                 s_in = s_ins[l % n_in]
@@ -261,12 +282,11 @@ def run_gpu(args):
             spp = ctypes.c_void_p(stream.cuda_stream)
             for l in range(NL):
                 stream.wait_event(landed[l])
-                check(lib.sa_forward(pd, P(q_[l]), P(k_[l]), P(v_[l]), P(o_[l]), P(lse_[l]), spp), "sa_forward")
+                fcall(q_[l], k_[l], v_[l], o_[l], lse_[l], pb_[l], spp)
             for l in reversed(range(NL)):
                 if drained[p_][l] is not None:
                     stream.wait_event(drained[p_][l])
-                check(lib.sa_backward(pd, P(q_[l]), P(k_[l]), P(v_[l]), P(o_[l]), P(lse_[l]), P(do_[l]),
-                                      P(dq_[l]), P(dk_[l]), P(dv_[l]), P(ws), nws, spp), "sa_backward")
+                bcall(q_[l], k_[l], v_[l], o_[l], lse_[l], pb_[l], do_[l], dq_[l], dk_[l], dv_[l], spp)
                 e = ev(); e.record(stream); used[p_][l] = e
                 with torch.cuda.stream(s_out):
                     s_out.wait_event(e)
@@ -307,13 +327,13 @@ def run_gpu(args):
         torch.cuda.empty_cache()
         llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
 
-    band = None
-    if not args.no_band:
+    alt = None   # the other SA mode, same workload
+    if not args.no_alt:
         torch.cuda.empty_cache()
         try:
-            band = run_band(args, sattn, dev, rnd, barrier, world, stream, hbm)
+            alt = run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, "lse" if band else "band")
         except Exception as e:
-            band = {"error": f"{type(e).__name__}: {e}"[:300]}
+            alt = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     hour = None
     if not args.no_hour:
@@ -348,10 +368,12 @@ def run_gpu(args):
            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic iid N(0,1) activations",
            "config": {"workload": "wav2vec2-base attention core: 12 layers x (SA fwd + SA bwd), untied per-layer "
                                   "Q/K/V/dO, bf16 in/out, fp32 accumulate",
+                      "mode": "stored band a_t (P:L342): sa_forward_p + sa_backward_p" if band
+                              else "LSE + recompute: sa_forward + sa_backward",
                       "B": B, "H": H, "T": T, "D": D, "L": L, "R": R, "layers": NL, "global_batch": B * world,
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
-           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, "band": band,
+           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, ("lse_mode" if band else "band_mode"): alt,
            "hour": hour, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
@@ -405,11 +427,12 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
             "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
 
 
-def run_band(args, sattn, dev, rnd, barrier, world, stream, hbm):
-    """NEXT-4: the same 12-layer SA step in the paper's stored-band mode (a_t kept as
-    [B,H,T,ld] bf16 by the forward and read by the backward) instead of LSE + recompute.
-    Algorithmic bytes per head-frame: forward 516 + 2W (the band write), backward
-    Q,K,V,dO + band + dQ,dK,dV = 896 + 2W (no O, no LSE: delta = rowsum(P o dP))."""
+def run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, mode):
+    """The same 12-layer SA step in the other mode: "band" = the paper's stored a_t
+    ([B,H,T,ld] bf16 kept by the forward and read by the backward; NEXT-4), "lse" =
+    LSE + recompute.  Algorithmic bytes per head-frame: band forward 516 + 2W (the band write),
+    backward Q,K,V,dO + band + dQ,dK,dV = 896 + 2W (no O, no LSE: delta = rowsum(P o dP));
+    lse 516 / 1028."""
     import ctypes
     import torch
     lib = sattn.lib()
@@ -428,15 +451,24 @@ def run_band(args, sattn, dev, rnd, barrier, world, stream, hbm):
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     sp = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
 
+    bm = mode == "band"
+    if not bm:
+        nws = lib.sa_backward_workspace(pd)
+        ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+
     def fwd():
         for l in range(NL):
-            assert lib.sa_forward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(Pb[l]), sp()) == 0, \
-                lib.sattn_last_error()
+            st = (lib.sa_forward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(Pb[l]), sp()) if bm else
+                  lib.sa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), sp()))
+            assert st == 0, lib.sattn_last_error()
 
     def bwd():
         for l in reversed(range(NL)):
-            assert lib.sa_backward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(Pb[l]), P(dO[l]), P(dQ[l]), P(dK[l]),
-                                     P(dV[l]), P(ws), nws, sp()) == 0, lib.sattn_last_error()
+            st = (lib.sa_backward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(Pb[l]), P(dO[l]), P(dQ[l]), P(dK[l]),
+                                    P(dV[l]), P(ws), nws, sp()) if bm else
+                  lib.sa_backward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(dO[l]), P(dQ[l]), P(dK[l]),
+                                  P(dV[l]), P(ws), nws, sp()))
+            assert st == 0, lib.sattn_last_error()
 
     fwd(); bwd()
     torch.cuda.synchronize()
@@ -460,16 +492,17 @@ def run_band(args, sattn, dev, rnd, barrier, world, stream, hbm):
     b_ms = sum(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]) for i in range(k)) / k
     ms = f_ms + b_ms
     W = L + R + 1
-    fb, bb = FWD_BYTES + 2 * W, 896 + 2 * W
+    fb, bb = (FWD_BYTES + 2 * W, 896 + 2 * W) if bm else (FWD_BYTES, BWD_BYTES)
+    kf, kb = ("sa_forward_p", "sa_backward_p") if bm else ("sa_forward", "sa_backward")
     units = B * H * T
-    return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4), "steps": k,
-            "per_call_ms": {"sa_forward_p": round(f_ms / NL, 4), "sa_backward_p": round(b_ms / NL, 4)},
-            "algorithmic_bytes_per_head_frame": {"forward": fb, "backward": bb},
-            "hbm_frac": {"sa_forward_p": round(fb * units / (f_ms / NL / 1e3) / 1e9 / hbm, 4),
-                         "sa_backward_p": round(bb * units / (b_ms / NL / 1e3) / 1e9 / hbm, 4),
+    return {"mode": mode, "value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 4),
+            "steps": k, "per_call_ms": {kf: round(f_ms / NL, 4), kb: round(b_ms / NL, 4)},
+            "algorithmic_bytes_per_head_frame": {kf: fb, kb: bb},
+            "hbm_frac": {kf: round(fb * units / (f_ms / NL / 1e3) / 1e9 / hbm, 4),
+                         kb: round(bb * units / (b_ms / NL / 1e3) / 1e9 / hbm, 4),
                          "step": round((fb + bb) * units * NL / (ms / 1e3) / 1e9 / hbm, 4)},
             "band_bytes_per_layer": units * ld * 2, "lse_bytes_per_layer": units * 4,
-            "workload": "12 layers x (sa_forward_p + sa_backward_p), untied per-layer inputs, stored band bf16"}
+            "workload": f"12 layers x ({kf} + {kb}), untied per-layer inputs, bf16"}
 
 
 def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
@@ -725,7 +758,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stream", action="store_true")
     ap.add_argument("--no-hour", action="store_true")
-    ap.add_argument("--no-band", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other SA mode's sub-measurement")
+    ap.add_argument("--mode", default="band", choices=["band", "lse"],
+                    help="headline SA mode: stored band a_t (paper P:L342) or LSE + recompute")
     ap.add_argument("--no-encoder", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()

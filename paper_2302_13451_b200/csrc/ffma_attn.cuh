@@ -336,8 +336,12 @@ __device__ __forceinline__ void dkdv_row(const float* qr, const float* dor, floa
   constexpr int HD = D / 2;
   const float dp = pair_sum(dot<HD>(dor, v));
   float p;
-  if constexpr (PST) p = valid ? pst : 0.f;
-  else p = valid ? exp2f(pair_sum(dot<HD>(qr, k)) * scale_log2 - lse2) : 0.f;
+  if constexpr (PST) {
+    p = valid ? pst : 0.f;
+  } else {
+    const float sc = pair_sum(dot<HD>(qr, k)) * scale_log2;   // every lane: pair_sum is a shuffle
+    p = valid ? exp2f(sc - lse2) : 0.f;
+  }
   const float ds = p * (dp - delta);
 #pragma unroll
   for (int i = 0; i < HD; ++i) {

@@ -87,16 +87,30 @@ __device__ __forceinline__ uint32_t mbar_test4(uint32_t a0, uint32_t p0, uint32_
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
   uint32_t n = 0;
-  while (!mbar_try_wait(a, phase)) {
-    if (++n > (1u << 28)) __trap();
+  long long t0 = 0;
+  while (!mbar_try_wait(a, phase)) {   // a wait that never completes is a bug: trap after ~20 s
+    if ((++n & 0x3ff) == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 20000000000LL) __trap();
+    }
   }
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void st_shared_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
 }
 __device__ __forceinline__ float ld_shared_bf16(uint32_t addr) {   // one bf16 -> fp32
   uint16_t v;
@@ -126,6 +140,7 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {

@@ -94,3 +94,25 @@ def test_sa_stored_band_deterministic():
     of, _, pf = s.sa_forward_p(q, k, v, L, R, impl="ffma")
     assert torch.equal(of, s.sa_forward(q, k, v, L, R, impl="ffma")[0])
     assert (p.float() - pf.float()).abs().max().item() <= 4e-3   # tensor-core band == CUDA-core band
+
+
+def test_sa_stored_band_full_base_shape_sampled_heads():
+    # BASELINE configs[1] (B=8, H=12, T=1750, D=64, (32,8), bf16) in the launch configuration the
+    # bench's headline (stored-band mode) times; 6 sampled heads checked element by element
+    s = sattn()
+    B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
+    W = L + R + 1
+    tq, tk, tv = (torch.randn(B, H, T, D, device="cuda", generator=torch.Generator("cuda").manual_seed(i))
+                  .to(torch.bfloat16) for i in range(3))
+    tdo = torch.randn(B, H, T, D, device="cuda", generator=torch.Generator("cuda").manual_seed(9)).to(torch.bfloat16)
+    o, lse, p = s.sa_forward_p(tq, tk, tv, L, R)
+    dq, dk, dv = s.sa_backward_p(tq, tk, tv, o, p, tdo, L, R)
+    for (b, h) in ((0, 0), (3, 7), (7, 11), (5, 2), (1, 10), (6, 5)):
+        q, k, v, do = (host(x[b, h]) for x in (tq, tk, tv, tdo))
+        O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
+        A = oracle.sa.sa_band_probs(q, k, L, R)
+        G = oracle.sa.sa_backward(q, k, v, do, L, R)
+        assert maxerr(p[b, h, :, :W], A) <= 4e-3, (b, h, "P")
+        for name, got, ref in (("O", o[b, h], O), ("LSE", lse[b, h], LSE), ("dQ", dq[b, h], G[0]),
+                               ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
+            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
