@@ -4,7 +4,9 @@ d_k = 64, N_T = 1000 frames, H in {8, 16} heads, receptive field W = A + B + 1 =
 steps of 10 (look-back B = ceil((W-1)/2), look-ahead A = floor((W-1)/2)), 5 repeats, mean.
 For each point: peak device memory of one SA forward + backward through the C ABI (bf16; the
 tensor-core kernels for W <= 65, the CUDA-core kernels beyond) per training vector (frame),
-and its time; next to masked acausal attention (MAA) as PyTorch computes it (dense T x T scores,
+and its time, for both SA modes -- LSE + recompute (sa_forward / sa_backward) and the paper's own
+stored band a_t (sa_forward_p / sa_backward_p; tensor cores for W <= 49) -- next to masked
+acausal attention (MAA) as PyTorch computes it (dense T x T scores,
 boolean band mask, softmax, autograd), which is what the paper compares against.  Writes
 profiles/r1/fig5.json and prints a markdown table.  Inputs are synthetic (iid N(0,1))."""
 import json
@@ -51,6 +53,10 @@ def run(H, B=8):
             o, lse = s.sa_forward(q, k, v, L, R)
             s.sa_backward(q, k, v, o, lse, do, L, R)
 
+        def sa_band():
+            o, lse, pb = s.sa_forward_p(q, k, v, L, R)
+            s.sa_backward_p(q, k, v, o, pb, do, L, R)
+
         idx = torch.arange(T, device=dev)
         mask = (idx[None, :] >= idx[:, None] - L) & (idx[None, :] <= idx[:, None] + R)
 
@@ -62,11 +68,14 @@ def run(H, B=8):
             y.backward(do)
 
         m_sa, t_sa = measure(sa)
+        m_sb, t_sb = measure(sa_band)
         m_maa, t_maa = measure(maa)
         frames = B * T
         rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 65 else "ffma",
+                     "band_kernels": "tcgen05" if W <= 49 else ("tcgen05 fwd + ffma bwd" if W <= 64 else "ffma"),
                      "sa_bytes_per_frame": m_sa / frames, "maa_bytes_per_frame": m_maa / frames,
-                     "sa_ms": t_sa, "maa_ms": t_maa})
+                     "sa_band_bytes_per_frame": m_sb / frames,
+                     "sa_ms": t_sa, "sa_band_ms": t_sb, "maa_ms": t_maa})
         del mask
     return rows
 
@@ -79,12 +88,13 @@ def main():
     path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1", "fig5.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
     json.dump(out, open(path, "w"), indent=1)
-    print("| H | W | kernels | SA KB/frame | MAA KB/frame | SA ms | MAA ms |")
-    print("|---|---|---|---|---|---|---|")
+    print("| H | W | kernels (lse / band) | SA KB/frame | SA-band KB/frame | MAA KB/frame | SA ms | SA-band ms | MAA ms |")
+    print("|---|---|---|---|---|---|---|---|---|")
     for r in out["rows"]:
         if r["W"] in (10, 20, 40, 50, 100, 200, 300, 490):
-            print(f"| {r['H']} | {r['W']} | {r['kernels']} | {r['sa_bytes_per_frame'] / 1024:.1f} | "
-                  f"{r['maa_bytes_per_frame'] / 1024:.1f} | {r['sa_ms']:.3f} | {r['maa_ms']:.3f} |")
+            print(f"| {r['H']} | {r['W']} | {r['kernels']} / {r['band_kernels']} | {r['sa_bytes_per_frame'] / 1024:.1f} | "
+                  f"{r['sa_band_bytes_per_frame'] / 1024:.1f} | {r['maa_bytes_per_frame'] / 1024:.1f} | "
+                  f"{r['sa_ms']:.3f} | {r['sa_band_ms']:.3f} | {r['maa_ms']:.3f} |")
 
 
 if __name__ == "__main__":
