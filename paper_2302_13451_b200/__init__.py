@@ -19,7 +19,7 @@ __all__ = [
     "MODE_SA", "MODE_LLSA", "IMPL_AUTO", "IMPL_FFMA", "IMPL_TC",
 ]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsattn.so")
+LIB_PATH = os.environ.get("SATTN_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsattn.so")
 F32, BF16 = 0, 1
 MODE_SA, MODE_LLSA = 0, 1
 IMPL_AUTO, IMPL_FFMA, IMPL_TC = 0, 1, 2
