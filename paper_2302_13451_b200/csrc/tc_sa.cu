@@ -928,13 +928,51 @@ __global__ void __launch_bounds__(320, 1)
       if (tr) trace_at(a.trace, 1, k);
       const uint32_t x = tbase + lanes + b * 256;
       const int c0 = 32 * q4;
-      float p[CW];
-      if constexpr (PST) {   // column i = query u0 - R + c0 + i; its band index of key u0 + r is lane - i + W - 1
+      if constexpr (PST) {
+        // P^T from the staged band (column i = query u0 - R + c0 + i; band index of key u0 + r is
+        // lane - i + W - 1), kept as packed bf16 pairs: the TMEM A operand needs exactly these
+        uint32_t pp[CW / 2];
         uint32_t pw = tc::smem_u32(stage0 + st * STG) + (c0 * a.ldp + lane + W - 1) * 2;
         const uint32_t step = 2 * (a.ldp - 1);
 #pragma unroll
-        for (int i = 0; i < CW; ++i, pw += step) p[i] = (i >= lane && i < lane + W) ? tc::ld_shared_bf16(pw) : 0.f;
+        for (int m = 0; m < CW / 2; ++m) {
+          const int i = 2 * m;
+          const uint32_t lo = (i >= lane && i < lane + W) ? tc::ld_shared_u16(pw) : 0u;
+          const uint32_t hi = (i + 1 >= lane && i + 1 < lane + W) ? tc::ld_shared_u16(pw + step) : 0u;
+          pp[m] = lo | (hi << 16);
+          pw += 2 * step;
+        }
+        if (tr) trace_at(a.trace, 3, k);
+        tc::mbar_wait(&dpfull[b], use & 1);
+        if (tr) trace_at(a.trace, 4, k);
+        __syncwarp();
+        tc::tc_fence_after();
+        float ds[CW];
+#pragma unroll
+        for (int j = 0; j < CW / 8; ++j) {
+          float dp[8];
+          tc::tmem_ld8(x + c0 + 8 * j, dp);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const uint32_t w = pp[(8 * j + e) / 2];
+            ds[8 * j + e] = __uint_as_float(w << 16) * (dp[e] - sDel[c0 + 8 * j + e]);
+            ds[8 * j + e + 1] = __uint_as_float(w & 0xffff0000u) * (dp[e + 1] - sDel[c0 + 8 * j + e + 1]);
+          }
+        }
+        {   // P^T -> packed columns [0, NQ/2) (as tmem_write_row, from the packed pairs)
+          const int pc0 = 16 * q4;
+#pragma unroll
+          for (int j = 0; j < CW / 8; ++j) tc::tmem_st4(x + pc0 + 4 * j, pp[4 * j], pp[4 * j + 1], pp[4 * j + 2], pp[4 * j + 3]);
+          for (int c = 0; c < NQ / 2; c += 4)
+            if (c < pc0 || c >= pc0 + CW / 2) tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
+        }
+        tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);      // dS^T -> packed columns [NQ/2, NQ)
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&pdsfull[b]);
       } else {
+      float p[CW];
       tc::mbar_wait(&sfull[b], use & 1);
       if (tr) trace_at(a.trace, 2, k);
       __syncwarp();
@@ -947,7 +985,6 @@ __global__ void __launch_bounds__(320, 1)
         p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
-      }
       if (tr) trace_at(a.trace, 3, k);
       tc::mbar_wait(&dpfull[b], use & 1);
       if (tr) trace_at(a.trace, 4, k);
@@ -967,6 +1004,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&pdsfull[b]);
+      }
       if (tr) trace_at(a.trace, 5, k);
       // dV / dK epilogue
       tc::mbar_wait(&kvfull[b], use & 1);
