@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_before();
       tc::mbar_arrive(&pfull[b]);
       if (tr) trace_at(a.trace, 5, k);
-      auto write_band = [&]() {   // a_t row -> band staging row r (ld bf16) -> TMA store (rows >= T clipped)
+      if constexpr (PST) {   // a_t row -> band staging row r (ld bf16) -> TMA store (rows >= T clipped)
         if (leader) tc::bulk_wait_read0();   // the O store of tile k - 2 has read the staging tile
         tc::named_bar(1 + wg, 128);
         const float inv = 1.f / l;
@@ -383,8 +383,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tma_store_3d(&tmP, pstage, 0, t0, bh);
           tc::bulk_commit();
         }
-      };
-      if (PST && !a.p_late) write_band();
+      }
       // epilogue (the other warpgroup runs the next tile's softmax meanwhile)
       tc::mbar_wait(&ofull[b], use & 1);
       if (tr) trace_at(a.trace, 6, k);
@@ -402,7 +401,6 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_store_3d(&tmO, ostage, 0, t0, bh);   // rows >= T are clipped by the tensor map
         tc::bulk_commit();
       }
-      if (PST && a.p_late) write_band();   // after the epilogue: TMEM buffer b is free earlier
       if (tr) trace_at(a.trace, 7, k);
     }
     if (leader) tc::bulk_wait0();
@@ -2880,7 +2878,6 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
       !make_map(&mv, a.V, a.T, a.BH, C::NK / ta.ksplit) || !make_map(&mo, a.Out, a.T, a.BH, kM))
     return SATTN_ECUDA;
   if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
-  if (const char* e = getenv("SATTN_FWD_P_LATE")) ta.p_late = atoi(e);
   cudaFuncSetAttribute(sa_fwd_tc<CW, PST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
