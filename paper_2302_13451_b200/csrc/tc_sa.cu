@@ -73,7 +73,6 @@ struct TcArgs {
   int bcast;                                     // K1: Q is one plane read as every channel (LLSA layer 1)
   float* ws_hand;                                // fused backward: per-CTA dQ hand-off rows [grid][48][64] fp32
   int ldp;                                       // stored-band mode: row stride of P [BH][T][ldp] (bf16)
-  int p_late;                                    // stored-band forward: write the band after the O epilogue
 };
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
