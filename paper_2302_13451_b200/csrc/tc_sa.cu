@@ -790,7 +790,8 @@ __global__ void __launch_bounds__(320, 1)
   // waited by alternating consumers could be passed a phase early (parity aliasing)
   uint64_t* kvfull = pdsfull + 2;     // [2]
   uint64_t* kvfree = kvfull + 2;      // [2] (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
+  uint64_t* dfull = kvfree + 2;       // [NS] PST: the stage's delta rows landed (K1's output)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + NS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
@@ -807,6 +808,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_init(&pdsfull[i], 128);
     }
     for (int i = 0; i < 2; ++i) { tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128); }
+    for (int i = 0; i < NS; ++i) tc::mbar_init(&dfull[i], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, 512);
@@ -815,12 +817,16 @@ __global__ void __launch_bounds__(320, 1)
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
   // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
-  tc::pdl_wait();
+  // Only the workspace rows (delta; LSE*log2e in the LSE mode) come from the preceding kernel
+  // (K1); K, V, Q, dO and the band were complete before K1 passed its own wait.  So the producer
+  // loads those first and waits on K1 (PDL) only before the workspace rows, which land on their
+  // own barrier (dfull): the first stages' loads and S / dP MMAs overlap K1's tail.
   tc::pdl_launch_dependents();
   const uint32_t DV = tbase + DVCOL, DK = tbase + 256 + DVCOL;
 
   if (warp == 0) {
     if (lane == 0) {
+      int nd = 0;   // PST: next tile whose delta rows are to be loaded
       for (int k = 0; k < ntile_me; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, u0 = (g % ntq) * kM;
@@ -830,19 +836,31 @@ __global__ void __launch_bounds__(320, 1)
         trace_at(a.trace, 0, k);
         const int na = (u0 - a.R) & ~3;   // floor to a multiple of 4 (also for negatives)
         if constexpr (PST) {
-          tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB + 2 * C::QB + C::NQP * 4);
+          tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB + 2 * C::QB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0 - a.R, bh);   // P rows of the query window
         } else {
-          tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
+          tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
-          // LSE*log2e of the NQ query columns (padded workspace rows written by K1; columns
-          // outside [0, T) are zero-filled: their Q / dO rows are zero, so they add nothing)
-          tc::tma_load_3d(b0 + OFF_L2, &tmL2, &full[st], na, bh, 0);
         }
         tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
         tc::tma_load_3d(b0 + OFF_Q, &tmQ, &full[st], 0, u0 - a.R, bh);
         tc::tma_load_3d(b0 + OFF_DO, &tmdO, &full[st], 0, u0 - a.R, bh);
-        tc::tma_load_3d(b0 + OFF_DEL, &tmDel, &full[st], na, bh, 0);
+        // workspace rows trail: once the first NS stages' other loads are in flight, wait for K1
+        // (PDL) and from then on load each stage's rows right after its other boxes.  LSE*log2e
+        // and delta of the NQ query columns (padded rows written by K1; columns outside [0, T)
+        // are zero-filled: their Q / dO rows are zero, so they add nothing)
+        (void)na;
+        if (k + 1 >= NS || k + 1 == ntile_me) {
+          if (nd == 0) tc::pdl_wait();   // K1 complete: its rows are visible
+          for (; nd <= k; ++nd) {
+            const int gd = blockIdx.x + nd * gridDim.x;
+            const int sd = nd % NS, nad = ((gd % ntq) * kM - a.R) & ~3;
+            uint8_t* bd = stage0 + sd * STG;
+            tc::mbar_expect_tx(&dfull[sd], (PST ? 1 : 2) * C::NQP * 4);
+            if (!PST) tc::tma_load_3d(bd + OFF_L2, &tmL2, &dfull[sd], nad, gd / ntq, 0);
+            tc::tma_load_3d(bd + OFF_DEL, &tmDel, &dfull[sd], nad, gd / ntq, 0);
+          }
+        }
       }
     }
   } else if (warp == 1) {
@@ -940,6 +958,7 @@ __global__ void __launch_bounds__(320, 1)
           pw += 2 * step;
         }
         if (tr) trace_at(a.trace, 3, k);
+        tc::mbar_wait(&dfull[st], (k / NS) & 1);   // delta rows (K1's output)
         tc::mbar_wait(&dpfull[b], use & 1);
         if (tr) trace_at(a.trace, 4, k);
         __syncwarp();
@@ -970,6 +989,7 @@ __global__ void __launch_bounds__(320, 1)
         tc::mbar_arrive(&pdsfull[b]);
       } else {
       float p[CW];
+      tc::mbar_wait(&dfull[st], (k / NS) & 1);   // LSE*log2e / delta rows (K1's output)
       tc::mbar_wait(&sfull[b], use & 1);
       if (tr) trace_at(a.trace, 2, k);
       __syncwarp();
