@@ -820,7 +820,10 @@ __global__ void __launch_bounds__(320, 1)
   // Only the workspace rows (delta; LSE*log2e in the LSE mode) come from the preceding kernel
   // (K1); K, V, Q, dO and the band were complete before K1 passed its own wait.  So the producer
   // loads those first and waits on K1 (PDL) only before the workspace rows, which land on their
-  // own barrier (dfull): the first stages' loads and S / dP MMAs overlap K1's tail.
+  // own barrier (dfull): the first stages' loads and S / dP MMAs overlap K1's tail.  Safe because
+  // K1 executes its griddepcontrol.wait before launch_dependents: K2 cannot start before every
+  // kernel ahead of K1 (the forward that wrote P, whatever wrote dO) has completed.  (K1 itself
+  // cannot do the same: its predecessor may be the forward that writes the band / LSE it reads.)
   tc::pdl_launch_dependents();
   const uint32_t DV = tbase + DVCOL, DK = tbase + 256 + DVCOL;
 
