@@ -93,3 +93,28 @@ def test_stream_state_errors(lib):
     h = ctypes.c_void_p()
     assert lib.llsa_stream_create(ctypes.byref(_desc()), 0, ctypes.byref(h)) == 1
     assert lib.llsa_stream_step(None, None, None, None, None) == 1
+
+
+def test_stored_band_abi(lib):
+    # NEXT-4 entry points: row stride = W rounded up to 8 elements (G29); workspace = delta rows;
+    # synchronous validation before anything is enqueued (no GPU needed)
+    import paper_2302_13451_b200 as pkg
+    for L, R, ld in ((5, 2, 8), (32, 8, 48), (0, 0, 8), (32, 16, 56), (7, 0, 8), (8, 0, 16)):
+        d = _desc(B=2, H=3, T=37, D=8, L=L, R=R)
+        assert lib.sa_p_ld(ctypes.byref(d)) == ld
+    d = _desc(B=2, H=3, T=37, D=8, L=5, R=2)
+    assert lib.sa_backward_p_workspace(ctypes.byref(d)) == 2 * 3 * 40 * 4
+    bad = _desc(T=0)
+    assert lib.sa_p_ld(ctypes.byref(bad)) == 0 and lib.sa_backward_p_workspace(ctypes.byref(bad)) == 0
+    p = ctypes.c_void_p(16)
+    assert lib.sa_forward_p(ctypes.byref(d), p, p, p, p, p, None, None) == 1          # NULL band
+    assert lib.sa_forward_p(ctypes.byref(d), p, p, p, p, p, ctypes.c_void_p(18), None) == 1   # misaligned
+    ws = 2 * 3 * 40 * 4
+    assert lib.sa_backward_p(ctypes.byref(d), p, p, p, p, None, p, p, p, p, p, ws, None) == 1
+    assert lib.sa_backward_p(ctypes.byref(d), p, p, p, p, p, p, p, p, p, p, ws - 4, None) == 3   # ECONFIG
+    # impl = TC outside the tensor-core limits (fp32) -> EUNSUPPORTED before any launch
+    t = _desc(B=1, H=1, T=16, D=64, L=3, R=1, impl="tc")
+    assert lib.sa_forward_p(ctypes.byref(t), p, p, p, p, p, p, None) == 4
+    tw = _desc(B=1, H=1, T=16, D=64, L=40, R=40, dtype=pkg.BF16, impl="tc")
+    assert lib.sa_forward_p(ctypes.byref(tw), p, p, p, p, p, p, None) == 4
+    assert lib.sattn_last_error()
