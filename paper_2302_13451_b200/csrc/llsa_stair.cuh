@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(256, 3) llsa_bwd_stair(StairArgs a) {
         }
       }
     }
+    // the K_h rows the dQ loop read (ldmatrix, other lanes' rows) are overwritten with dK below
+    __syncwarp();
     // ---- dV_h = P^T dO_h and dK_h = scale dS^T Q_h (16 x 64; rows c', k = c)
     {
       uint32_t ap[4], as[4];
