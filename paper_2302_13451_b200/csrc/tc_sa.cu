@@ -1423,7 +1423,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
-  tc::pdl_wait();
+  // only the LSE*log2e / delta rows come from K1: the producer waits (PDL) just before loading
+  // them (see sa_bwd_dkdv_tc for why this is safe)
   tc::pdl_launch_dependents();
   const uint32_t DV = tbase + NQ, DK = tbase + 256 + NQ;
 
@@ -1454,6 +1455,7 @@ __global__ void __launch_bounds__(320, 1)
         if (k >= 2) tc::mbar_wait(&vempty[s], ((k - 2) >> 1) & 1);
         tc::mbar_expect_tx(&vfull[s], C::KB);
         tc::tma_load_3d(v0 + s * C::KB, &tmV, &vfull[s], 0, u0, bh);
+        if (k == 0) tc::pdl_wait();
         if (k >= 2) tc::mbar_wait(&rempty[s], ((k - 2) >> 1) & 1);
         const int na = (u0 - a.R) & ~3;
         tc::mbar_expect_tx(&rfull[s], C::RW);
