@@ -139,6 +139,15 @@ def _same(ref, *ts):
             raise SattnError("Q, K, V (and dO) must share shape, dtype and device")
 
 
+def _expect(t, shape, dtype, device, name):
+    """Shape / dtype / device check of a tensor the kernels index directly (no device-side checks)."""
+    if t is None:
+        raise SattnError(f"{name} is None")
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != device:
+        raise SattnError(f"{name}: expected {tuple(shape)} {dtype} on {device}, got {tuple(t.shape)} {t.dtype} on "
+                         f"{t.device}")
+
+
 # --------------------------------------------------------------------------- SA
 
 def sa_forward(q, k, v, L: int, R: int, scale=None, impl="auto"):
@@ -154,6 +163,7 @@ def sa_forward(q, k, v, L: int, R: int, scale=None, impl="auto"):
 def sa_backward(q, k, v, o, lse, do, L: int, R: int, scale=None, impl="auto", ws=None):
     """SA backward (Eq. 7-13) -> (dq, dk, dv)."""
     _same(q, k, v, o, do)
+    _expect(lse, q.shape[:-1], torch.float32, q.device, "lse")
     d = _desc_from(q, L, R, scale, impl)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     nws = lib().sa_backward_workspace(ctypes.byref(d))
@@ -183,6 +193,8 @@ def sa_backward_p(q, k, v, o, p, do, L: int, R: int, scale=None, impl="auto", ws
     """SA backward from the stored band p of sa_forward_p (no score recompute) -> (dq, dk, dv)."""
     _same(q, k, v, o, do)
     d = _desc_from(q, L, R, scale, impl)
+    ld = int(lib().sa_p_ld(ctypes.byref(d)))
+    _expect(p, tuple(q.shape[:-1]) + (ld,), q.dtype, q.device, "p (the band of sa_forward_p with the same L, R)")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     nws = lib().sa_backward_p_workspace(ctypes.byref(d))
     if ws is None or ws.numel() < nws:
@@ -213,6 +225,10 @@ def llsa_backward(q, k, v, o, lse, do, L: int, R: int, scale=None, impl="auto", 
     """LLSA backward (exact gradient; Eq. 16 for dv) -> dense (dq, dk, dv) [C,B,H,T,D]."""
     _same(q, k, v)
     d = _desc_from(q, L, R, scale, impl, llsa=True, broadcast=broadcast)
+    shp = (R + 1,) + tuple(q.shape[-4:])
+    _expect(o, shp, q.dtype, q.device, "o")
+    _expect(do, shp, q.dtype, q.device, "do")
+    _expect(lse, shp[:-1], torch.float32, q.device, "lse")
     dq = torch.empty_like(o)
     dk = torch.empty_like(o)
     dv = torch.empty_like(o)
@@ -269,8 +285,12 @@ class LLSAStream:
         self._h = h
         self._y = torch.empty((B, H, D), device=self.device, dtype=dtype)
 
+    def _check_x(self, x):
+        _expect(x, (self.B, self.H, self.D), self.dtype, self.device if self.device.index is not None else x.device, "x")
+
     def step(self, x):
         """x [B,H,D] -> (frame index, y [B,H,D]) or None while h < R (y is a fresh tensor)."""
+        self._check_x(x)
         fr = ctypes.c_int64(-1)
         y = torch.empty((self.B, self.H, self.D), device=self.device, dtype=self.dtype)
         _check(lib().llsa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "llsa_stream_step")
@@ -278,6 +298,8 @@ class LLSAStream:
 
     def step_into(self, x, y):
         """Graph-capturable variant: writes into y, returns the emitted frame index (-1 if none)."""
+        self._check_x(x)
+        self._check_x(y)
         fr = ctypes.c_int64(-1)
         _check(lib().llsa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "llsa_stream_step")
         return fr.value
@@ -311,14 +333,19 @@ class SAStream:
         _check(lib().sa_stream_create(ctypes.byref(d), n_layers, ctypes.byref(h)), "sa_stream_create")
         self._h = h
 
+    _check_x = LLSAStream._check_x
+
     def step(self, x):
         """x [B,H,D] -> (frame index, y [B,H,D]) or None while h < n_layers R."""
+        self._check_x(x)
         fr = ctypes.c_int64(-1)
         y = torch.empty((self.B, self.H, self.D), device=self.device, dtype=self.dtype)
         _check(lib().sa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "sa_stream_step")
         return None if fr.value < 0 else (fr.value, y)
 
     def step_into(self, x, y):
+        self._check_x(x)
+        self._check_x(y)
         fr = ctypes.c_int64(-1)
         _check(lib().sa_stream_step(self._h, _ptr(x), _ptr(y), ctypes.byref(fr), _stream()), "sa_stream_step")
         return fr.value

@@ -16,6 +16,7 @@
 #include "ffma_attn.cuh"
 #include "stream_step.cuh"
 #include "tc_dispatch.h"
+#include "host_util.h"
 
 using namespace sattn;
 
@@ -105,11 +106,6 @@ AttnArgs make_args(const sattn_desc* d, bool llsa) {
   return a;
 }
 
-template <class K>
-void set_smem(K kernel, size_t bytes) {
-  // idempotent; cheap enough to call on every launch (not a stream operation)
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-}
 
 sattn_status ffma_forward(const sattn_desc* d, bool llsa, const AttnArgs& a, cudaStream_t st) {
   const int C = llsa ? d->R + 1 : 1;
@@ -212,9 +208,7 @@ size_t attn_bwd_ws(const sattn_desc* d, bool llsa) {
   const size_t C = llsa ? d->R + 1 : 1;
   const size_t Tp = (size_t)((d->T + 3) & ~3LL);
   const size_t rows = (llsa ? 3 : 2) * C * d->B * d->H * Tp * sizeof(float);
-  // SA tensor-core backward: + the fused sweep's CTA hand-off rows (SATTN_SA_BWD=fused)
-  const size_t hand = (!llsa && tc_ok(d, false, true)) ? tc_backward_ws_bytes() : 0;
-  return rows > hand ? rows : hand;
+  return rows;
 }
 
 sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const void* K, const void* V,
@@ -566,6 +560,7 @@ extern "C" {
 sattn_status sa_stream_create(const sattn_desc* d, int n_layers, sattn_stream** out) {
   if (!out) return fail(SATTN_EARG, "out is NULL");
   *out = nullptr;
+  if (!d) return fail(SATTN_EARG, "desc is NULL");
   sattn_desc dd = *d;
   dd.T = 1;
   sattn_status r = validate(&dd);
@@ -609,12 +604,15 @@ sattn_status sa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void
   const long long T = s->n_in, lat = (long long)s->n_layers * s->d.R;
   const size_t frame_b = s->d.B * s->d.H * s->d.D * elem_size(s->d.dtype);
   int cnt = 0;
+  // every step h in [T, T + lat) runs: layers 0..n-2 still compute frames h - (l+1)R for the next
+  // layer's ring even when the last layer has nothing to emit yet (h < lat, a stream shorter
+  // than the stack's latency); only steps with h >= lat write an output frame
   for (long long h = T; h < T + lat; ++h) {
-    if (h - lat < 0) continue;
-    sattn_status r = sa_stream_launch(s, nullptr, static_cast<char*>(y_tail) + cnt * frame_b, h, T - 1,
-                                      (cudaStream_t)stream);
+    const bool emit = h - lat >= 0;
+    sattn_status r = sa_stream_launch(s, nullptr, emit ? static_cast<char*>(y_tail) + cnt * frame_b : nullptr, h,
+                                      T - 1, (cudaStream_t)stream);
     if (r != SATTN_OK) return r;
-    ++cnt;
+    cnt += emit ? 1 : 0;
   }
   if (n_out) *n_out = cnt;
   return SATTN_OK;
@@ -637,6 +635,7 @@ void sa_stream_destroy(sattn_stream* s) {
 sattn_status llsa_stream_create(const sattn_desc* d, int n_layers, sattn_stream** out) {
   if (!out) return fail(SATTN_EARG, "out is NULL");
   *out = nullptr;
+  if (!d) return fail(SATTN_EARG, "desc is NULL");
   sattn_desc dd = *d;
   dd.T = 1;
   sattn_status r = validate(&dd);

@@ -24,6 +24,7 @@
 #include "ffma_attn.cuh"
 #include "tc_dispatch.h"
 #include "tc_ptx.cuh"
+#include "host_util.h"
 
 namespace sattn {
 namespace {
@@ -371,36 +372,12 @@ __global__ void __launch_bounds__(320, 1)
 // ------------------------------------------------------------------------------------------
 // host
 // ------------------------------------------------------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encoder() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
 // [C][BH][T][64] bf16 as a 4-D tensor (64, T, BH, C); box (64, rows, 1, 1); 128B swizzle.
 bool map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) {
-    g_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
   cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)BH, (cuuint64_t)C};
   cuuint64_t strides[3] = {128, (cuuint64_t)T * 128, (cuuint64_t)BH * T * 128};
   cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (r != CUDA_SUCCESS) {
     g_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return false;
@@ -425,15 +402,11 @@ int num_sms() {
 // channel rows) in a single TMA copy.  Coordinates past the frame bounds of the diagonal read
 // neighbouring planes (finite data); the kernel masks those slots (P = 0).
 bool map_skew(CUtensorMap* m, const void* base, int T, int BH, int C, int R, int rows, int nch) {
-  EncodeTiledFn enc = encoder();
-  if (!enc || (long long)BH * T - 1 < (long long)T + R) return false;
+  if ((long long)BH * T - 1 < (long long)T + R) return false;
   cuuint64_t dims[4] = {64, (cuuint64_t)(T + R), (cuuint64_t)C, (cuuint64_t)BH};
   cuuint64_t strides[3] = {128, ((cuuint64_t)BH * T - 1) * 128, (cuuint64_t)T * 128};
   cuuint32_t box[4] = {64, (cuuint32_t)rows, (cuuint32_t)nch, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) == CUDA_SUCCESS;
 }
 
 template <int NB>
@@ -448,7 +421,7 @@ sattn_status launch(const AttnArgs& a, cudaStream_t st) {
     return SATTN_ECUDA;
   // skewed single-box staging of the staircase and of each item's Q rows (dense inputs only:
   // a broadcast plane would need a negative channel stride); falls back to per-channel boxes
-  bool skew = a.in_cs != 0 && !getenv("SATTN_LLSA_NOSKEW");
+  bool skew = a.in_cs != 0;
   if (skew) {
     CUtensorMap sq, sk, sv;
     skew = map_skew(&sq, a.Q, a.T, a.BH, C, a.R, kHT, 4) && map_skew(&sk, a.K, a.T, a.BH, C, a.R, kHT, a.R) &&
@@ -465,7 +438,7 @@ sattn_status launch(const AttnArgs& a, cudaStream_t st) {
   const int nht = (a.T + a.R + kHT - 1) / kHT;
   const int ntiles = nht * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  cudaFuncSetAttribute(llsa_fwd_tc<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
+  set_smem(llsa_fwd_tc<NB>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);

@@ -38,6 +38,7 @@
 #include "llsa_stair.cuh"
 #include "tc_dispatch.h"
 #include "tc_ptx.cuh"
+#include "host_util.h"
 
 namespace sattn {
 namespace {
@@ -59,19 +60,14 @@ struct TcArgs {
   const bf16* Og; const float* LSEin;           // bwd inputs
   bf16* dQ; bf16* dK; bf16* dV; float* delta;    // bwd outputs
   long long* trace;                              // optional per-phase clock64 trace of CTA 0 (debug)
-  int qsplit, ksplit;                            // forward TMA box splits (tuning)
-  int ksplit_pf;                                 // forward L2 prefetch distance (tiles)
-  int mma_sleep;                                 // backward MMA issuers: ns to sleep when nothing is ready
   int kshift;                                    // keys of query t are frames [t-L-kshift, t+R-kshift]
                                                  // (0 for SA; R-c for LLSA channel c's band, with R := 0)
   float* ws_del; float* ws_l2;                   // padded [BH][Tp] delta / LSE*log2e rows (K1 -> K2)
   const float* ws_dx;                            // padded [BH][Tp] rowsum(P o dP) over slots outside the
                                                  // band (LLSA staircase, from the stair pre-pass); null for SA
   int dq_split;                                  // K1: dQ MMA on bf16 dS hi + lo (LLSA, whose dQ is rounded twice)
-  int mma_order;                                 // fused backward: MMA issue priority (tuning)
   int nch;                                       // K1: channels in one launch (LLSA band pass: C; SA: 1)
   int bcast;                                     // K1: Q is one plane read as every channel (LLSA layer 1)
-  float* ws_hand;                                // fused backward: per-CTA dQ hand-off rows [grid][48][64] fp32
   int ldp;                                       // stored-band mode: row stride of P [BH][T][ldp] (bf16)
 };
 
@@ -250,38 +246,22 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      auto prefetch = [&](int k) {  // warm L2 for tile k so its TMA load later is an L2 hit
-        if (k >= ntile_me) return;
-        const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / ntq, t0 = (g % ntq) * kM;
-        tc::tma_prefetch_3d(&tmQ, 0, t0, bh);
-        tc::tma_prefetch_3d(&tmK, 0, t0 - a.L, bh);
-        tc::tma_prefetch_3d(&tmV, 0, t0 - a.L, bh);
-      };
-      const int pfd = a.ksplit_pf;                 // L2 prefetch distance in tiles (0: none)
-      for (int k = NQK; k < NQK + pfd; ++k) prefetch(k);
       for (int k = 0; k < ntile_me; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / ntq, t0 = (g % ntq) * kM;
         const int st = k % NQK;
         if (k >= NQK) tc::mbar_wait(&empty[st], ((k - NQK) / NQK) & 1);
-        if (k >= NQK && pfd) prefetch(k + pfd);
         uint8_t* sQ = qk0 + st * C::QKB;
         trace_at(a.trace, 0, k);
         tc::mbar_expect_tx(&full[st], C::QKB);
-        // boxes may be split into a.qsplit / a.ksplit row blocks (multiples of 8 rows)
-        for (int i = 0; i < a.qsplit; ++i)
-          tc::tma_load_3d(sQ + i * (C::QB / a.qsplit), &tmQ, &full[st], 0, t0 + i * (kM / a.qsplit), bh);
-        for (int i = 0; i < a.ksplit; ++i)
-          tc::tma_load_3d(sQ + C::QB + i * (C::KB / a.ksplit), &tmK, &full[st], 0, t0 - a.L + i * (C::NK / a.ksplit), bh);
+        tc::tma_load_3d(sQ, &tmQ, &full[st], 0, t0, bh);
+        tc::tma_load_3d(sQ + C::QB, &tmK, &full[st], 0, t0 - a.L, bh);
         // V(k) into its own ring: the stage frees when PV(k - NV) completes
         const int sv = k % NV;
         if (k >= NV) tc::mbar_wait(&vempty[sv], ((k - NV) / NV) & 1);
         trace_at(a.trace, 9, k);
         tc::mbar_expect_tx(&vfull[sv], C::KB);
-        for (int i = 0; i < a.ksplit; ++i)
-          tc::tma_load_3d(v0 + sv * C::KB + i * (C::KB / a.ksplit), &tmV, &vfull[sv], 0,
-                          t0 - a.L + i * (C::NK / a.ksplit), bh);
+        tc::tma_load_3d(v0 + sv * C::KB, &tmV, &vfull[sv], 0, t0 - a.L, bh);
       }
     }
   } else if (warp == 1) {
@@ -593,7 +573,6 @@ __global__ void __launch_bounds__(320, 1)
           ++ns;
           continue;
         }
-        if (a.mma_sleep) __nanosleep(a.mma_sleep);   // nothing ready: leave the issue slots to the WGs
       }
     }
   } else {
@@ -924,7 +903,6 @@ __global__ void __launch_bounds__(320, 1)
           ++ns;
           continue;
         }
-        if (a.mma_sleep) __nanosleep(a.mma_sleep);   // nothing ready: leave the issue slots to the WGs
       }
     }
   } else {
@@ -1068,251 +1046,6 @@ __global__ void __launch_bounds__(320, 1)
       }
       }
       if (tr) trace_at(a.trace, 7, k);
-    }
-    if (leader) tc::bulk_wait0();
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 512);
-}
-
-// ------------------------------------------------------------------------------------------
-// backward K2 with M = 64 sub-tiles (SATTN_K2=m64): the 128-key tile of sa_bwd_dkdv_tc as two
-// 64-key halves whose accumulators share TMEM columns.  An M = 64 tcgen05 accumulator uses 16
-// of each TMEM subpartition's 32 lanes; half A (keys u0 .. u0+63) sits at lane offset 0, half
-// B (keys u0+64 ..) at lane offset 16 of the same columns, so a warp's lanes 0-15 / 16-31 hold
-// one row of each half.  A half's query window is 63 + W -> NQH = 16-rounded columns (112 for
-// (32,8)) instead of 176 for the full tile: 36 % less MMA work and TMEM per key, which leaves
-// room for three S/dP buffers (3 x NQH + dV 64 + dK 64 <= 512).
-// ------------------------------------------------------------------------------------------
-template <int CW> struct M64Cfg {
-  static constexpr int NQ = nk_of(CW);                       // the stage's query window (both halves)
-  static constexpr int NQH = ((CW - 32 + 63) + 15) / 16 * 16;   // one half's window: 63 + W, W <= CW - 31
-  static constexpr int CWH = (CW - 16 + 7) / 8 * 8;           // strip of a 16-row group: 16 + W - 1
-  static constexpr int NX = 3;
-  static_assert(64 + NQH <= NQ + 16 && NX * NQH + 128 <= 512, "window / TMEM layout");
-};
-
-template <int CW>
-__global__ void __launch_bounds__(320, 1)
-    sa_bwd_dkdv_m64_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                       const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                       const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
-                       const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel, TcArgs a) {
-  using C = DkvCfg<CW>;
-  using M = M64Cfg<CW>;
-  constexpr int NS = C::NS, NQH = M::NQH, CWH = M::CWH, NX = M::NX;
-  constexpr uint32_t LB = 16u << 16;                 // TMEM lane offset of half B
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage0 = smem;                       // [K | V | Q | dO | LSE | delta]
-  uint8_t* obuf0 = smem + NS * C::STAGE;        // per warpgroup: [dV | dK] staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * C::KB);
-  uint64_t* full = bars;              // [NS]
-  uint64_t* empty = full + NS;        // [NS]
-  uint64_t* sfull = empty + NS;       // [NX]
-  uint64_t* xfree = sfull + NX;       // [NX] (128)
-  uint64_t* dpfull = xfree + NX;      // [NX]
-  uint64_t* pdsfull = dpfull + NX;    // [NX] (128)
-  uint64_t* kvfull = pdsfull + NX;    // [2] (by warpgroup)
-  uint64_t* kvfree = kvfull + 2;      // [2] (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int T = a.T, W = a.L + a.R + 1;
-  const int ntq = (T + kM - 1) / kM;
-  const int ntiles = ntq * a.BH;
-  const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-
-  if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
-    for (int i = 0; i < NX; ++i) {
-      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
-      tc::mbar_init(&pdsfull[i], 128);
-    }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128); }
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tslot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  tc::pdl_wait();
-  tc::pdl_launch_dependents();
-  const uint32_t DV = tbase + NX * NQH, DK = DV + 64;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int k = 0; k < ntile_me; ++k) {
-        const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / ntq, u0 = (g % ntq) * kM;
-        const int st = k % NS;
-        uint8_t* b0 = stage0 + st * C::STAGE;
-        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
-        tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB + 2 * C::NQP * 4);
-        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - a.R, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - a.R, bh);
-        const int na = (u0 - a.R) & ~3;
-        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB, &tmL2, &full[st], na, bh, 0);
-        tc::tma_load_3d(b0 + 2 * C::KB + 2 * C::QB + C::NQP * 4, &tmDel, &full[st], na, bh, 0);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idS = tc::idesc_bf16(64, NQH, 0, 0);
-      constexpr uint32_t idG = tc::idesc_bf16(64, kD, 0, 1);
-      constexpr uint32_t H64 = 64 * 128;            // 64 rows of a 128-byte-row smem tile (8 swizzle atoms)
-      int ns = 0, ndp = 0, nkv = 0;
-      while (nkv < ntile_me) {
-        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv % NX]), (nkv / NX) & 1,
-                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
-                                          tc::smem_u32(&xfree[ndp % NX]), (ndp / NX) & 1,
-                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
-        if (nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
-          tc::tc_fence_after();
-          const int st = nkv % NS;
-          const uint32_t x = tbase + (nkv % NX) * NQH;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t q = base + 2 * C::KB, dO = q + C::QB;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {                // half A (lanes 0-15), half B (lanes 16-31)
-            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
-#pragma unroll
-            for (int j = 0; j < NQH / 16; ++j)
-              tc::mma_bf16_ts(DV | lo, (x + 8 * j) | lo, tc::desc_mnmajor_sw128(dO + roff + 2048 * j), idG, j > 0);
-#pragma unroll
-            for (int j = 0; j < NQH / 16; ++j)
-              tc::mma_bf16_ts(DK | lo, (x + NQH / 2 + 8 * j) | lo, tc::desc_mnmajor_sw128(q + roff + 2048 * j), idG,
-                              j > 0);
-          }
-          tc::mma_commit(&kvfull[nkv & 1]);
-          tc::mma_commit(&empty[st]);
-          ++nkv;
-          continue;
-        }
-        if (ndp < ns && (m & 4)) {
-          tc::tc_fence_after();
-          const int st = ndp % NS;
-          const uint32_t x = tbase + (ndp % NX) * NQH;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
-#pragma unroll
-            for (int j = 0; j < kD / 16; ++j)
-              tc::mma_bf16(x | lo, tc::desc_kmajor_sw128(v + roff + 32 * j), tc::desc_kmajor_sw128(dO + roff + 32 * j),
-                           idS, j > 0);
-          }
-          tc::mma_commit(&dpfull[ndp % NX]);
-          ++ndp;
-          continue;
-        }
-        if (ns < ntile_me && ns < nkv + NX && (m & 8)) {
-          tc::tc_fence_after();
-          const uint32_t x = tbase + (ns % NX) * NQH;
-          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
-          const uint32_t kk = base, q = base + 2 * C::KB;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t lo = h ? LB : 0u, roff = h ? H64 : 0u;
-#pragma unroll
-            for (int j = 0; j < kD / 16; ++j)
-              tc::mma_bf16(x | lo, tc::desc_kmajor_sw128(kk + roff + 32 * j), tc::desc_kmajor_sw128(q + roff + 32 * j),
-                           idS, j > 0);
-          }
-          tc::mma_commit(&sfull[ns % NX]);
-          ++ns;
-        }
-      }
-    }
-  } else {
-    const int wg = (warp - 2) >> 2;
-    const int q4 = warp & 3;
-    const int hb = lane >> 4, rr = 16 * q4 + (lane & 15);   // half, row within the half
-    const int r = 64 * hb + rr;                               // key row within the 128-key tile
-    const int l16 = lane & 15;
-    const uint32_t lanes = uint32_t(32 * q4) << 16;
-    const bool leader = q4 == 2 && lane == 0;
-    uint8_t* ostage = obuf0 + wg * 2 * C::KB;
-    for (int k = wg; k < ntile_me; k += 2) {
-      const int g = blockIdx.x + k * gridDim.x;
-      const int bh = g / ntq, u0 = (g % ntq) * kM;
-      const int xb = k % NX, use = k / NX, st = k % NS;
-      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
-      // this half's window starts 64 query rows into the stage window for half B
-      const float* sL2 = reinterpret_cast<const float*>(stage0 + st * C::STAGE + 2 * C::KB + 2 * C::QB) + sh + 64 * hb;
-      const float* sDel = sL2 + C::NQP;
-      tc::mbar_wait(&full[st], (k / NS) & 1);
-      const uint32_t x = tbase + lanes + xb * NQH;
-      const int c0 = 16 * q4;
-      tc::mbar_wait(&sfull[xb], use & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      float p[CWH];
-#pragma unroll
-      for (int j = 0; j < CWH / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < CWH; ++i)
-        p[i] = (i >= l16 && i < l16 + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
-      tc::tc_fence_before();
-      tc::mbar_arrive(&xfree[xb]);
-      tc::mbar_wait(&dpfull[xb], use & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      float ds[CWH];
-#pragma unroll
-      for (int j = 0; j < CWH / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
-      }
-      // packed P^T (columns [0, NQH/2)) and dS^T ([NQH/2, NQH)) of this row: the strip at packed
-      // column 8 q4, zeros elsewhere
-      {
-        const int pc0 = 8 * q4;
-#pragma unroll
-        for (int j = 0; j < CWH / 8; ++j) {
-          tc::tmem_st4(x + pc0 + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
-                       pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
-          tc::tmem_st4(x + NQH / 2 + pc0 + 4 * j, pack_bf16(ds[8 * j], ds[8 * j + 1]),
-                       pack_bf16(ds[8 * j + 2], ds[8 * j + 3]), pack_bf16(ds[8 * j + 4], ds[8 * j + 5]),
-                       pack_bf16(ds[8 * j + 6], ds[8 * j + 7]));
-        }
-        for (int c = 0; c < NQH / 2; c += 4)
-          if (c < pc0 || c >= pc0 + CWH / 2) {
-            tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
-            tc::tmem_st4(x + NQH / 2 + c, 0u, 0u, 0u, 0u);
-          }
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&pdsfull[xb]);
-      // dV / dK rows (row r of the 128-key tile)
-      tc::mbar_wait(&kvfull[k & 1], (k >> 1) & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      if (leader) tc::bulk_wait_read0();
-      tc::named_bar(1 + wg, 128);
-      tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
-      tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
-      tc::tc_fence_before();
-      tc::mbar_arrive(&kvfree[k & 1]);
-      tc::fence_proxy_async_smem();
-      tc::named_bar(1 + wg, 128);
-      if (leader) {
-        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
-        tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
-        tc::bulk_commit();
-      }
     }
     if (leader) tc::bulk_wait0();
   }
@@ -1768,305 +1501,6 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// backward K2, block ring + M = 64 halves (SATTN_K2=rm64): the query window as 128-row blocks
-// shared by consecutive tiles of a contiguous sweep (3-slot ring, loads well ahead), K and V
-// through one 3-slot ring in load order K(0) V(0) K(1) V(1) ... (K freed by S, V by dP), the
-// 128-key tile as two M = 64 halves at TMEM lane offsets 0 / 16 (three S/dP buffers), and the
-// two-tile [dV | dK] staging per warpgroup of the original K2.
-// ------------------------------------------------------------------------------------------
-template <int CW> struct RM64Cfg {
-  static constexpr int NQ = nk_of(CW);
-  static constexpr int NQH = ((CW - 32 + 63) + 15) / 16 * 16;   // a half's window
-  static constexpr int NB2 = NQH > 64 ? NQH - 64 : 0;           // half B rows taken from the second block
-  static constexpr int NB = NB2 > 0 ? 2 : 1;
-  static constexpr int CWH = (CW - 16 + 7) / 8 * 8;
-  static constexpr int NX = 3;
-  static constexpr int KB = kM * 128;
-  static constexpr int BLK = 2 * KB;                             // [Q block | dO block]
-  static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
-  static constexpr int RW = 2 * NQP * 4;
-  static constexpr int SMEM = 1024 + 3 * BLK + 3 * KB + 4 * KB + 2 * RW + 512;
-  static constexpr int THREADS = 320;
-  static_assert(SMEM <= 232448 && NX * NQH + 128 <= 512 && NQH <= 128, "smem / TMEM layout");
-};
-
-template <int CW>
-__global__ void __launch_bounds__(320, 1)
-    sa_bwd_dkdv_rm64_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                        const __grid_constant__ CUtensorMap tmdK, const __grid_constant__ CUtensorMap tmdV,
-                        const __grid_constant__ CUtensorMap tmL2, const __grid_constant__ CUtensorMap tmDel,
-                        TcArgs a) {
-  using C = RM64Cfg<CW>;
-  constexpr int NQH = C::NQH, NB2 = C::NB2, NB = C::NB, CWH = C::CWH, NX = C::NX;
-  constexpr uint32_t LB = 16u << 16;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* blk0 = smem;                             // [Q | dO] x 3 block slots
-  uint8_t* kv0 = blk0 + 3 * C::BLK;                 // K / V x 3 (load order K0 V0 K1 V1 ...)
-  uint8_t* obuf0 = kv0 + 3 * C::KB;                 // per warpgroup [dV | dK]
-  uint8_t* rw0 = obuf0 + 4 * C::KB;                 // LSE / delta windows x 2
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rw0 + 2 * C::RW);
-  uint64_t* bfull = bars;             // [3]
-  uint64_t* bempty = bfull + 3;       // [3]
-  uint64_t* kvf = bempty + 3;         // [3] K/V slot landed
-  uint64_t* kve = kvf + 3;            // [3] K/V slot free
-  uint64_t* rfull = kve + 3;          // [2]
-  uint64_t* rempty = rfull + 2;       // [2] (128)
-  uint64_t* sfull = rempty + 2;       // [NX]
-  uint64_t* xfree = sfull + NX;       // [NX] (128)
-  uint64_t* dpfull = xfree + NX;      // [NX]
-  uint64_t* pdsfull = dpfull + NX;    // [NX] (128)
-  uint64_t* kvfull = pdsfull + NX;    // [2] by warpgroup
-  uint64_t* kvfree = kvfull + 2;      // [2] (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(kvfree + 2);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int T = a.T, W = a.L + a.R + 1;
-  const int ntq = (T + kM - 1) / kM;
-  const int ntiles = ntq * a.BH;
-  const int G = gridDim.x;
-  const int g_begin = (int)((long long)blockIdx.x * ntiles / G);
-  const int ntile_me = (int)((long long)(blockIdx.x + 1) * ntiles / G) - g_begin;
-
-  if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
-    for (int i = 0; i < 3; ++i) {
-      tc::mbar_init(&bfull[i], 1); tc::mbar_init(&bempty[i], 1);
-      tc::mbar_init(&kvf[i], 1); tc::mbar_init(&kve[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&rfull[i], 1); tc::mbar_init(&rempty[i], 128);
-      tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
-    }
-    for (int i = 0; i < NX; ++i) {
-      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
-      tc::mbar_init(&pdsfull[i], 128);
-    }
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tslot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  tc::pdl_wait();
-  tc::pdl_launch_dependents();
-  const uint32_t DV = tbase + NX * NQH, DK = DV + 64;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      BlkSeq sq;
-      sq.init();
-      auto kv_load = [&](int item, const CUtensorMap* map, int u0, int bh) {   // item 2k = K(k), 2k+1 = V(k)
-        const int sl = item % 3;
-        if (item >= 3) tc::mbar_wait(&kve[sl], ((item / 3) - 1) & 1);
-        tc::mbar_expect_tx(&kvf[sl], C::KB);
-        tc::tma_load_3d(kv0 + sl * C::KB, map, &kvf[sl], 0, u0, bh);
-      };
-      for (int k = 0; k < ntile_me; ++k) {
-        const int g = g_begin + k;
-        const int bh = g / ntq, kt = g % ntq, u0 = kt * kM;
-        int f, s2, nl0, nl1;
-        sq.next(g, ntq, NB, f, s2, nl0, nl1);
-        for (int n = nl0; n < nl1; ++n) {
-          const int sl = n % 3;
-          if (n >= 3) tc::mbar_wait(&bempty[sl], ((n / 3) - 1) & 1);
-          const int b = (n == f) ? kt : kt + 1;
-          uint8_t* d = blk0 + sl * C::BLK;
-          tc::mbar_expect_tx(&bfull[sl], C::BLK);
-          tc::tma_load_3d(d, &tmQ, &bfull[sl], 0, b * kM - a.R, bh);
-          tc::tma_load_3d(d + C::KB, &tmdO, &bfull[sl], 0, b * kM - a.R, bh);
-        }
-        kv_load(2 * k, &tmK, u0, bh);
-        kv_load(2 * k + 1, &tmV, u0, bh);
-        const int s = k & 1;
-        if (k >= 2) tc::mbar_wait(&rempty[s], ((k - 2) >> 1) & 1);
-        const int na = (u0 - a.R) & ~3;
-        tc::mbar_expect_tx(&rfull[s], C::RW);
-        tc::tma_load_3d(rw0 + s * C::RW, &tmL2, &rfull[s], na, bh, 0);
-        tc::tma_load_3d(rw0 + s * C::RW + C::NQP * 4, &tmDel, &rfull[s], na, bh, 0);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idA = tc::idesc_bf16(64, NQH, 0, 0);              // half A: one block
-      constexpr uint32_t idB1 = tc::idesc_bf16(64, NB2 > 0 ? 64 : NQH, 0, 0);   // half B: rows 64.. of block f
-      constexpr uint32_t idB2 = tc::idesc_bf16(64, NB2 > 0 ? NB2 : 16, 0, 0);   // ... and rows 0.. of block s
-      constexpr uint32_t idG = tc::idesc_bf16(64, kD, 0, 1);
-      constexpr uint32_t H64 = 64 * 128;
-      BlkSeq qs, qd, qk;
-      qs.init(); qd.init(); qk.init();
-      int sf = 0, ss = 0, df = 0, ds2 = 0, kf = 0, ks2 = 0, krel2 = 0;
-      int ns = 0, ndp = 0, nkv = 0;
-      auto blk = [&](int n) { return tc::smem_u32(blk0 + (n % 3) * C::BLK); };
-      auto kvs = [&](int item) { return tc::smem_u32(kv0 + (item % 3) * C::KB); };
-      bool s_ready = false, d_ready = false, k_ready = false;
-      // S^T or dP^T of both halves: A rows (K or V) 0..63 / 64..127, B = the half's query window
-      auto sdp = [&](uint32_t x, uint32_t arows, uint32_t bf, uint32_t bs, uint32_t boff) {
-#pragma unroll
-        for (int j = 0; j < kD / 16; ++j) {
-          tc::mma_bf16(x, tc::desc_kmajor_sw128(arows + 32 * j), tc::desc_kmajor_sw128(bf + boff + 32 * j), idA, j > 0);
-          tc::mma_bf16(x | LB, tc::desc_kmajor_sw128(arows + H64 + 32 * j),
-                       tc::desc_kmajor_sw128(bf + boff + H64 + 32 * j), idB1, j > 0);
-          if (NB2 > 0)
-            tc::mma_bf16((x + 64) | LB, tc::desc_kmajor_sw128(arows + H64 + 32 * j),
-                         tc::desc_kmajor_sw128(bs + boff + 32 * j), idB2, j > 0);
-        }
-      };
-      while (nkv < ntile_me) {
-        if (!s_ready && ns < ntile_me) { int a0, a1; qs.next(g_begin + ns, ntq, NB, sf, ss, a0, a1); s_ready = true; }
-        if (!d_ready && ndp < ns) { int a0, a1; qd.next(g_begin + ndp, ntq, NB, df, ds2, a0, a1); d_ready = true; }
-        if (!k_ready && nkv < ndp) {
-          int a0, a1; qk.next(g_begin + nkv, ntq, NB, kf, ks2, a0, a1);
-          const int g = g_begin + nkv, gn = g + 1;
-          krel2 = (NB == 2) && !(nkv + 1 < ntile_me && gn / ntq == g / ntq && gn % ntq == g % ntq + 1);
-          k_ready = true;
-        }
-        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv % NX]), (nkv / NX) & 1,
-                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
-                                          tc::smem_u32(&xfree[ndp % NX]), (ndp / NX) & 1,
-                                          tc::smem_u32(&kvf[(2 * ns) % 3]), ((2 * ns) / 3) & 1);
-        if (k_ready && nkv < ndp && (m & 1) && (nkv < 1 || (m & 2))) {
-          tc::tc_fence_after();
-          const uint32_t x = tbase + (nkv % NX) * NQH;
-          const uint32_t bf = blk(kf), bs = NB == 2 ? blk(ks2) : bf;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t lo = h ? LB : 0u;
-#pragma unroll
-            for (int j = 0; j < NQH / 16; ++j) {   // K-step j: window rows 64 h + 16 j
-              const int row = 64 * h + 16 * j;
-              const uint32_t bb = row < kM ? bf + 128 * row : bs + 128 * (row - kM);
-              tc::mma_bf16_ts(DV | lo, (x + 8 * j) | lo, tc::desc_mnmajor_sw128(bb + C::KB), idG, j > 0);
-            }
-#pragma unroll
-            for (int j = 0; j < NQH / 16; ++j) {
-              const int row = 64 * h + 16 * j;
-              const uint32_t bb = row < kM ? bf + 128 * row : bs + 128 * (row - kM);
-              tc::mma_bf16_ts(DK | lo, (x + NQH / 2 + 8 * j) | lo, tc::desc_mnmajor_sw128(bb), idG, j > 0);
-            }
-          }
-          tc::mma_commit(&kvfull[nkv & 1]);
-          tc::mma_commit(&bempty[kf % 3]);
-          if (krel2) tc::mma_commit(&bempty[ks2 % 3]);
-          ++nkv;
-          k_ready = false;
-          continue;
-        }
-        if (d_ready && ndp < ns && (m & 4) &&
-            tc::mbar_test(tc::smem_u32(&kvf[(2 * ndp + 1) % 3]), ((2 * ndp + 1) / 3) & 1)) {
-          tc::tc_fence_after();
-          const uint32_t x = tbase + (ndp % NX) * NQH;
-          sdp(x, kvs(2 * ndp + 1), blk(df), NB == 2 ? blk(ds2) : blk(df), C::KB);
-          tc::mma_commit(&dpfull[ndp % NX]);
-          tc::mma_commit(&kve[(2 * ndp + 1) % 3]);
-          ++ndp;
-          d_ready = false;
-          continue;
-        }
-        if (s_ready && ns < ntile_me && ns < nkv + NX && (m & 8) &&
-            tc::mbar_test(tc::smem_u32(&bfull[sf % 3]), (sf / 3) & 1) &&
-            (NB == 1 || tc::mbar_test(tc::smem_u32(&bfull[ss % 3]), (ss / 3) & 1))) {
-          tc::tc_fence_after();
-          const uint32_t x = tbase + (ns % NX) * NQH;
-          sdp(x, kvs(2 * ns), blk(sf), NB == 2 ? blk(ss) : blk(sf), 0);
-          tc::mma_commit(&sfull[ns % NX]);
-          tc::mma_commit(&kve[(2 * ns) % 3]);
-          ++ns;
-          s_ready = false;
-        }
-      }
-    }
-  } else {
-    const int wg = (warp - 2) >> 2;
-    const int q4 = warp & 3;
-    const int hb = lane >> 4, rr = 16 * q4 + (lane & 15);
-    const int r = 64 * hb + rr;
-    const int l16 = lane & 15;
-    const uint32_t lanes = uint32_t(32 * q4) << 16;
-    const bool leader = q4 == 2 && lane == 0;
-    uint8_t* ostage = obuf0 + wg * 2 * C::KB;
-    for (int k = wg; k < ntile_me; k += 2) {
-      const int g = g_begin + k;
-      const int bh = g / ntq, u0 = (g % ntq) * kM;
-      const int xb = k % NX, use = k / NX, s = k & 1;
-      const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);
-      const float* sL2 = reinterpret_cast<const float*>(rw0 + s * C::RW) + sh + 64 * hb;
-      const float* sDel = sL2 + C::NQP;
-      tc::mbar_wait(&rfull[s], (k >> 1) & 1);
-      const uint32_t x = tbase + lanes + xb * NQH;
-      const int c0 = 16 * q4;
-      tc::mbar_wait(&sfull[xb], use & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      float p[CWH];
-#pragma unroll
-      for (int j = 0; j < CWH / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < CWH; ++i)
-        p[i] = (i >= l16 && i < l16 + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
-      tc::tc_fence_before();
-      tc::mbar_arrive(&xfree[xb]);
-      tc::mbar_wait(&dpfull[xb], use & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      float ds[CWH];
-#pragma unroll
-      for (int j = 0; j < CWH / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
-      }
-      tc::mbar_arrive(&rempty[s]);
-      {
-        const int pc0 = 8 * q4;
-#pragma unroll
-        for (int j = 0; j < CWH / 8; ++j) {
-          tc::tmem_st4(x + pc0 + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
-                       pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
-          tc::tmem_st4(x + NQH / 2 + pc0 + 4 * j, pack_bf16(ds[8 * j], ds[8 * j + 1]),
-                       pack_bf16(ds[8 * j + 2], ds[8 * j + 3]), pack_bf16(ds[8 * j + 4], ds[8 * j + 5]),
-                       pack_bf16(ds[8 * j + 6], ds[8 * j + 7]));
-        }
-        for (int c = 0; c < NQH / 2; c += 4)
-          if (c < pc0 || c >= pc0 + CWH / 2) {
-            tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
-            tc::tmem_st4(x + NQH / 2 + c, 0u, 0u, 0u, 0u);
-          }
-      }
-      tc::tmem_st_wait();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&pdsfull[xb]);
-      tc::mbar_wait(&kvfull[k & 1], (k >> 1) & 1);
-      __syncwarp();
-      tc::tc_fence_after();
-      if (leader) tc::bulk_wait_read0();
-      tc::named_bar(1 + wg, 128);
-      tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
-      tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
-      tc::tc_fence_before();
-      tc::mbar_arrive(&kvfree[k & 1]);
-      tc::fence_proxy_async_smem();
-      tc::named_bar(1 + wg, 128);
-      if (leader) {
-        tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
-        tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
-        tc::bulk_commit();
-      }
-    }
-    if (leader) tc::bulk_wait0();
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 512);
-}
-
-// ------------------------------------------------------------------------------------------
 // LLSA backward, band keys (channel R), key-major: for a tile of 128 channel-R keys u, every
 // query channel c = 0..R contributes through the band: query (t, c) sees (u, R) iff
 // u in [t + c - R - L, t + c - R]  <=>  t in [u + s_c, u + s_c + L],  s_c = R - c
@@ -2308,458 +1742,20 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
 }
 
-// ------------------------------------------------------------------------------------------
-// backward, fused single pass (SA): one key-major sweep per CTA over a contiguous range of key
-// tiles (head-major, time-minor), so each dQ row is finished inside the sweep instead of by a
-// second, query-major kernel (1028 B per head-frame instead of K1 + K2's 1424).
-// Per key tile (128 keys u0.., query window n0 = u0 - R .. n0 + NQ):
-//   WG   LSE*log2e and delta_n = dO_n . O_n of the NQ window rows (Eq. 9's <g, p> term)
-//   MMA  S^T = K Q^T -> X_b                  WG  P^T = exp2(S^T*sl2 - LSE_n*log2e)
-//   MMA  dP^T = V dO^T -> X_b                WG  dS^T = P^T (dP^T - delta_n); P^T, dS^T -> X_b
-//                                                (packed bf16, TMEM A operands) and dS^T -> smem
-//   MMA  dV = P^T dO, dK = dS^T Q            WG  rows -> global
-//   MMA  dQ0 = dS[queries 0..127] K  -> X_b[0, 64)      (A = dS^T read MN-major from smem)
-//        dQ1 = dS[queries 128..255] K -> X_b[64, 128)   (only keys >= 128 - W + 1 reach them)
-//                                            WG  dQ rows 0..W-2 of a tile also receive the previous
-//                                                key tile's dQ1 (the "carry", in smem) -> global
-// The dS^T buffer holds the window's query columns as three 64-column chunks in the order
-// [c2 | c0 | c1] (16 KB each, 128 key rows, 128B swizzle).  dQ0 reads c0, c1 (LBO = 16 KB); dQ1
-// reads c2 and then "c3" = c2 + 16 KB = c0, whose key rows >= 64 are never written (every row's
-// band starts at its own key, so rows >= 64 only reach columns >= 64): zeros, as the padded
-// query rows 192..255 must be.  A CTA's first tile (if not a head start) and last tile (if not a
-// head end) meet the neighbouring CTA's tiles: the first tile's dQ0 rows 0..W-2 go to a per-CTA
-// workspace slot, a grid-wide barrier (cooperative launch) orders them, and the CTA owning the
-// previous key tile adds them to its dQ1 carry.  fp32 a + b == b + a, so the result is bitwise
-// independent of where the CTA ranges fall (time-sharded == unsharded, G18).
-// ------------------------------------------------------------------------------------------
-template <int CW> struct FusCfg {
-  static constexpr int NQ = nk_of(CW);
-  static constexpr int KB = kM * 128;
-  static constexpr int QB = NQ * 128;
-  static constexpr int STAGE = 2 * KB + 2 * QB;   // [K | V | Q | dO]
-  static constexpr int NS = 2;
-  static constexpr int DSB = 3 * 16384;           // dS^T chunks [c2 | c0 | c1]
-  static constexpr int NCR = 48;                  // carry rows (W - 1)
-  static constexpr int CARRY = NCR * 256;
-  static constexpr int NQA = 192;
-  static constexpr int ROWS = NS * 2 * NQA * 4;   // per stage: LSE*log2e [NQA], delta [NQA]
-  static constexpr int SMEM = 1024 + NS * STAGE + DSB + CARRY + ROWS + 512;
-  static constexpr int THREADS = 384;            // TMA, MMA, 2 x 4 WG warps, 2 row warps
-};
-
-// carry row r (64 fp32) in smem, float4 s stored at slot s ^ (r & 15) (conflict-free row-per-thread)
-__device__ __forceinline__ float4* carry_at(float* carry, int r, int s) {
-  return reinterpret_cast<float4*>(carry + r * 64) + (s ^ (r & 15));
-}
-
-template <int CW>
-__global__ void __launch_bounds__(384, 1)
-    sa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                    const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ CUtensorMap tmO, TcArgs a) {
-  using C = FusCfg<CW>;
-  constexpr int NQ = C::NQ, NS = C::NS;
-  static_assert(NQ + 64 <= 256 && NQ >= 128 && 96 + CW <= NQ, "TMEM / window layout");
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage0 = smem;                                   // [K | V | Q | dO] x NS
-  uint8_t* dsb = smem + NS * C::STAGE;                      // dS^T [c2 | c0 | c1]
-  float* carry = reinterpret_cast<float*>(dsb + C::DSB);    // dQ1 rows of the previous tile
-  float* rows = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(carry) + C::CARRY);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(rows) + C::ROWS);
-  uint64_t* full = bars;              // [NS]
-  uint64_t* empty = full + NS;        // [NS]
-  uint64_t* sfull = empty + NS;       // [2]
-  uint64_t* xfree = sfull + 2;        // [2] (128)
-  uint64_t* dpfull = xfree + 2;       // [2]
-  uint64_t* pdsfull = dpfull + 2;     // [2] (128)
-  uint64_t* kvfull = pdsfull + 2;     // [2]
-  uint64_t* kvfree = kvfull + 2;      // [2] (128)
-  uint64_t* dqfull = kvfree + 2;      // [2]
-  uint64_t* tfree = dqfull + 2;       // [2] (128) X_b drained (dQ read)
-  uint64_t* dsfree = tfree + 2;       // [2] dQ MMAs of tile k done (by tile parity): smem dS^T reusable
-  uint64_t* cfull = dsfree + 2;       // [1] (128) tile k's dQ epilogue done (carry written), tiles in order
-  uint64_t* rfull = cfull + 1;        // [NS] (64) LSE / delta rows of the stage's tile written
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(rfull + NS);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int T = a.T, R = a.R, W = a.L + a.R + 1;
-  const int nc = W - 1;                                     // carry rows
-  const int ntq = (T + kM - 1) / kM;
-  const int ntiles = ntq * a.BH;
-  const int G = gridDim.x;
-  const int g_begin = (int)((long long)blockIdx.x * ntiles / G);
-  const int g_end = (int)((long long)(blockIdx.x + 1) * ntiles / G);
-  const int ntile_me = g_end - g_begin;
-  trace_cta(a.trace, 0);
-
-  // dS^T buffer starts (and, outside the rows' band strips, stays) zero
-  for (int i = tid; i < C::DSB / 16; i += blockDim.x) tc::st_shared_v4(tc::smem_u32(dsb) + 16 * i, make_uint4(0, 0, 0, 0));
-  tc::fence_proxy_async_smem();
-  if (tid == 0) {
-    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
-    tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmO);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
-      tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
-      tc::mbar_init(&dqfull[i], 1); tc::mbar_init(&tfree[i], 128);
-    }
-    tc::mbar_init(&dsfree[0], 1); tc::mbar_init(&dsfree[1], 1);
-    tc::mbar_init(cfull, 128);
-    for (int i = 0; i < NS; ++i) tc::mbar_init(&rfull[i], 64);
-    tc::fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tslot, 512);
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  tc::pdl_wait();
-  tc::pdl_launch_dependents();
-  const uint32_t DV = tbase + NQ, DK = tbase + 256 + NQ;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int k = 0; k < ntile_me; ++k) {
-        const int g = g_begin + k;
-        const int bh = g / ntq, u0 = (g % ntq) * kM;
-        const int st = k % NS;
-        uint8_t* b0 = stage0 + st * C::STAGE;
-        if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
-        trace_at(a.trace, 0, k);
-        tc::mbar_expect_tx(&full[st], C::STAGE);
-        tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + C::KB, &tmV, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB, &tmQ, &full[st], 0, u0 - R, bh);
-        tc::tma_load_3d(b0 + 2 * C::KB + C::QB, &tmdO, &full[st], 0, u0 - R, bh);
-        // warm L2 for tile k + NS (its stage is only free once tile k's dQ MMAs are done; the O rows
-        // are read by the row warps with plain loads)
-        if (a.qsplit && k + NS < ntile_me) {
-          const int g2 = g + NS, bh2 = g2 / ntq, v0 = (g2 % ntq) * kM;
-          tc::tma_prefetch_3d(&tmK, 0, v0, bh2);
-          tc::tma_prefetch_3d(&tmV, 0, v0, bh2);
-          tc::tma_prefetch_3d(&tmQ, 0, v0 - R, bh2);
-          tc::tma_prefetch_3d(&tmdO, 0, v0 - R, bh2);
-          tc::tma_prefetch_3d(&tmO, 0, v0 - R, bh2);
-        }
-        if (k == 0) tc::tma_prefetch_3d(&tmO, 0, u0 - R, bh);
-        if (k == 1 || (k == 0 && ntile_me > 1)) {
-          const int g1 = g_begin + 1, bh1 = g1 / ntq, v1 = (g1 % ntq) * kM;
-          if (k == 0) tc::tma_prefetch_3d(&tmO, 0, v1 - R, bh1);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idS = tc::idesc_bf16(kM, NQ, 0, 0);
-      constexpr uint32_t idG = tc::idesc_bf16(kM, kD, 0, 1);
-      constexpr uint32_t idQ = tc::idesc_bf16(kM, kD, 1, 1);
-      const int ks1 = (kM - W + 1) / 16;                    // first 16-key step that reaches window rows >= 128
-      const uint32_t dsc2 = tc::smem_u32(dsb), dsc0 = dsc2 + 16384;
-      int ns = 0, ndp = 0, nkv = 0;
-      while (nkv < ntile_me) {
-        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
-                                          tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
-                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
-                                          tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
-        const bool kv_ok = nkv < ndp && (m & 1) && (nkv < 1 || (m & 2));
-        const bool dp_ok = ndp < ns && (m & 4);
-        const bool s_ok = ns < ntile_me && (m & 8) &&
-                          (ns < 2 || tc::mbar_test(tc::smem_u32(&tfree[ns & 1]), ((ns - 2) >> 1) & 1));
-        // issue priority (a.mma_order): 0 = kv/dQ > dP > S, 1 = dP > S > kv/dQ, 2 = dP > kv/dQ > S
-        int pick = -1;
-        if (a.mma_order == 0) pick = kv_ok ? 0 : dp_ok ? 1 : s_ok ? 2 : -1;
-        else if (a.mma_order == 1) pick = dp_ok ? 1 : s_ok ? 2 : kv_ok ? 0 : -1;
-        else pick = dp_ok ? 1 : kv_ok ? 0 : s_ok ? 2 : -1;
-        if (pick == 0) {
-          tc::tc_fence_after();
-          const int b = nkv & 1, st = nkv % NS;
-          const uint32_t x = tbase + b * 256;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t kk = base, q = base + 2 * C::KB, dO = q + C::QB;
-#pragma unroll
-          for (int j = 0; j < NQ / 16; ++j)
-            tc::mma_bf16_ts(DV, x + 8 * j, tc::desc_mnmajor_sw128(dO + 2048 * j), idG, j > 0);
-#pragma unroll
-          for (int j = 0; j < NQ / 16; ++j)
-            tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
-          tc::mma_commit(&kvfull[b]);
-          // dQ0 / dQ1 over X_b's first 128 columns (P^T / dS^T there were read by the MMAs above)
-#pragma unroll
-          for (int j = 0; j < kM / 16; ++j)
-            tc::mma_bf16(x, tc::sdesc(dsc0 + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(kk + 2048 * j), idQ,
-                         j > 0);
-          for (int j = ks1; j < kM / 16; ++j)
-            tc::mma_bf16(x + 64, tc::sdesc(dsc2 + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(kk + 2048 * j),
-                         idQ, j > ks1);
-          tc::mma_commit(&dqfull[b]);
-          tc::mma_commit(&dsfree[b]);
-          tc::mma_commit(&empty[st]);
-          ++nkv;
-        } else if (pick == 1) {
-          tc::tc_fence_after();
-          const int b = ndp & 1, st = ndp % NS;
-          const uint32_t base = tc::smem_u32(stage0 + st * C::STAGE);
-          const uint32_t v = base + C::KB, dO = base + 2 * C::KB + C::QB;
-#pragma unroll
-          for (int j = 0; j < kD / 16; ++j)
-            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
-                         j > 0);
-          tc::mma_commit(&dpfull[b]);
-          ++ndp;
-        } else if (pick == 2) {
-          tc::tc_fence_after();
-          const int b = ns & 1;
-          const uint32_t base = tc::smem_u32(stage0 + (ns % NS) * C::STAGE);
-          const uint32_t kk = base, q = base + 2 * C::KB;
-#pragma unroll
-          for (int j = 0; j < kD / 16; ++j)
-            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
-                         j > 0);
-          tc::mma_commit(&sfull[b]);
-          ++ns;
-        }
-      }
-    }
-  } else if (warp < 10) {
-    const int wg = (warp - 2) >> 2;
-    const int q4 = warp & 3;
-    const int r = 32 * q4 + lane;
-    const uint32_t lanes = uint32_t(32 * q4) << 16;
-    const int c0 = 32 * q4;
-    const uint32_t dsu = tc::smem_u32(dsb);
-    for (int k = wg; k < ntile_me; k += 2) {
-      const int g = g_begin + k;
-      const int bh = g / ntq, kt = g % ntq, u0 = kt * kM;
-      const int n0 = u0 - R;                         // frame of window row 0
-      const int b = wg, use = k >> 1, st = k % NS;
-      const bool tr = (tid == 64) || (tid == 192);
-      const float* lse2_s = rows + st * 2 * C::NQA;
-      const float* del_s = lse2_s + C::NQA;
-      tc::mbar_wait(&rfull[st], (k / NS) & 1);       // LSE / delta of the window rows (row warps)
-      if (tr) trace_at(a.trace, 1, k);
-      const uint32_t x = tbase + lanes + b * 256;
-      tc::mbar_wait(&sfull[b], use & 1);
-      if (tr) trace_at(a.trace, 2, k);
-      __syncwarp();
-      tc::tc_fence_after();
-      float p[CW];
-#pragma unroll
-      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
-      tc::tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < CW; ++i)
-        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -lse2_s[c0 + i])) : 0.f;
-      tc::tc_fence_before();
-      tc::mbar_arrive(&xfree[b]);
-      tc::mbar_wait(&dpfull[b], use & 1);
-      if (tr) trace_at(a.trace, 3, k);
-      __syncwarp();
-      tc::tc_fence_after();
-      float ds[CW];
-#pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - del_s[c0 + 8 * j + e]);
-      }
-      tmem_write_row<CW, NQ>(x, q4, p);               // P^T  -> packed columns [0, NQ/2)
-      tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);     // dS^T -> packed columns [NQ/2, NQ)
-      // dS^T -> smem for the dQ MMAs, once the previous tile's dQ MMAs have read the buffer
-      if (k >= 1) tc::mbar_wait(&dsfree[(k - 1) & 1], ((k - 1) >> 1) & 1);
-#pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        const int col8 = 4 * q4 + j, ch = col8 >> 3, s = col8 & 7;
-        const uint32_t addr = dsu + (ch == 2 ? 0 : (ch + 1) * 16384) + r * 128 + ((s ^ (r & 7)) << 4);
-        tc::st_shared_v4(addr, make_uint4(pack_bf16(ds[8 * j], ds[8 * j + 1]), pack_bf16(ds[8 * j + 2], ds[8 * j + 3]),
-                                          pack_bf16(ds[8 * j + 4], ds[8 * j + 5]), pack_bf16(ds[8 * j + 6], ds[8 * j + 7])));
-      }
-      tc::tmem_st_wait();
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      tc::mbar_arrive(&pdsfull[b]);
-      if (tr) trace_at(a.trace, 4, k);
-      // dV / dK rows (lane r = key u0 + r)
-      tc::mbar_wait(&kvfull[b], use & 1);
-      if (tr) trace_at(a.trace, 5, k);
-      __syncwarp();
-      tc::tc_fence_after();
-      {
-        float v[64];
-        const long long row = (long long)bh * T + u0 + r;
-        tmem_ld64(DV + lanes, v);
-        if (u0 + r < T) store_row_bf16(a.dV + row * kD, v, 1.f);
-        tmem_ld64(DK + lanes, v);
-        if (u0 + r < T) store_row_bf16(a.dK + row * kD, v, a.scale);
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&kvfree[b]);
-      // dQ rows (lane r = window row r = frame n0 + r; dQ1 lane r = frame n0 + 128 + r)
-      tc::mbar_wait(&dqfull[b], use & 1);
-      if (tr) trace_at(a.trace, 6, k);
-      __syncwarp();
-      tc::tc_fence_after();
-      const bool has_prev = kt > 0, prev_local = has_prev && k > 0;
-      const bool has_next = kt + 1 < ntq;
-      // tiles finish their dQ epilogues in order (cfull completes once per tile: the carry of
-      // tile k - 1 is written, and no arrivals of two tiles can mix in one phase)
-      if (k >= 1) tc::mbar_wait(cfull, (k - 1) & 1);
-      {
-        float v[64];
-        tmem_ld64(x, v);
-        const int n = n0 + r;
-        bool out = n >= 0 && n < T;
-        if (r < nc && has_prev) {
-          if (prev_local) {
-#pragma unroll
-            for (int s = 0; s < 16; ++s) {
-              const float4 c = *carry_at(carry, r, s);
-              v[4 * s] += c.x; v[4 * s + 1] += c.y; v[4 * s + 2] += c.z; v[4 * s + 3] += c.w;
-            }
-          } else {   // first tile of this CTA: the partial goes to the CTA owning key tile kt - 1
-            float4* dst = reinterpret_cast<float4*>(a.ws_hand + ((long long)blockIdx.x * C::NCR + r) * kD);
-#pragma unroll
-            for (int s = 0; s < 16; ++s) dst[s] = make_float4(v[4 * s], v[4 * s + 1], v[4 * s + 2], v[4 * s + 3]);
-            out = false;
-          }
-        }
-        if (out) store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
-      }
-      if (q4 * 32 < nc) {                              // warp-uniform: warps holding carry rows
-        float v[64];
-        tmem_ld64(x + 64, v);
-        if (r < nc) {
-          if (!has_next) {                             // last key tile: these rows are complete
-            const int n = n0 + kM + r;
-            if (n < T) store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
-          } else {                                     // carry for the next tile (here or in the next CTA)
-#pragma unroll
-            for (int s = 0; s < 16; ++s) *carry_at(carry, r, s) = make_float4(v[4 * s], v[4 * s + 1], v[4 * s + 2], v[4 * s + 3]);
-          }
-        }
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tfree[b]);
-      tc::mbar_arrive(cfull);
-      if (tr) trace_at(a.trace, 7, k);
-    }
-  } else {
-    // row warps 10, 11: LSE*log2e and delta_n = dO_n . O_n of each tile's NQ window rows into the
-    // stage's row arrays.  The O loads do not depend on the stage, so they are issued before the
-    // stage lands (latency overlapped with the TMA); dO comes from the landed stage.
-    const int dl = tid - 320;
-    for (int k = 0; k < ntile_me; ++k) {
-      const int g = g_begin + k;
-      const int bh = g / ntq, u0 = (g % ntq) * kM, n0 = u0 - R, st = k % NS;
-      uint4 ov[3][8];
-      float l2[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int w = dl + 64 * i, n = n0 + w;
-        l2[i] = 0.f;
-        if (w < NQ && n >= 0 && n < T) {
-          const uint4* orow = reinterpret_cast<const uint4*>(a.Og + ((long long)bh * T + n) * kD);
-#pragma unroll
-          for (int s = 0; s < 8; ++s) ov[i][s] = __ldg(orow + s);
-          l2[i] = a.LSEin[(long long)bh * T + n] * kLog2e;
-        } else {
-#pragma unroll
-          for (int s = 0; s < 8; ++s) ov[i][s] = make_uint4(0, 0, 0, 0);
-        }
-      }
-      tc::mbar_wait(&full[st], (k / NS) & 1);
-      float* lse2_s = rows + st * 2 * C::NQA;
-      float* del_s = lse2_s + C::NQA;
-      const uint32_t dOs = tc::smem_u32(stage0 + st * C::STAGE + 2 * C::KB + C::QB);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const int w = dl + 64 * i;
-        if (w < NQ) {
-          float de = 0.f;
-#pragma unroll
-          for (int s = 0; s < 8; ++s) de += dot8_bf16(ov[i][s], tc::ld_shared_v4(dOs + w * 128 + ((s ^ (w & 7)) << 4)));
-          lse2_s[w] = l2[i];
-          del_s[w] = de;
-        }
-      }
-      tc::mbar_arrive(&rfull[st]);
-    }
-  }
-  // hand-off between neighbouring CTAs' tiles of one head (see above)
-  if (a.trace && tid == 64 && blockIdx.x == 0) a.trace[8 * 64] = clock64();
-  __threadfence();
-  cg::this_grid().sync();
-  if (ntile_me > 0) {
-    const int kl = ntile_me - 1;                       // last tile of this CTA
-    const int g = g_begin + kl;
-    const int bh = g / ntq, kt = g % ntq;
-    if (kt + 1 < ntq && warp >= 2 && ((warp - 2) >> 2) == (kl & 1)) {
-      const int r = 32 * (warp & 3) + lane;
-      const int n = kt * kM + kM - R + r;
-      if (r < nc && n < T) {
-        const float4* src = reinterpret_cast<const float4*>(a.ws_hand + ((long long)(blockIdx.x + 1) * C::NCR + r) * kD);
-        float v[64];
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-          const float4 c = *carry_at(carry, r, s), o = __ldcg(src + s);
-          v[4 * s] = c.x + o.x; v[4 * s + 1] = c.y + o.y; v[4 * s + 2] = c.z + o.z; v[4 * s + 3] = c.w + o.w;
-        }
-        store_row_bf16(a.dQ + ((long long)bh * T + n) * kD, v, a.scale);
-      }
-    }
-  }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tbase, 512);
-  trace_cta(a.trace, 1);
-}
-
 static_assert(DqCfg<72>::STAGE % 1024 == 0 && DkvCfg<72>::STAGE % 1024 == 0 && FwdCfg<72>::STAGE % 1024 == 0,
               "smem stages must be 1024-byte aligned");
 
 // ------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encoder() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
 // [BH][T][64] bf16 viewed as a 3-D tensor (64, T, BH); box (64, rows, 1), 128B swizzle.
-CUtensorMapL2promotion l2_promo() {   // SATTN_L2_PROMO = 0 (none) / 64 / 128 / 256 (default) bytes
-  const char* e = getenv("SATTN_L2_PROMO");
-  const int v = e ? atoi(e) : 256;
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-       : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
+CUtensorMapL2promotion l2_promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
 bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) {
-    g_tc_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
   cuuint64_t dims[3] = {64, (cuuint64_t)T, (cuuint64_t)BH};
   cuuint64_t strides[2] = {64 * 2, (cuuint64_t)T * 64 * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo());
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return false;
@@ -2769,18 +1765,10 @@ bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
 
 // [C][BH][T][64] bf16 as a 4-D tensor (64, T, BH, C); box (64, rows, 1, 1), 128B swizzle.
 bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) {
-    g_tc_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
   cuuint64_t dims[4] = {64, (cuuint64_t)T, (cuuint64_t)BH, (cuuint64_t)C};
   cuuint64_t strides[3] = {128, (cuuint64_t)T * 128, (cuuint64_t)BH * T * 128};
   cuuint32_t box[4] = {64, (cuuint32_t)rows, 1, 1};
-  cuuint32_t es[4] = {1, 1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled (4d) failed (" + std::to_string((int)r) + ")";
     return false;
@@ -2791,18 +1779,10 @@ bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows)
 // stored band P [BH][T][ldp] bf16 as (ldp, T, BH); box (ldp, rows, 1), no swizzle (row-major
 // [rows][ldp] in shared memory); rows outside [0, T) load as zeros and are clipped on store.
 bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) {
-    g_tc_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
   cuuint64_t dims[3] = {(cuuint64_t)ldp, (cuuint64_t)T, (cuuint64_t)BH};
   cuuint64_t strides[2] = {(cuuint64_t)ldp * 2, (cuuint64_t)T * ldp * 2};
   cuuint32_t box[3] = {(cuuint32_t)ldp, (cuuint32_t)rows, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled (band) failed (" + std::to_string((int)r) + ")";
     return false;
@@ -2812,19 +1792,11 @@ bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int ro
 
 // padded fp32 workspace rows [BH][Tp] viewed as a 2-D tensor (T, BH); box (rows, 1); no swizzle.
 bool make_map_f32_rows(CUtensorMap* m, const void* base, int T, int Tp, int BH, int box) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) {
-    g_tc_err = "cuTensorMapEncodeTiled unavailable";
-    return false;
-  }
   // 3-D view (T, BH, 1) so the load uses the same tensor-tile instruction form as the bf16 tiles
   cuuint64_t dims[3] = {(cuuint64_t)T, (cuuint64_t)BH, 1};
   cuuint64_t strides[2] = {(cuuint64_t)Tp * 4, (cuuint64_t)Tp * 4 * BH};
   cuuint32_t bx[3] = {(cuuint32_t)box, 1, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, bx, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, bx, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE);
   if (r != CUDA_SUCCESS) {
     g_tc_err = "cuTensorMapEncodeTiled (f32 rows) failed (" + std::to_string((int)r) + ")";
     return false;
@@ -2859,7 +1831,6 @@ int cw_of(int W) {
 
 TcArgs tc_args(const AttnArgs& a) {
   TcArgs t{};
-  if (const char* e = getenv("SATTN_MMA_SLEEP")) t.mma_sleep = atoi(e);
   t.T = a.T; t.L = a.L; t.R = a.R; t.BH = a.BH;
   t.scale = a.scale; t.scale_log2 = a.scale_log2;
   t.O = reinterpret_cast<bf16*>(a.Out); t.LSE = a.LSEout;
@@ -2868,8 +1839,6 @@ TcArgs tc_args(const AttnArgs& a) {
   t.delta = a.delta;
   t.Tp = (a.T + 3) & ~3;
   t.trace = g_trace;
-  t.qsplit = 1;
-  t.ksplit = 1;
   t.kshift = 0;
   t.ws_del = a.delta;
   t.ws_l2 = a.delta + (long long)a.BH * t.Tp;
@@ -2892,119 +1861,49 @@ template <int CW, bool PST = false>
 sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   using C = FwdCfg<CW, PST>;
   TcArgs ta = tc_args(a);
-  if (const char* e = getenv("SATTN_FWD_QSPLIT")) ta.qsplit = atoi(e);
-  if (const char* e = getenv("SATTN_FWD_KSPLIT")) ta.ksplit = atoi(e);
-  ta.ksplit_pf = 0;   // L2 prefetch of later tiles measured slower (18.7 vs 22.6 us, gpurun_out/diag8)
-  if (const char* e = getenv("SATTN_FWD_PF")) ta.ksplit_pf = atoi(e);
-  if (kM % ta.qsplit || (kM / ta.qsplit) % 8 || C::NK % ta.ksplit || (C::NK / ta.ksplit) % 8) ta.qsplit = ta.ksplit = 1;
   CUtensorMap mq, mk, mv, mo, mp;
-  if (!make_map(&mq, a.Q, a.T, a.BH, kM / ta.qsplit) || !make_map(&mk, a.K, a.T, a.BH, C::NK / ta.ksplit) ||
-      !make_map(&mv, a.V, a.T, a.BH, C::NK / ta.ksplit) || !make_map(&mo, a.Out, a.T, a.BH, kM))
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, C::NK) ||
+      !make_map(&mv, a.V, a.T, a.BH, C::NK) || !make_map(&mo, a.Out, a.T, a.BH, kM))
     return SATTN_ECUDA;
   if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
-  cudaFuncSetAttribute(sa_fwd_tc<CW, PST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  set_smem(sa_fwd_tc<CW, PST>, C::SMEM);
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   launch_pdl(sa_fwd_tc<CW, PST>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, PST ? mp : mo, ta);
   return SATTN_OK;
 }
 
-size_t fused_ws_bytes() { return (size_t)num_sms() * FusCfg<72>::NCR * kD * sizeof(float); }
-
-// SA backward variant: the two-kernel K1 + K2 path (default; faster on B200 as measured)
-// or, with SATTN_SA_BWD=fused, the single-pass key-major sweep (sa_bwd_fused_tc).  Read per call.
-bool sa_bwd_split() {
-  const char* e = getenv("SATTN_SA_BWD");
-  return !(e && !strcmp(e, "fused"));
-}
-
-template <int CW>
-sattn_status bwd_fused_launch(const AttnArgs& a, cudaStream_t st) {
-  using C = FusCfg<CW>;
-  CUtensorMap mk, mv, mq, mdo, mo;
-  if (!make_map(&mk, a.K, a.T, a.BH, kM) || !make_map(&mv, a.V, a.T, a.BH, kM) ||
-      !make_map(&mq, a.Q, a.T, a.BH, C::NQ) || !make_map(&mdo, a.dO, a.T, a.BH, C::NQ) ||
-      !make_map(&mo, a.O, a.T, a.BH, C::NQ))
-    return SATTN_ECUDA;
-  TcArgs t = tc_args(a);
-  t.ws_hand = a.delta;
-  if (const char* e = getenv("SATTN_FUSED_ORDER")) t.mma_order = atoi(e);
-  t.qsplit = 1;   // fused: L2 prefetch of tile k + 2 (SATTN_FUSED_PREFETCH=0 disables)
-  if (const char* e = getenv("SATTN_FUSED_PREFETCH")) t.qsplit = atoi(e);
-  const int ntiles = (a.T + kM - 1) / kM * a.BH;
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  cudaFuncSetAttribute(sa_bwd_fused_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;   // grid-wide barrier for the CTA-boundary dQ rows
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, sa_bwd_fused_tc<CW>, mk, mv, mq, mdo, mo, t);
-  if (e != cudaSuccess) {
-    g_tc_err = std::string("fused backward launch: ") + cudaGetErrorString(e);
-    return SATTN_ECUDA;
-  }
-  return SATTN_OK;
-}
-
 template <int CW>
 sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
-  if (!sa_bwd_split()) return bwd_fused_launch<CW>(a, st);
   constexpr int NK = nk_of(CW);
   const int Tp = (a.T + 3) & ~3;
   const float* l2ws = a.delta + (long long)a.BH * Tp;
+  // bands too wide for the two-stage K2's shared memory (W > 49: NQ = 192) take the block-ring
+  // kernel with the column-split warpgroups (its registers hold half a row)
+  constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
+  constexpr int NQP = wide ? DkvRCfg<CW>::NQP : DkvCfg<CW>::NQP;
   CUtensorMap mq, mk, mv, mdo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv, ml2, mdel;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
       !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
       !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
       !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
       !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
-      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, DkvCfg<CW>::NQP) ||
-      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, DkvCfg<CW>::NQP))
+      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NQP) ||
+      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, NQP))
     return SATTN_ECUDA;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  const char* only = getenv("SATTN_BWD_ONLY");  // debug: run only K1 ("1") or only K2 ("2")
-  if (!only || only[0] != '2') {
-  cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+  set_smem(sa_bwd_dq_tc<CW>, DqCfg<CW>::SMEM);
   launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq,
              tc_args(a));
-  }
-  if (!only || only[0] != '1') {
-    // K2 variant: the two-stage window kernel (default, measured faster) or, with SATTN_K2=ring,
-    // the block-ring sweep (loads hidden, but a longer warpgroup chain: DESIGN.md §10)
-    const char* k2 = getenv("SATTN_K2");
-    // bands too wide for the two-stage kernel's shared memory (W > 49: NQ = 192) take the
-    // block-ring kernel with the column-split warpgroups (its registers hold half a row)
-    constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
-    if (!wide && k2 && !strcmp(k2, "rm64")) {
-      cudaFuncSetAttribute(sa_bwd_dkdv_rm64_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, RM64Cfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_rm64_tc<CW>, dim3(grid), dim3(RM64Cfg<CW>::THREADS), RM64Cfg<CW>::SMEM, st, mq, mk128,
-                 mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
-    } else if (!wide && k2 && !strcmp(k2, "m64")) {
-      cudaFuncSetAttribute(sa_bwd_dkdv_m64_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_m64_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128,
-                 mv128, mdoN, mdk, mdv, ml2, mdel, tc_args(a));
-    } else if (wide || (k2 && !strcmp(k2, "coop"))) {
-      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
-                 mk128, mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
-    } else if (!(k2 && !strcmp(k2, "ring"))) {
-      cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
-                 mdoN, mdk, mdv, ml2, mdel, tc_args(a));
-    } else {
-      cudaFuncSetAttribute(sa_bwd_dkdv_ring_tc<CW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvRCfg<CW>::SMEM);
-      launch_pdl(sa_bwd_dkdv_ring_tc<CW, false>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq, mk128,
-                 mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
-    }
+  if constexpr (wide) {
+    set_smem(sa_bwd_dkdv_ring_tc<CW, true>, DkvRCfg<CW>::SMEM);
+    launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
+               mk128, mv128, mdo, mdk, mdv, ml2, mdel, tc_args(a));
+  } else {
+    set_smem(sa_bwd_dkdv_tc<CW>, DkvCfg<CW>::SMEM);
+    launch_pdl(sa_bwd_dkdv_tc<CW>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN, mk128, mv128,
+               mdoN, mdk, mdv, ml2, mdel, tc_args(a));
   }
   return SATTN_OK;
 }
@@ -3044,13 +1943,13 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   // (0) staircase part of delta = rowsum(P o dP)
   {
     const size_t smem = stair_smem_bytes(R, true);
-    cudaFuncSetAttribute(llsa_bwd_stair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem(llsa_bwd_stair<true>, (int)smem);
     llsa_bwd_stair<true><<<sgrid, 256, smem, st>>>(sa);
   }
   // (1) query-major band pass of every channel in one launch: the SA dQ kernel with R := 0 and
   //     channel c's keys shifted by R - c (tiles ordered channel-major)
   {
-    cudaFuncSetAttribute(sa_bwd_dq_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+    set_smem(sa_bwd_dq_tc<CW>, DqCfg<CW>::SMEM);
     CUtensorMap mq, mk, mv, mdo, mdq;
     if (!make_map4(&mq, Q, a.T, a.BH, bc ? 1 : C, kM) || !make_map(&mk, Kr, a.T, a.BH, NK) ||
         !make_map(&mv, Vr, a.T, a.BH, NK) || !make_map4(&mdo, dO, a.T, a.BH, C, kM) ||
@@ -3080,14 +1979,14 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
         !make_map_f32_rows(&mdel, ws_del, a.T, Tp, C * a.BH, LC::NQP))
       return SATTN_ECUDA;
     TcArgs t = tc_args(a);
-    cudaFuncSetAttribute(llsa_bwd_kv_tc<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, LC::SMEM);
+    set_smem(llsa_bwd_kv_tc<CW>, LC::SMEM);
     launch_pdl(llsa_bwd_kv_tc<CW>, dim3(grid), dim3(320), LC::SMEM, st, mq4, mk, mv, mdo4, mdk, mdv, ml2, mdel, t, C,
                bc ? 1 : 0);
   }
   // (3) staircase keys and the staircase part of dQ (mma.sync)
   {
     const size_t smem = stair_smem_bytes(R, false);
-    cudaFuncSetAttribute(llsa_bwd_stair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem(llsa_bwd_stair<false>, (int)smem);
     llsa_bwd_stair<false><<<sgrid, 256, smem, st>>>(sa);
   }
   return SATTN_OK;
@@ -3130,7 +2029,7 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-int tc_backward_launches() { return sa_bwd_split() ? 2 : 1; }
+int tc_backward_launches() { return 2; }
 
 // ---- stored-band mode (NEXT-4): forward W <= 64 (P staging rows fit the O tile), backward
 // W <= 49 (the P window replaces K in the two-stage K2 stage; for W > 41 with one dV/dK
@@ -3170,10 +2069,10 @@ sattn_status bwd_p_launch(const AttnArgs& a, cudaStream_t st) {
     return SATTN_ECUDA;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  cudaFuncSetAttribute(sa_bwd_dq_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<CW>::SMEM);
+  set_smem(sa_bwd_dq_tc<CW, true>, DqCfg<CW>::SMEM);
   launch_pdl(sa_bwd_dq_tc<CW, true>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mp128, mk, mv, mdo,
              mdq, tc_args(a));
-  cudaFuncSetAttribute(sa_bwd_dkdv_tc<CW, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, K2::SMEM_P);
+  set_smem(sa_bwd_dkdv_tc<CW, true>, K2::SMEM_P);
   launch_pdl(sa_bwd_dkdv_tc<CW, true>, dim3(grid), dim3(K2::THREADS), K2::SMEM_P, st, mqN, mpN, mv128, mdoN, mdk,
              mdv, mdel, mdel, tc_args(a));
   return SATTN_OK;
@@ -3190,7 +2089,7 @@ sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st) {
   g_tc_err = "band too wide for the tensor-core stored-band backward";
   return SATTN_EUNSUPPORTED;
 }
-size_t tc_backward_ws_bytes() { return fused_ws_bytes(); }
+size_t tc_backward_ws_bytes() { return 0; }
 
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {
   // band width L+1 on the SA kernels (CW <= 80), staircase staging of 16 + 2R frames x C channels

@@ -8,8 +8,10 @@ neighbours per call is exact:
 
     forward   K, V (and Q, to keep tile alignment) halo: L frames from the left
               neighbour, R frames from the right
-    backward  Q, K, V, O, dO, LSE halo of max(L, R) frames on both sides
-              (halo queries carry their true LSE and O, so P and delta are exact)
+    backward  Q, K, V, O, dO, LSE halo of L + R frames on both sides: halo queries
+              n in [t0 - R, t0) feed local dK/dV, and the tensor-core K1 computes their
+              delta = rowsum(P o dP) over their whole window [n - L, n + R], which reaches
+              t0 - R - L (reading G26), so the halo must hold it
 
 The exchange is point-to-point (torch.distributed batch_isend_irecv: NCCL over
 NVLink between GPUs, gloo on CPU for the tests).  The attention runs on the
@@ -110,7 +112,7 @@ def sa_backward_tsharded(q, k, v, o, lse, do, L: int, R: int, group=None, align:
     o, lse are this rank's rows of the forward."""
     attn_bwd = attn_bwd or _default_bwd
     T_loc = q.shape[-2]
-    h = _halo(max(L, R), align, T_loc, group)
+    h = _halo(L + R, align, T_loc, group)
     q_e, nl = exchange_halo(q, h, h, group)
     k_e, _ = exchange_halo(k, h, h, group)
     v_e, _ = exchange_halo(v, h, h, group)

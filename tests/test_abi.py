@@ -81,10 +81,9 @@ def test_workspace_and_saved_sizes(lib):
     assert lib.llsa_backward_workspace(ctypes.byref(d)) == 3 * 3 * 2 * 3 * 40 * 4
     assert lib.sattn_stack_saved_bytes(ctypes.byref(d), pkg.MODE_SA, 2) > 0
     assert lib.sattn_stack_saved_bytes(ctypes.byref(d), 9, 2) == 0
-    # bf16, D = 64, W <= 65 (tensor-core backward): at least the fused sweep's hand-off rows
-    # (one 48 x 64 fp32 slot per CTA of the persistent grid)
+    # bf16, D = 64 (tensor-core backward): the same padded rows
     tcd = _desc(B=1, H=1, T=37, D=64, L=5, R=2, dtype=pkg.BF16)
-    assert lib.sa_backward_workspace(ctypes.byref(tcd)) >= 148 * 48 * 64 * 4
+    assert lib.sa_backward_workspace(ctypes.byref(tcd)) == 2 * 1 * 40 * 4
     bad = _desc(T=0)
     assert lib.sa_backward_workspace(ctypes.byref(bad)) == 0
 

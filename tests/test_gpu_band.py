@@ -40,7 +40,7 @@ def test_sa_stored_band(shape, L, R, dt, impl):
     assert p.shape == tuple(shape[:-1]) + (_ld(L, R),) and p.dtype == tq.dtype
     O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
     A = oracle.sa.sa_band_probs(q, k, L, R)
-    assert excess(o, O, dt) <= 0, ("O", maxerr(o, O))
+    assert excess(o, O, dt, "O") <= 0, ("O", maxerr(o, O))
     assert maxerr(lse, LSE) <= TOL[dt], ("LSE", maxerr(lse, LSE))
     # the band: entries within the gate; exact zeros outside the clipped window and in the padding
     ph = host(p)
@@ -53,7 +53,7 @@ def test_sa_stored_band(shape, L, R, dt, impl):
     dq, dk, dv = s.sa_backward_p(tq, tk, tv, o, p, tdo, L, R, impl=impl)
     G = oracle.sa.sa_backward(q, k, v, do, L, R)
     for name, got, ref in (("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
+        assert excess(got, ref, dt, name) <= 0, (name, maxerr(got, ref))
     # backward from the oracle's band (rounded to the tensor dtype): the band-form oracle
     pa = torch.zeros_like(p)
     pa[..., :W] = dev(A, dt)
@@ -62,7 +62,7 @@ def test_sa_stored_band(shape, L, R, dt, impl):
     Ar = host(pa)[..., :W]
     G2 = oracle.sa.sa_backward_band(Ar, q, k, v, do, L, R)
     for name, got, ref in (("dQ", dq2, G2[0]), ("dK", dk2, G2[1]), ("dV", dv2, G2[2])):
-        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
+        assert excess(got, ref, dt, name) <= 0, (name, maxerr(got, ref))
 
 
 def test_sa_stored_band_errors():
@@ -115,4 +115,4 @@ def test_sa_stored_band_full_base_shape_sampled_heads():
         assert maxerr(p[b, h, :, :W], A) <= 4e-3, (b, h, "P")
         for name, got, ref in (("O", o[b, h], O), ("LSE", lse[b, h], LSE), ("dQ", dq[b, h], G[0]),
                                ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
+            assert excess(got, ref, "bf16", name) <= 0, (b, h, name, maxerr(got, ref))

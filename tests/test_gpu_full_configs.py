@@ -14,9 +14,9 @@ pytestmark = pytest.mark.gpu
 L, R = 32, 8
 
 
-def _excess(got, ref):
+def _excess(got, ref, name=""):
     from test_gpu_parity import excess
-    return excess(got, ref, "bf16")
+    return excess(got, ref, "bf16", name)
 
 
 def _rand(shape, seed):
@@ -42,7 +42,7 @@ def test_large_config_sampled_heads():
         G = oracle.sa.sa_backward(Q, K, V, dO, L, R)
         for name, got, ref in (("O", o[b, h], O), ("LSE", lse[b, h], LSE), ("dQ", dq[b, h], G[0]),
                                ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert _excess(got, ref) <= 0, (b, h, name)
+            assert _excess(got, ref, name) <= 0, (b, h, name)
 
 
 def test_hour_stream_slabs():
@@ -68,7 +68,7 @@ def test_hour_stream_slabs():
         for name, got, ref in (("O", o[0, :, lo:hi], O[:, r]), ("LSE", lse[0, :, lo:hi], LSE[:, r]),
                                ("dQ", dq[0, :, lo:hi], G[0][:, r]), ("dK", dk[0, :, lo:hi], G[1][:, r]),
                                ("dV", dv[0, :, lo:hi], G[2][:, r])):
-            assert _excess(got, ref) <= 0, (c, name)
+            assert _excess(got, ref, name) <= 0, (c, name)
 
 
 def test_llsa_base_config_sampled_heads():
@@ -85,4 +85,4 @@ def test_llsa_base_config_sampled_heads():
         for name, got, ref in (("O", o[:, b:b + 1, h:h + 1], O), ("LSE", lse[:, b:b + 1, h:h + 1], LSE),
                                ("dQ", dq[:, b:b + 1, h:h + 1], G[0]), ("dK", dk[:, b:b + 1, h:h + 1], G[1]),
                                ("dV", dv[:, b:b + 1, h:h + 1], G[2])):
-            assert _excess(got, ref) <= 0, (b, h, name)
+            assert _excess(got, ref, name) <= 0, (b, h, name)

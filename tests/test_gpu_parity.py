@@ -15,7 +15,8 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"f32": 1e-5, "bf16": 2e-2}
+from gates import TOL, excess as _gate_excess
+
 TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
 
 
@@ -36,23 +37,10 @@ def maxerr(got, ref):
     return float(np.abs(host(got) - np.asarray(ref)).max()) if np.asarray(ref).size else 0.0
 
 
-def bf16_ulp(ref):
-    """Spacing of the bf16 grid at |ref| (8 significant bits)."""
-    a = np.abs(np.asarray(ref, dtype=np.float64))
-    return np.exp2(np.floor(np.log2(np.maximum(a, 2.0 ** -126))) - 7)
-
-
-def excess(got, ref, dt):
-    """max over elements of |got - ref| - bound, bound = TOL (fp32) or, for bf16 outputs,
-    max(TOL, ulp_bf16(ref)) (G27: a bf16 result is within the gate or is one of the
-    two bf16 neighbours of the exact value; the relaxation only acts where |ref| >= 4, where a
-    correctly rounded value alone may sit 0.0156 from it).  <= 0 passes."""
-    ref = np.asarray(ref)
-    if not ref.size:
-        return 0.0
-    e = np.abs(host(got) - ref)
-    bound = TOL[dt] if dt == "f32" else np.maximum(TOL[dt], bf16_ulp(ref))
-    return float((e - bound).max())
+def excess(got, ref, dt, name=""):
+    """<= 0 passes: |got - ref| <= TOL (fp32) or <= 2e-2 + ulp_bf16(ref)/2 (bf16 outputs,
+    DESIGN.md G27); recorded in the session's parity gate report (tests/gates.py)."""
+    return _gate_excess(host(got), ref, dt, name)
 
 
 SA_F32 = [
@@ -75,7 +63,7 @@ def test_sa_fp32(shape, L, R, impl):
     O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
     G = oracle.sa.sa_backward(q, k, v, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert maxerr(got, ref) <= TOL["f32"], (name, maxerr(got, ref))
+        assert excess(got, ref, "f32", name) <= 0, (name, maxerr(got, ref))
 
 
 SA_BF16 = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16),
@@ -94,7 +82,7 @@ def test_sa_bf16(shape, L, R, impl):
     O, LSE = oracle.sa.sa_forward(q, k, v, L, R)
     G = oracle.sa.sa_backward(q, k, v, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert excess(got, ref, "bf16") <= 0, (name, maxerr(got, ref))
+        assert excess(got, ref, "bf16", name) <= 0, (name, maxerr(got, ref))
 
 
 @pytest.mark.parametrize("impl", ["auto", "ffma"])
@@ -114,7 +102,7 @@ def test_sa_full_base_shape_sampled_heads(impl):
         G = oracle.sa.sa_backward(q, k, v, do, L, R)
         for name, got, ref in (("O", o[b, h], O), ("LSE", lse[b, h], LSE), ("dQ", dq[b, h], G[0]),
                                ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
+            assert excess(got, ref, "bf16", name) <= 0, (b, h, name, maxerr(got, ref))
 
 
 LLSA_CASES = [
@@ -144,7 +132,7 @@ def test_llsa(dt, shape, L, R, broadcast):
     O, LSE = oracle.llsa.llsa_forward(Q, K, V, L, R)
     G = oracle.llsa.llsa_backward(Q, K, V, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert excess(got, ref, dt) <= 0, (name, maxerr(got, ref))
+        assert excess(got, ref, dt, name) <= 0, (name, maxerr(got, ref))
 
 
 def test_deterministic_bitwise():
@@ -189,55 +177,14 @@ def test_sa_locality_exact_zero_fwd_and_bwd(dt):
     assert not changed[~expect].any()
 
 
-# The single-pass key-major backward (SATTN_SA_BWD=fused, sa_bwd_fused_tc): a CTA sweeps a
-# contiguous range of key tiles; dQ rows near tile and CTA boundaries combine two partial sums
-# (a carry in smem, or a workspace hand-off across a grid barrier).  Same gates as the default.
-FUSED = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16),
-         ((1, 3, 777, 64), 32, 8), ((1, 1, 130, 64), 8, 40), ((3, 2, 300, 64), 24, 0)]
+# The block-ring K2 (taken for 49 < W <= 65): a contiguous key-tile sweep per CTA with 128-row
+# Q/dO blocks shared by consecutive tiles; block reuse and release at head changes are what these
+# shapes exercise (several heads per CTA range, ragged ends).
+RING = [((2, 2, 1750, 64), 32, 32), ((1, 2, 300, 64), 40, 24), ((1, 3, 777, 64), 16, 48), ((2, 3, 300, 64), 64, 0)]
 
 
-@pytest.mark.parametrize("shape,L,R", FUSED)
-def test_sa_bf16_fused_backward(shape, L, R, monkeypatch):
-    monkeypatch.setenv("SATTN_SA_BWD", "fused")
-    s = sattn()
-    q, k, v = synth.qkv(5, shape, "bf16")
-    do = synth.grad_out(5, shape, "bf16")
-    tq, tk, tv, tdo = (dev(x, "bf16") for x in (q, k, v, do))
-    o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
-    dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
-    G = oracle.sa.sa_backward(q, k, v, do, L, R)
-    for name, got, ref in (("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
-        assert excess(got, ref, "bf16") <= 0, (name, maxerr(got, ref))
-    # run-to-run bitwise
-    dq2, dk2, dv2 = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
-    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
-
-
-def test_sa_fused_backward_full_shape_cta_boundaries(monkeypatch):
-    # B=8, H=12, T=1750: 1344 key tiles over the grid, so CTA ranges start and end inside heads;
-    # check every head in full against the oracle (dQ rows at hand-offs included)
-    monkeypatch.setenv("SATTN_SA_BWD", "fused")
-    s = sattn()
-    B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
-    g = torch.Generator("cuda").manual_seed(11)
-    tq, tk, tv, tdo = (torch.randn(B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
-    o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
-    dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
-    for (b, h) in ((0, 0), (0, 1), (2, 5), (4, 9), (7, 11)):
-        q, k, v, do = (host(x[b, h]) for x in (tq, tk, tv, tdo))
-        G = oracle.sa.sa_backward(q, k, v, do, L, R)
-        for name, got, ref in (("dQ", dq[b, h], G[0]), ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
-
-
-# The block-ring K2 (SATTN_K2=ring): a contiguous key-tile sweep per CTA with 128-row Q/dO
-# blocks shared by consecutive tiles; block reuse and release at head changes are what these
-# shapes exercise (several heads per CTA range, ragged ends, W from 1 to 49).
-RING = [((1, 2, 129, 64), 0, 0), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16), ((1, 3, 777, 64), 32, 8),
-        ((3, 2, 300, 64), 24, 0), ((8, 12, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 32), ((1, 2, 300, 64), 40, 24)]
-
-
-def _ring_check(shape, L, R):
+@pytest.mark.parametrize("shape,L,R", RING)
+def test_sa_bf16_block_ring_k2(shape, L, R):
     s = sattn()
     B, H = shape[:2]
     q, k, v = synth.qkv(6, shape, "bf16")
@@ -245,19 +192,10 @@ def _ring_check(shape, L, R):
     tq, tk, tv, tdo = (dev(x, "bf16") for x in (q, k, v, do))
     o, lse = s.sa_forward(tq, tk, tv, L, R, impl="tc")
     dq, dk, dv = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
-    heads = [(b, h) for b in range(B) for h in range(H)][:: max(1, (B * H) // 6)]
-    for (b, h) in heads:
-        G = oracle.sa.sa_backward(q[b, h], k[b, h], v[b, h], do[b, h], L, R)
-        for name, got, ref in (("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
-            assert excess(got, ref, "bf16") <= 0, (b, h, name, maxerr(got, ref))
+    for b in range(B):
+        for h in range(H):
+            G = oracle.sa.sa_backward(q[b, h], k[b, h], v[b, h], do[b, h], L, R)
+            for name, got, ref in (("dQ", dq[b, h], G[0]), ("dK", dk[b, h], G[1]), ("dV", dv[b, h], G[2])):
+                assert excess(got, ref, "bf16", name) <= 0, (b, h, name, maxerr(got, ref))
     dq2, dk2, dv2 = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R, impl="tc")
     assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
-
-
-@pytest.mark.parametrize("variant", ["ring", "coop", "m64", "rm64"])
-@pytest.mark.parametrize("shape,L,R", RING)
-def test_sa_bf16_k2_variants(shape, L, R, variant, monkeypatch):
-    # SATTN_K2=ring: block-ring sweep; SATTN_K2=coop: the same with both warpgroups on every
-    # tile (column halves of each row, deferred dV / dK epilogue)
-    monkeypatch.setenv("SATTN_K2", variant)
-    _ring_check(shape, L, R)

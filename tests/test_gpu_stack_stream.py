@@ -128,3 +128,58 @@ def test_sa_stream_matches_oracle_recurrence_and_offline(dt, tol, n):
         assert np.abs(host(ys) - Y_or).max() <= tol * mag
     y_off, _ = s.stack_forward(tx, L, R, n, s.MODE_SA)
     assert np.abs(host(ys) - host(y_off)).max() <= tol * mag
+
+
+@pytest.mark.parametrize("mode", ["sa", "llsa"])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_stack_base_shape_12_layers_vs_oracle(mode, dt):
+    # SURVEY §8(c) parity grid: the base shape (T=1750, D=64, (32,8)) through the 12-layer stack on
+    # 2 (b,h) units, forward and backward, against the fp64 oracle stack.  The bf16 stack rounds X_l
+    # to bf16 at every layer boundary (its activation dtype) while the oracle carries fp64; the gate is
+    # the north_star gate per unit output magnitude (reading G24) and the plain max-abs is reported.
+    from gates import excess
+    s = sattn()
+    m = s.MODE_SA if mode == "sa" else s.MODE_LLSA
+    B, H, T, D, L, R, n = 1, 2, 1750, 64, 32, 8, 12
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    x = synth.round_to(synth.normal(8, "X", (B, H, T, D)), dt)
+    dyshape = ((R + 1,) if mode == "llsa" else ()) + (B, H, T, D)
+    dy = synth.round_to(synth.normal(8, "dY", dyshape), dt)
+    tx, tdy = dev(x, tdt), dev(dy, tdt)
+    y, saved = s.stack_forward(tx, L, R, n, m)
+    dx = s.stack_backward(tx, saved, tdy, L, R, n, m)
+    Y, _ = oracle.stack.stack_forward(x, L, R, n, mode)
+    DX = oracle.stack.stack_backward(x, dy, L, R, n, mode)
+    sy, sdx = max(1.0, float(np.abs(Y).max())), max(1.0, float(np.abs(DX).max()))
+    assert excess(host(y), Y, dt, "Y", scale=sy) <= 0, np.abs(host(y) - Y).max()
+    assert excess(host(dx), DX, dt, "dX0", scale=sdx) <= 0, np.abs(host(dx) - DX).max()
+
+
+@pytest.mark.parametrize("dt,tol", [(torch.float32, 1e-5), (torch.bfloat16, 2e-2)])
+def test_sa_stream_shorter_than_latency(dt, tol):
+    # a stream shorter than the stack's latency n R (T=20 < 3 x 8): every output comes from the
+    # flush, whose steps must still push layers 0..n-2's frames into the next layer's ring
+    s = sattn()
+    B, H, T, D, L, R, n = 1, 2, 20, 64, 32, 8, 3
+    x = synth.round_to(synth.normal(9, "X", (B, H, T, D)), "f32" if dt == torch.float32 else "bf16")
+    tx = dev(x, dt)
+    st = s.SAStream(B, H, D, L, R, n, dtype=dt)
+    for h in range(T):
+        assert st.step(tx[:, :, h].contiguous()) is None
+    tail = st.flush()
+    assert tail.shape[0] == T
+    Y_or, _ = oracle.stream.sa_stream_all(x, L, R, n)
+    mag = max(1.0, float(np.abs(Y_or).max()))
+    assert np.abs(host(tail.permute(1, 2, 0, 3)) - Y_or).max() <= tol * mag
+    # and a second, longer stream on the same handle after reset matches too (no stale ring rows)
+    st.reset()
+    x2 = synth.round_to(synth.normal(10, "X", (B, H, 40, D)), "f32" if dt == torch.float32 else "bf16")
+    tx2 = dev(x2, dt)
+    ys = []
+    for h in range(40):
+        r = st.step(tx2[:, :, h].contiguous())
+        if r is not None:
+            ys.append(r[1])
+    ys = torch.stack(ys + list(st.flush()), 2)
+    Y2, _ = oracle.stream.sa_stream_all(x2, L, R, n)
+    assert np.abs(host(ys) - Y2).max() <= tol * max(1.0, float(np.abs(Y2).max()))

@@ -136,7 +136,8 @@ def test_llsa_extra_compute_ratio():
 
 
 # ---- infer_sa (NEXT-2): the SA stack run incrementally; latency n_layers x R (Table 3)
-@pytest.mark.parametrize("L,R,n,T", [(3, 1, 2, 16), (4, 2, 3, 40), (0, 3, 2, 25), (5, 0, 3, 20), (6, 2, 1, 9)])
+@pytest.mark.parametrize("L,R,n,T", [(3, 1, 2, 16), (4, 2, 3, 40), (0, 3, 2, 25), (5, 0, 3, 20), (6, 2, 1, 9),
+                                     (5, 4, 3, 7), (2, 3, 4, 5)])  # T < n R: every output from the flush
 def test_sa_stream_online_equals_offline(L, R, n, T):
     x = synth.normal(4, "X", (2, 3, T, 4))
     y_off = stack.stack_forward(x, L, R, n, "sa")[0]
