@@ -42,7 +42,7 @@ typedef enum {
   SATTN_ECONFIG = 3,       /* inconsistent configuration (e.g. workspace too small) */
   SATTN_EUNSUPPORTED = 4,  /* valid but not implemented (dtype x D x impl) */
   SATTN_ECUDA = 5,         /* a CUDA runtime/driver call failed */
-  SATTN_ENCCL = 6          /* reserved for the time-sharded (NCCL) path */
+  SATTN_ENCCL = 6          /* the time-sharded path's exchange failed (NCCL or callback) */
 } sattn_status;
 
 enum { SATTN_F32 = 0, SATTN_BF16 = 1 };            /* desc->dtype */
@@ -132,6 +132,10 @@ sattn_status llsa_backward(const sattn_desc* desc, const void* Q, const void* K,
 size_t sattn_stack_saved_bytes(const sattn_desc* desc, int mode, int n_layers);
 sattn_status sattn_stack_forward(const sattn_desc* desc, int mode, int n_layers, const void* X0,
                                  void* saved, size_t saved_bytes, void* Y, void* stream);
+/* Byte offsets in `saved` of layer l's input X_l (l = 0: [B][H][T][D]; l > 0: [C][B][H][T][D]
+ * for LLSA, [B][H][T][D] for SA), its attention output O_l and LSE_l (shaped as the forward
+ * calls' outputs) — for inspecting the stack layer by layer (out3 = {X_l, O_l, LSE_l}).       */
+sattn_status sattn_stack_saved_offsets(const sattn_desc* desc, int mode, int n_layers, int layer, int64_t* out3);
 /* Gradient of <dY, Y> w.r.t. X0 (dY shaped like Y; dX0 [B][H][T][D]).
  * ws >= sattn_stack_workspace(desc, mode, n_layers).                          */
 size_t sattn_stack_workspace(const sattn_desc* desc, int mode, int n_layers);
@@ -177,6 +181,55 @@ sattn_status sa_stream_step(sattn_stream* s, const void* x_new, void* y_out, int
 sattn_status sa_stream_flush(sattn_stream* s, void* y_tail, int32_t* n_out, void* stream);
 sattn_status sa_stream_reset(sattn_stream* s);
 void sa_stream_destroy(sattn_stream* s);
+
+/* ---------------- time sharding over ranks (Eq. 4) ----
+ * One long stream (the hour-long stream) split over ranks by time: rank r owns frames
+ * [t0, t0 + T) of every (b, h), shards in rank order.  Eq. 4's window makes O_t depend on
+ * K, V over [t-L, t+R] and Eq. 7/13's gathers (G3) make dK_u, dV_u depend on queries
+ * [u-R, u+L], so one exchange of boundary frames with the two neighbours per call is exact.
+ *
+ * MARGINED layout: every tensor of these calls is [B][H][M + T + M][D] (LSE
+ * [B][H][M + T + M], fp32) with M = SATTN_TSHARD_MARGIN frames on both sides; the local
+ * frames are rows [M, M + T).  The library fills the margins it needs from the neighbours
+ * (forward: K, V L+R rows each side, Q R rows left / L right; backward: dO R left / L right)
+ * and computes the halo queries' LSE (forward) and delta (backward) itself, so no LSE or
+ * delta crosses ranks.  Margin rows the exchange does not write must hold finite values
+ * (zero-initialise the buffers once).  The backward must get the same Q, K, V buffers (with
+ * the margins the forward filled) and the forward's LSE.  Outputs: local rows of O / LSE /
+ * dQ / dK / dV (margin rows of the outputs are scratch).  With t0 a multiple of 128 the local
+ * rows are bitwise equal to the unsharded call's.  Tensor-core path only: bf16, D = 64,
+ * L + R + 1 <= 65, L + R <= M; every shard T >= L + R when it has neighbours.
+ * The exchange overlaps the tiles whose operands are all local; no host synchronisation.
+ * Transport: NCCL (sattn_dist_init: one communicator per process, send/recv to rank +- 1
+ * in one group on a library stream) or a caller callback (sattn_dist_init_external). */
+#define SATTN_TSHARD_MARGIN 128
+typedef struct {
+  sattn_desc local;      /* B, H, D, L, R, dtype, scale, impl; T = this rank's frames */
+  int64_t t0;            /* global index of this rank's first frame */
+  int64_t T_global;      /* frames of the whole stream */
+} sattn_tshard_desc;
+typedef struct sattn_dist sattn_dist;   /* opaque: communicator, stream, events */
+/* callback transport: exchange the four DEVICE buffers with rank-1 (send_left / recv_left) and
+ * rank+1 (send_right / recv_right); NULL / 0 where there is no neighbour.  `send_*` are ready
+ * once `stream`'s prior work completes; `recv_*` must be filled before later work on `stream`
+ * runs (the callback may synchronise).  Return 0 on success. */
+typedef int (*sattn_exchange_fn)(void* user, const void* send_left, size_t send_left_bytes, void* recv_left,
+                                 size_t recv_left_bytes, const void* send_right, size_t send_right_bytes,
+                                 void* recv_right, size_t recv_right_bytes, void* stream);
+int64_t sattn_tshard_margin(void);
+sattn_status sattn_dist_unique_id(void* id_out /* 128 bytes (ncclUniqueId), host */);
+sattn_status sattn_dist_init(int rank, int world, const void* nccl_unique_id, sattn_dist** out);
+sattn_status sattn_dist_init_external(int rank, int world, sattn_exchange_fn fn, void* user, sattn_dist** out);
+void sattn_dist_destroy(sattn_dist* d);
+/* device workspace (bytes) for either call below; 0 if the configuration is invalid */
+size_t sa_tsharded_workspace(const sattn_tshard_desc* td, const sattn_dist* d);
+sattn_status sa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,
+                                 float* LSE, void* ws, size_t ws_bytes, void* stream);
+sattn_status sa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
+                                  const void* V, const float* LSE, void* dO, void* dQ, void* dK, void* dV,
+                                  void* ws, size_t ws_bytes, void* stream);
+/* host-only: out6 = {hl, hr, slab frames, query tiles, first interior tile, first right-edge tile} */
+sattn_status sattn_tshard_geometry(const sattn_tshard_desc* td, int rank, int world, int64_t* out6);
 
 /* ---------------- misc ---------------------------------------------------------*/
 const char* sattn_last_error(void);      /* thread-local message of the last failure */

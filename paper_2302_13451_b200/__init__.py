@@ -15,7 +15,7 @@ import torch
 
 __all__ = [
     "SattnError", "lib", "sa_forward", "sa_backward", "sa_forward_p", "sa_backward_p", "llsa_forward", "llsa_backward",
-    "stack_forward", "stack_backward", "LLSAStream", "SAFunction", "LLSAFunction", "launch_count",
+    "stack_forward", "stack_backward", "stack_saved_views", "LLSAStream", "SAFunction", "LLSAFunction", "launch_count",
     "MODE_SA", "MODE_LLSA", "IMPL_AUTO", "IMPL_FFMA", "IMPL_TC",
 ]
 
@@ -54,6 +54,7 @@ EXPORTS = {
     "llsa_backward_workspace": (_SZ, [_PD]),
     "llsa_backward": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sattn_stack_saved_bytes": (_SZ, [_PD, _I, _I]),
+    "sattn_stack_saved_offsets": (_I, [_PD, _I, _I, _I, ctypes.POINTER(ctypes.c_int64)]),
     "sattn_stack_forward": (_I, [_PD, _I, _I, _P, _P, _SZ, _P, _P]),
     "sattn_stack_workspace": (_SZ, [_PD, _I, _I]),
     "sattn_stack_backward": (_I, [_PD, _I, _I, _P, _P, _P, _P, _SZ, _P]),
@@ -255,6 +256,24 @@ def stack_forward(x0, L: int, R: int, n_layers: int, mode: int = MODE_SA, scale=
     _check(lib().sattn_stack_forward(ctypes.byref(d), mode, n_layers, _ptr(x0), _ptr(saved), nb, _ptr(y), _stream()),
            "sattn_stack_forward")
     return y, saved
+
+
+def stack_saved_views(x0_like, saved, L: int, R: int, n_layers: int, mode: int = MODE_SA, scale=None, impl="auto"):
+    """Per-layer views into stack_forward's `saved` buffer: [(X_l, O_l, LSE_l)] for l < n_layers."""
+    d = _desc_from(x0_like, L, R, scale, impl)
+    B, H, T, D = x0_like.shape
+    C = R + 1 if mode == MODE_LLSA else 1
+    es = x0_like.element_size()
+    out = []
+    for layer in range(n_layers):
+        off = (ctypes.c_int64 * 3)()
+        _check(lib().sattn_stack_saved_offsets(ctypes.byref(d), mode, n_layers, layer, off), "sattn_stack_saved_offsets")
+        xs = (B, H, T, D) if (layer == 0 or C == 1) else (C, B, H, T, D)
+        os_ = (C, B, H, T, D) if C > 1 else (B, H, T, D)
+        view = lambda o, shp, dt, e: saved[o:o + e * int(torch.tensor(shp).prod())].view(dt).view(shp)  # noqa: E731
+        out.append((view(off[0], xs, x0_like.dtype, es), view(off[1], os_, x0_like.dtype, es),
+                    view(off[2], os_[:-1], torch.float32, 4)))
+    return out
 
 
 def stack_backward(x0_like, saved, dy, L: int, R: int, n_layers: int, mode: int = MODE_SA, scale=None, impl="auto",

@@ -53,6 +53,11 @@ struct AttnArgs {
   int T, L, R, BH;
   float scale, scale_log2;
   long long in_cs, out_cs;
+  // time-shard launches (tensor-core SA only; 0 = defaults): row stride ld (frames) of the
+  // [BH][ld][D] tensors and [BH][ld] LSE when it differs from T, and a query-tile subset
+  // (see TcArgs in tc_sa.cu)
+  int ld;
+  int nkt, kt0, kt_split, kt_jump;
 };
 
 template <int D> struct Smem {

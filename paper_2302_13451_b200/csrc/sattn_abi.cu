@@ -288,6 +288,14 @@ StackLayout stack_layout(const sattn_desc* d, int mode, int n) {
 
 }  // namespace
 
+// internal hooks for the other translation units (tshard.cu); declared in internal.h
+namespace sattn {
+sattn_status set_error(sattn_status st, const char* msg) { return fail(st, "%s", msg); }
+sattn_status check_desc(const sattn_desc* d) { return validate(d); }
+void count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+float desc_scale(const sattn_desc* d) { return eff_scale(d); }
+}  // namespace sattn
+
 extern "C" {
 
 const char* sattn_last_error(void) { return g_err.c_str(); }
@@ -382,6 +390,19 @@ sattn_status sa_backward_p(const sattn_desc* d, const void* Q, const void* K, co
     return SATTN_OK;
   }
   return ffma_backward_p(d, a, (cudaStream_t)stream);
+}
+
+sattn_status sattn_stack_saved_offsets(const sattn_desc* d, int mode, int n_layers, int layer, int64_t* out3) {
+  sattn_status r = validate(d);
+  if (r != SATTN_OK) return r;
+  if (!out3) return fail(SATTN_EARG, "out is NULL");
+  if (n_layers < 1 || layer < 0 || layer >= n_layers || (mode != SATTN_MODE_SA && mode != SATTN_MODE_LLSA))
+    return fail(SATTN_EARG, "bad mode / n_layers / layer");
+  const StackLayout s = stack_layout(d, mode, n_layers);
+  out3[0] = (int64_t)s.off_x(layer);
+  out3[1] = (int64_t)s.off_o(layer);
+  out3[2] = (int64_t)s.off_lse(layer);
+  return SATTN_OK;
 }
 
 size_t sattn_stack_saved_bytes(const sattn_desc* d, int mode, int n_layers) {

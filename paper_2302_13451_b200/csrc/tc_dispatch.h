@@ -10,7 +10,10 @@ struct AttnArgs;
 bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward);
 sattn_status tc_forward(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
+// phase bit 0: K1 (dQ, delta) over the args' query-tile subset; bit 1: K2 (dK, dV) over every tile
+sattn_status tc_backward_phase(const AttnArgs& a, cudaStream_t st, int phase);
 int tc_backward_launches();
+int tc_key_box_rows(int L, int R);   // rows of the K / V box a query tile loads (NK)
 size_t tc_backward_ws_bytes();
 bool tc_p_supported(int dtype, int D, int L, int R, bool backward);   // stored-band mode (NEXT-4)
 sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st);

@@ -69,7 +69,17 @@ struct TcArgs {
   int nch;                                       // K1: channels in one launch (LLSA band pass: C; SA: 1)
   int bcast;                                     // K1: Q is one plane read as every channel (LLSA layer 1)
   int ldp;                                       // stored-band mode: row stride of P [BH][T][ldp] (bf16)
+  int ld;                                        // row stride (frames) of the caller's [BH][ld] LSE rows and
+                                                 // [BH][ld][64] tensors (= T, or the margined length of a
+                                                 // time shard, whose maps start at a row offset)
+  // query tiles of this launch per head: kt = kt0 + i + (i >= kt_split ? kt_jump : 0), i < nkt
+  // (all tiles: kt0 = 0, nkt = ceil(T/128); a time shard launches interior and edge tiles apart)
+  int nkt, kt0, kt_split, kt_jump;
 };
+
+__device__ __forceinline__ int tile_t0(int i, const TcArgs& a) {
+  return (a.kt0 + i + (i >= a.kt_split ? a.kt_jump : 0)) * 128;
+}
 
 __device__ __forceinline__ void trace_at(long long* tr, int ev, int k) {
   if (tr && blockIdx.x == 0 && k < 64) tr[ev * 64 + k] = clock64();
@@ -217,7 +227,7 @@ __global__ void __launch_bounds__(320, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
-  const int ntq = (T + kM - 1) / kM;
+  const int ntq = a.nkt;
   const int ntiles = ntq * a.BH;
   const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   trace_cta(a.trace, 0);
@@ -248,7 +258,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       for (int k = 0; k < ntile_me; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / ntq, t0 = (g % ntq) * kM;
+        const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
         const int st = k % NQK;
         if (k >= NQK) tc::mbar_wait(&empty[st], ((k - NQK) / NQK) & 1);
         uint8_t* sQ = qk0 + st * C::QKB;
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(320, 1)
     uint8_t* pstage = ostage;
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
-      const int bh = g / ntq, t0 = (g % ntq) * kM;
+      const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
       const int t = t0 + r;
       const int b = wg;
       const int use = k >> 1;
@@ -373,7 +383,7 @@ __global__ void __launch_bounds__(320, 1)
       tmem_row64_to_smem_sw128(pa + NK, 1.f / l, ostage, r);
       tc::tc_fence_before();
       tc::mbar_arrive(&tfree[b]);
-      if (t < T) a.LSE[(long long)bh * T + t] = m * a.scale + __log2f(l) * kLn2;
+      if (t < T) a.LSE[(long long)bh * a.ld + t] = m * a.scale + __log2f(l) * kLn2;
       tc::fence_proxy_async_smem();
       tc::named_bar(1 + wg, 128);
       if (leader) {
@@ -459,7 +469,7 @@ __global__ void __launch_bounds__(320, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
-  const int ntq = (T + kM - 1) / kM;
+  const int ntq = a.nkt;
   // tiles: (channel c, head bh, query tile) with c slowest; SA has one channel.  LLSA runs every
   // channel's band pass in one launch: channel c's queries see channel-R keys shifted by R - c.
   const int nch = a.nch > 0 ? a.nch : 1;
@@ -491,7 +501,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int k = 0; k < ntile_me; ++k) {
         const int g0 = blockIdx.x + k * gridDim.x;
         const int c = g0 / tpc, g = g0 % tpc;
-        const int bh = g / ntq, t0 = (g % ntq) * kM;
+        const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
         const int ksh = a.kshift - c;                    // LLSA: R - c (a.kshift = R); SA: 0
         const int st = k % NS;
         uint8_t* b0 = stage0 + st * C::STAGE;
@@ -587,21 +597,21 @@ __global__ void __launch_bounds__(320, 1)
       if (k >= ntile_me || !src) return 0.f;
       const int g0 = blockIdx.x + k * gridDim.x;
       const int c = g0 / tpc, g = g0 % tpc;
-      const int t = (g % ntq) * kM + r;
+      const int t = tile_t0(g % ntq, a) + r;
       return t < T ? src[((long long)c * a.BH + g / ntq) * stride + t] * mul : 0.f;
     };
-    float lse_next = PST ? 0.f : row_of(wg, a.LSEin, T, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
+    float lse_next = PST ? 0.f : row_of(wg, a.LSEin, a.ld, kLog2e), dx_next = row_of(wg, a.ws_dx, a.Tp, 1.f);
     for (int k = wg; k < ntile_me; k += 2) {
       const int g0 = blockIdx.x + k * gridDim.x;
       const int c = g0 / tpc, g = g0 % tpc;
-      const int bh = g / ntq, t0 = (g % ntq) * kM;
+      const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
       const int ksh = a.kshift - c;
       const long long cbh = (long long)c * a.BH + bh;    // row of the [C][BH][Tp] workspaces
       const int t = t0 + r;
       const bool row_ok = t < T;
       const int b = wg, use = k >> 1;
       const float lse2 = lse_next, dx = dx_next;
-      if (!PST) lse_next = row_of(k + 2, a.LSEin, T, kLog2e);
+      if (!PST) lse_next = row_of(k + 2, a.LSEin, a.ld, kLog2e);
       dx_next = row_of(k + 2, a.ws_dx, a.Tp, 1.f);
       const uint32_t x = tbase + lanes + b * 256;
       float p[CW];
@@ -1751,9 +1761,9 @@ static_assert(DqCfg<72>::STAGE % 1024 == 0 && DkvCfg<72>::STAGE % 1024 == 0 && F
 // [BH][T][64] bf16 viewed as a 3-D tensor (64, T, BH); box (64, rows, 1), 128B swizzle.
 CUtensorMapL2promotion l2_promo() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
-bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows) {
+bool make_map(CUtensorMap* m, const void* base, int T, int BH, int rows, int ld = 0) {
   cuuint64_t dims[3] = {64, (cuuint64_t)T, (cuuint64_t)BH};
-  cuuint64_t strides[2] = {64 * 2, (cuuint64_t)T * 64 * 2};
+  cuuint64_t strides[2] = {64 * 2, (cuuint64_t)(ld > 0 ? ld : T) * 64 * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)rows, 1};
   CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo());
   if (r != CUDA_SUCCESS) {
@@ -1843,6 +1853,13 @@ TcArgs tc_args(const AttnArgs& a) {
   t.ws_del = a.delta;
   t.ws_l2 = a.delta + (long long)a.BH * t.Tp;
   t.ldp = a.ldp;
+  t.ld = a.ld > 0 ? a.ld : a.T;
+  const int ntq = (a.T + kM - 1) / kM;
+  if (a.nkt > 0) {
+    t.nkt = a.nkt; t.kt0 = a.kt0; t.kt_split = a.kt_split; t.kt_jump = a.kt_jump;
+  } else {
+    t.nkt = ntq; t.kt0 = 0; t.kt_split = ntq; t.kt_jump = 0;
+  }
   return t;
 }
 
@@ -1862,19 +1879,21 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
   using C = FwdCfg<CW, PST>;
   TcArgs ta = tc_args(a);
   CUtensorMap mq, mk, mv, mo, mp;
-  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, C::NK) ||
-      !make_map(&mv, a.V, a.T, a.BH, C::NK) || !make_map(&mo, a.Out, a.T, a.BH, kM))
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM, a.ld) || !make_map(&mk, a.K, a.T, a.BH, C::NK, a.ld) ||
+      !make_map(&mv, a.V, a.T, a.BH, C::NK, a.ld) || !make_map(&mo, a.Out, a.T, a.BH, kM, a.ld))
     return SATTN_ECUDA;
   if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
   set_smem(sa_fwd_tc<CW, PST>, C::SMEM);
-  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int ntiles = ta.nkt * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
   launch_pdl(sa_fwd_tc<CW, PST>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, PST ? mp : mo, ta);
   return SATTN_OK;
 }
 
+// phase: bit 0 = K1 (over the launch's query tiles, tc_args), bit 1 = K2 (every key tile).  A time
+// shard runs K1 on its interior tiles during the halo exchange, then K1 on the edge tiles and K2.
 template <int CW>
-sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
+sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st, int phase = 3) {
   constexpr int NK = nk_of(CW);
   const int Tp = (a.T + 3) & ~3;
   const float* l2ws = a.delta + (long long)a.BH * Tp;
@@ -1882,20 +1901,26 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st) {
   // kernel with the column-split warpgroups (its registers hold half a row)
   constexpr bool wide = DkvCfg<CW>::SMEM > 232448;
   constexpr int NQP = wide ? DkvRCfg<CW>::NQP : DkvCfg<CW>::NQP;
+  const int ld = a.ld;
   CUtensorMap mq, mk, mv, mdo, mdq, mqN, mdoN, mk128, mv128, mdk, mdv, ml2, mdel;
-  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
-      !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
-      !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
-      !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
-      !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
-      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NQP) ||
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM, ld) || !make_map(&mk, a.K, a.T, a.BH, NK, ld) ||
+      !make_map(&mv, a.V, a.T, a.BH, NK, ld) || !make_map(&mdo, a.dO, a.T, a.BH, kM, ld) ||
+      !make_map(&mdq, a.dQ, a.T, a.BH, kM, ld) || !make_map(&mqN, a.Q, a.T, a.BH, NK, ld) ||
+      !make_map(&mdoN, a.dO, a.T, a.BH, NK, ld) || !make_map(&mk128, a.K, a.T, a.BH, kM, ld) ||
+      !make_map(&mv128, a.V, a.T, a.BH, kM, ld) || !make_map(&mdk, a.dK, a.T, a.BH, kM, ld) ||
+      !make_map(&mdv, a.dV, a.T, a.BH, kM, ld) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NQP) ||
       !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, NQP))
     return SATTN_ECUDA;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  set_smem(sa_bwd_dq_tc<CW>, DqCfg<CW>::SMEM);
-  launch_pdl(sa_bwd_dq_tc<CW>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv, mdo, mdq,
-             tc_args(a));
+  if (phase & 1) {
+    const TcArgs t1 = tc_args(a);
+    const int nt1 = t1.nkt * a.BH;
+    set_smem(sa_bwd_dq_tc<CW>, DqCfg<CW>::SMEM);
+    launch_pdl(sa_bwd_dq_tc<CW>, dim3(nt1 < num_sms() ? nt1 : num_sms()), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM,
+               st, mq, mk, mv, mdo, mdq, t1);
+  }
+  if (!(phase & 2)) return SATTN_OK;
   if constexpr (wide) {
     set_smem(sa_bwd_dkdv_ring_tc<CW, true>, DkvRCfg<CW>::SMEM);
     launch_pdl(sa_bwd_dkdv_ring_tc<CW, true>, dim3(grid), dim3(DkvRCfg<CW>::THREADS), DkvRCfg<CW>::SMEM, st, mq,
@@ -2016,20 +2041,23 @@ sattn_status tc_forward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) {
+sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) { return tc_backward_phase(a, st, 3); }
+
+sattn_status tc_backward_phase(const AttnArgs& a, cudaStream_t st, int phase) {
   switch (cw_of(a.L + a.R + 1)) {
-    case 32: return bwd_launch<32>(a, st);
-    case 48: return bwd_launch<48>(a, st);
-    case 64: return bwd_launch<64>(a, st);
-    case 72: return bwd_launch<72>(a, st);
-    case 80: return bwd_launch<80>(a, st);
-    case 96: return bwd_launch<96>(a, st);
+    case 32: return bwd_launch<32>(a, st, phase);
+    case 48: return bwd_launch<48>(a, st, phase);
+    case 64: return bwd_launch<64>(a, st, phase);
+    case 72: return bwd_launch<72>(a, st, phase);
+    case 80: return bwd_launch<80>(a, st, phase);
+    case 96: return bwd_launch<96>(a, st, phase);
   }
   g_tc_err = "band too wide for the tensor-core kernels";
   return SATTN_EUNSUPPORTED;
 }
 
 int tc_backward_launches() { return 2; }
+int tc_key_box_rows(int L, int R) { const int cw = cw_of(L + R + 1); return cw > 0 ? nk_of(cw) : -1; }
 
 // ---- stored-band mode (NEXT-4): forward W <= 64 (P staging rows fit the O tile), backward
 // W <= 49 (the P window replaces K in the two-stage K2 stage; for W > 41 with one dV/dK

@@ -1,26 +1,15 @@
-"""Time sharding of SA over ranks: the hour-long-stream partition.
+"""Time sharding over ranks: partition helpers and the deep-halo stack.
 
-Rank r of P owns frames [t0, t1) of every (b, h) (contiguous, rank order; see
-shard_bounds).  Eq. 4's window makes output t depend on keys/values in
-[t-L, t+R] only, and Eq. 7/13's gathers make dK_u, dV_u depend on queries in
-[u-R, u+L] only (reading G3), so one exchange of boundary frames with the two
-neighbours per call is exact:
+The per-layer time-sharded SA call is in the C ABI (``sa_forward_tsharded`` /
+``sa_backward_tsharded``, include/sattn.h; Python binding ``paper_2302_13451_b200.dist``):
+the library packs, exchanges (NCCL or a callback) and unpacks the halo rows and overlaps
+the exchange with the interior tiles.  This module keeps
 
-    forward   K, V (and Q, to keep tile alignment) halo: L frames from the left
-              neighbour, R frames from the right
-    backward  Q, K, V, O, dO, LSE halo of L + R frames on both sides: halo queries
-              n in [t0 - R, t0) feed local dK/dV, and the tensor-core K1 computes their
-              delta = rowsum(P o dP) over their whole window [n - L, n + R], which reaches
-              t0 - R - L (reading G26), so the halo must hold it
-
-The exchange is point-to-point (torch.distributed batch_isend_irecv: NCCL over
-NVLink between GPUs, gloo on CPU for the tests).  The attention runs on the
-halo-extended local slab through the C ABI and only the local rows are kept.
-Halo widths are rounded up to `align` frames (default 128 = the tensor-core tile)
-when every shard is long enough, so each local frame sits at the same tile offset
-as in the unsharded call: with deterministic kernels the sharded result is then
-bitwise equal to the unsharded one.  `attn_fwd` / `attn_bwd` default to the CUDA
-path; tests inject the CPU oracle to check the host-side exchange on gloo.
+* ``shard_bounds``: rank r's frames [t0, t1), 128-frame aligned so that every local frame
+  keeps its tile offset (the sharded rows are then bitwise equal to the unsharded call's);
+* the deep-halo variant (NEXT-4): a whole n-layer stack on a time shard with ONE exchange
+  of n x (L + R) frames (``exchange_halo`` over torch.distributed point-to-point), traded
+  against recomputing the halo frames in every layer.
 """
 from __future__ import annotations
 
@@ -82,46 +71,6 @@ def _halo(width: int, align: int, T_loc: int, group) -> int:
         raise ValueError(f"shards of {min_T} frames cannot supply a {width}-frame halo: use fewer ranks")
     r = _round_up(width, align) if width else 0
     return r if r <= min_T else width
-
-
-def _default_fwd(q, k, v, L, R):
-    import paper_2302_13451_b200 as s
-    return s.sa_forward(q, k, v, L, R)
-
-
-def _default_bwd(q, k, v, o, lse, do, L, R):
-    import paper_2302_13451_b200 as s
-    return s.sa_backward(q, k, v, o, lse, do, L, R)
-
-
-def sa_forward_tsharded(q, k, v, L: int, R: int, group=None, align: int = 128, attn_fwd=None):
-    """q, k, v: this rank's slabs [B, H, T_loc, D].  Returns the local (o, lse): the rows
-    [t0, t1) of the unsharded sa_forward."""
-    attn_fwd = attn_fwd or _default_fwd
-    T_loc = q.shape[-2]
-    hl, hr = _halo(L, align, T_loc, group), _halo(R, align, T_loc, group)
-    q_e, nl = exchange_halo(q, hl, hr, group)
-    k_e, _ = exchange_halo(k, hl, hr, group)
-    v_e, _ = exchange_halo(v, hl, hr, group)
-    o, lse = attn_fwd(q_e, k_e, v_e, L, R)
-    return o[..., nl:nl + T_loc, :].contiguous(), lse[..., nl:nl + T_loc].contiguous()
-
-
-def sa_backward_tsharded(q, k, v, o, lse, do, L: int, R: int, group=None, align: int = 128, attn_bwd=None):
-    """Local (dq, dk, dv) [B, H, T_loc, D]: the rows [t0, t1) of the unsharded sa_backward.
-    o, lse are this rank's rows of the forward."""
-    attn_bwd = attn_bwd or _default_bwd
-    T_loc = q.shape[-2]
-    h = _halo(L + R, align, T_loc, group)
-    q_e, nl = exchange_halo(q, h, h, group)
-    k_e, _ = exchange_halo(k, h, h, group)
-    v_e, _ = exchange_halo(v, h, h, group)
-    o_e, _ = exchange_halo(o, h, h, group)
-    do_e, _ = exchange_halo(do, h, h, group)
-    lse_e, _ = exchange_halo(lse.unsqueeze(-1).contiguous(), h, h, group)
-    dq, dk, dv = attn_bwd(q_e, k_e, v_e, o_e, lse_e.squeeze(-1).contiguous(), do_e, L, R)
-    sl = slice(nl, nl + T_loc)
-    return dq[..., sl, :].contiguous(), dk[..., sl, :].contiguous(), dv[..., sl, :].contiguous()
 
 
 # ------------------------------------------------------------------ deep halo (NEXT-4)
