@@ -12,9 +12,14 @@ A "frame" is one time step of one sequence carried through all heads and layers,
 forward and backward: frames/step = B*T.  The same step with LLSA (C = R+1 = 9
 channels per frame) is reported under "llsa".
 
-Multi-GPU (torchrun, one rank per GPU): batch x head sharding is embarrassingly
-parallel - every rank runs its own B=8 batch, no data-path
-collective; scaling "weak"; value = frames of all ranks / max-over-ranks time.
+Multi-GPU (one rank per GPU; `--gpus N` re-executes itself under torch.distributed.run when
+it is not already a rank, and fails loudly if fewer than N GPUs are visible): batch x head
+sharding is embarrassingly parallel - the headline has every rank run its own
+B=8 batch, no data-path collective ("weak"); value = frames of all ranks / max-over-ranks
+time.  Sub-objects: "llsa" = M2, the LLSA step with the B*H = 96 (b, h) units split over the
+ranks (strong scaling); "large" = M3, wav2vec2-large (B=64, H=16, 24 layers) batch-sharded
+(strong); "hour" = M4, one hour-long stream time-sharded through the library's NCCL halo
+exchange (sa_forward_tsharded / sa_backward_tsharded, strong).
 
 --impl reference runs the CPU oracle (oracle/, numpy fp64) on a bounded sample of
 the same workload (the task's reference arm for this paper-only reference).
@@ -108,8 +113,15 @@ def run_gpu(args):
 
     world, rank, local = dist_setup()
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        t = torch.ones(1, device=torch.device("cuda", local))
+        dist.all_reduce(t)
+        comm = {"backend": "nccl", "nranks": dist.get_world_size(), "all_reduce_check": int(t.item()),
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version())}
+        print(f"[bench] rank {rank}: NCCL communicator up, nranks={comm['nranks']} (all_reduce of ones = "
+              f"{comm['all_reduce_check']}), NCCL {comm['nccl_version']}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     bf = torch.bfloat16
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -255,7 +267,7 @@ def run_gpu(args):
             for j, src in enumerate((Qs, Ks, Vs, dOs)):
                 hin[l][j].copy_(src[l])
         # H2D on copy stream(s) (layers alternate when more than one), D2H on another
-        n_in = int(os.environ.get("SATTN_E2E_H2D_STREAMS", "1"))   # 2-3 measured no faster (PCIe-bound)
+        n_in = 1   # 2-3 H2D copy streams measured no faster (PCIe-bound)
         s_ins = [torch.cuda.Stream(dev) for _ in range(n_in)]
         s_out = torch.cuda.Stream(dev)
         ev = lambda: torch.cuda.Event()  # noqa: E731
@@ -325,7 +337,10 @@ def run_gpu(args):
     if not args.no_llsa:
         del Qs, Ks, Vs, dOs, Os, dQs, dKs, dVs
         torch.cuda.empty_cache()
-        llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
+        try:
+            llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
+        except Exception as e:
+            llsa = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     alt = None   # the other SA mode, same workload
     if not args.no_alt:
@@ -334,6 +349,22 @@ def run_gpu(args):
             alt = run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, "lse" if band else "band")
         except Exception as e:
             alt = {"error": f"{type(e).__name__}: {e}"[:300]}
+
+    large = None
+    if not args.no_large:
+        torch.cuda.empty_cache()
+        try:
+            large = run_large(args, sattn, dev, rnd, barrier, world, stream, hbm)
+        except Exception as e:
+            large = {"error": f"{type(e).__name__}: {e}"[:300]}
+
+    fa2 = None
+    if not args.no_fa2 and world == 1:
+        torch.cuda.empty_cache()
+        try:
+            fa2 = run_fa2(args, dev, rnd)
+        except Exception as e:
+            fa2 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     hour = None
     if not args.no_hour:
@@ -374,17 +405,38 @@ def run_gpu(args):
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
            "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, ("lse_mode" if band else "band_mode"): alt,
-           "hour": hour, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
+           "large": large, "hour": hour, "fa2_local_context": fa2, "comm": comm, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
 
 
+def _strong_batch(Btot, world):
+    """Per-rank batch of a batch-sharded strong-scaling config (Btot sequences over the ranks)."""
+    if Btot % world:
+        raise ValueError(f"batch {Btot} does not split over {world} ranks")
+    return Btot // world
+
+
+def _max_ms(ms, world, dev):
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+    tt = torch.tensor([ms], device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
 def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
+    """M2 (BASELINE configs[2]): the 12-layer LLSA step (C = R+1 = 9 channels) at the base shape with
+    the B*H = 96 (b, h) units split over the ranks - strong scaling (B/N sequences per rank, every
+    rank all H heads); value = B*T frames / max-over-ranks step time."""
     import ctypes
     import torch
     lib = sattn.lib()
     C = R + 1
-    shp = (C, B, H, T, D)
+    Br = _strong_batch(B, world)
+    shp = (C, Br, H, T, D)
     bf = torch.bfloat16
     n_layers = NL
     Q, K, V, dO = ([rnd(*shp) for _ in range(n_layers)] for _ in range(4))
@@ -392,39 +444,152 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
     LSE = [torch.empty(shp[:-1], device=dev, dtype=torch.float32) for _ in range(n_layers)]
     dQ, dK, dV = torch.empty(shp, device=dev, dtype=bf), torch.empty(shp, device=dev, dtype=bf), \
         torch.empty(shp, device=dev, dtype=bf)
-    desc = sattn.make_desc(B, H, T, D, L, R, sattn.BF16, impl=args.kernels)
+    desc = sattn.make_desc(Br, H, T, D, L, R, sattn.BF16, impl=args.kernels)
     pd = ctypes.byref(desc)
     nws = lib.llsa_backward_workspace(pd)
     ws = torch.empty(nws, device=dev, dtype=torch.uint8)
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-    def step():
+
+    def fwd():
         for l in range(n_layers):
             assert lib.llsa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]),
                                     ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+
+    def bwd():
         for l in reversed(range(n_layers)):
             assert lib.llsa_backward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(dO[l]), P(dQ), P(dK),
                                      P(dV), P(ws), nws, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
 
-    step()
+    fwd(); bwd()
     torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=torch.cuda.Stream()):
-        step()
+    cap = torch.cuda.Stream(dev)
+    gF, gB = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gF, stream=cap):
+        fwd()
+    with torch.cuda.graph(gB, stream=cap):
+        bwd()
     for _ in range(max(1, args.warmup)):
-        g.replay()
+        gF.replay(); gB.replay()
     barrier()
     k = max(1, min(args.steps, 5))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k + 1)]
+    evs[0].record(stream)
+    for i in range(k):
+        gF.replay(); evs[2 * i + 1].record(stream)
+        gB.replay(); evs[2 * i + 2].record(stream)
+    barrier()
+    f_ms = sum(evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(k)) / k
+    b_ms = sum(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]) for i in range(k)) / k
+    ms = _max_ms(f_ms + b_ms, world, dev)
+    units = C * Br * H * T
+    return {"value": round(B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "scaling": "strong",
+            "channels": C, "steps": k, "bh_units_per_rank": Br * H,
+            "hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * n_layers / ((f_ms + b_ms) / 1e3) / 1e9 / hbm, 4),
+            "per_call_ms": {"llsa_forward": round(f_ms / n_layers, 4), "llsa_backward": round(b_ms / n_layers, 4)},
+            "hbm_frac_per_call": {"llsa_forward": round(FWD_BYTES * units / (f_ms / n_layers / 1e3) / 1e9 / hbm, 4),
+                                  "llsa_backward": round(BWD_BYTES * units / (b_ms / n_layers / 1e3) / 1e9 / hbm, 4)},
+            "workload": f"M2: 12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs, B*H = {B * H} "
+                        f"(b,h) units split over {world} rank(s) ({Br * H} per rank)"}
+
+
+def run_large(args, sattn, dev, rnd, barrier, world, stream, hbm):
+    """M3 (BASELINE configs[3]): wav2vec2-large attention core, B=64, H=16, T=1750, D=64, 24 layers
+    (reading G22), SA fwd + bwd in the headline mode, batch-sharded over the ranks (strong scaling:
+    64/N sequences per rank); value = 64*T frames / max-over-ranks step time."""
+    import ctypes
+    import torch
+    lib = sattn.lib()
+    Bl, Hl, nl = 64, 16, 24
+    Br = _strong_batch(Bl, world)
+    shp = (Br, Hl, T, D)
+    bf = torch.bfloat16
+    band = args.mode == "band"
+    desc = sattn.make_desc(Br, Hl, T, D, L, R, sattn.BF16, impl=args.kernels)
+    pd = ctypes.byref(desc)
+    ld = int(lib.sa_p_ld(pd))
+    Q, K, V, dO = ([rnd(*shp) for _ in range(nl)] for _ in range(4))
+    O = [torch.empty(shp, device=dev, dtype=bf) for _ in range(nl)]
+    LSE = [torch.empty(shp[:-1], device=dev, dtype=torch.float32) for _ in range(nl)]
+    Pb = [torch.empty(shp[:-1] + (ld,), device=dev, dtype=bf) for _ in range(nl)] if band else LSE
+    dQ, dK, dV = (torch.empty(shp, device=dev, dtype=bf) for _ in range(3))
+    nws = lib.sa_backward_p_workspace(pd) if band else lib.sa_backward_workspace(pd)
+    ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    sp = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)  # noqa: E731
+
+    def fwd():
+        for l in range(nl):
+            st = (lib.sa_forward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(Pb[l]), sp()) if band else
+                  lib.sa_forward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), sp()))
+            assert st == 0, lib.sattn_last_error()
+
+    def bwd():
+        for l in reversed(range(nl)):
+            st = (lib.sa_backward_p(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(Pb[l]), P(dO[l]), P(dQ), P(dK), P(dV),
+                                    P(ws), nws, sp()) if band else
+                  lib.sa_backward(pd, P(Q[l]), P(K[l]), P(V[l]), P(O[l]), P(LSE[l]), P(dO[l]), P(dQ), P(dK), P(dV),
+                                  P(ws), nws, sp()))
+            assert st == 0, lib.sattn_last_error()
+
+    fwd(); bwd()
+    torch.cuda.synchronize()
+    cap = torch.cuda.Stream(dev)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        fwd(); bwd()
+    for _ in range(max(1, min(args.warmup, 3))):
+        g.replay()
+    barrier()
+    k = max(1, min(args.steps, 3))
     a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
     a0.record(stream)
     for _ in range(k):
         g.replay()
     a1.record(stream)
     barrier()
+    ms_loc = a0.elapsed_time(a1) / k
+    ms = _max_ms(ms_loc, world, dev)
+    W = L + R + 1
+    fb, bb = (FWD_BYTES + 2 * W, 896 + 2 * W) if band else (FWD_BYTES, BWD_BYTES)
+    units = Br * Hl * T
+    return {"value": round(Bl * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "scaling": "strong",
+            "steps": k, "per_layer_ms": round(ms / nl, 4),
+            "hbm_frac": round((fb + bb) * units * nl / (ms_loc / 1e3) / 1e9 / hbm, 4),
+            "workload": f"M3: wav2vec2-large attention core B={Bl}, H={Hl}, T={T}, {nl} layers x (SA fwd + bwd, "
+                        f"{'stored band' if band else 'LSE'} mode), batch-sharded over {world} rank(s) ({Br} "
+                        f"sequences per rank)"}
+
+
+def run_fa2(args, dev, rnd):
+    """Context only: FlashAttention-2's local attention
+    (flash_attn_func(..., window_size=(L, R)), a library kernel) fwd + bwd on the headline
+    workload (12 distinct layers, [B, T, H, D] bf16), next to the repo's per-layer times."""
+    import torch
+    from flash_attn import flash_attn_func
+    shp = (B, T, H, D)
+    qs = [[rnd(*shp).requires_grad_(True) for _ in range(3)] for _ in range(NL)]
+    dos = [rnd(*shp) for _ in range(NL)]
+
+    def step():
+        outs = [flash_attn_func(q, k, v, window_size=(L, R)) for q, k, v in qs]
+        for o, do in zip(reversed(outs), reversed(dos)):
+            o.backward(do)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    k = 3
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(k):
+        step()
+    a1.record()
+    torch.cuda.synchronize()
     ms = a0.elapsed_time(a1) / k
-    bytes_step = (FWD_BYTES + BWD_BYTES) * C * B * H * T * n_layers
-    return {"value": round(world * B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
-            "channels": C, "hbm_frac": round(bytes_step / (ms / 1e3) / 1e9 / hbm, 4), "steps": k,
-            "workload": "12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs"}
+    return {"value": round(B * T / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3),
+            "per_layer_fwd_bwd_ms": round(ms / NL, 4),
+            "workload": f"flash_attn {__import__('flash_attn').__version__} flash_attn_func window_size=({L},{R}) "
+                        f"fwd+bwd, 12 layers, B={B}, T={T}, H={H}, D={D}, bf16, eager autograd (context only)"}
 
 
 def run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, mode):
@@ -506,64 +671,80 @@ def run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, mode):
 
 
 def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
-    """BASELINE configs[4]: one hour-long stream (B=1, H=12, T=180,000 frames = 1 h at 50 Hz),
-    12 layers x (SA fwd + SA bwd), bf16, time-sharded over the ranks: rank r owns
-    frames [r T/N, (r+1) T/N) and every call exchanges the L+R boundary frames with its two
-    neighbours (tshard: NCCL point-to-point over NVLink), so the whole-job rate counts each frame
-    once.  At N = 1 the calls run on the whole sequence with no exchange."""
+    """M4 (BASELINE configs[4]): one hour-long stream (B=1, H=12, T=180,000 frames = 1 h at 50 Hz),
+    12 layers x (SA fwd + SA bwd), bf16, time-sharded over the ranks through the library
+    (sa_forward_tsharded / sa_backward_tsharded on margined shards: rank r owns frames [t0, t1),
+    128-aligned; each call exchanges the halo rows with its neighbours over NCCL on a library
+    stream while the interior tiles run).  At N = 1 the same calls run with no neighbours.
+    Strong scaling: value = T frames / max-over-ranks step time."""
+    import ctypes
     import torch
-    import torch.distributed as dist
+    from paper_2302_13451_b200 import dist as sd
     from paper_2302_13451_b200 import tshard
     Th, Bh, n_layers = 180_000, 1, NL
     t0, t1 = tshard.shard_bounds(Th, world, rank, 128)
-    shp = (Bh, H, t1 - t0, D)
-    Q, K, V, dO = ([rnd(*shp) for _ in range(n_layers)] for _ in range(4))
-    O, LSE = [None] * n_layers, [None] * n_layers
-    ws = [None]
-
-    def fwd(l):
-        if world == 1:
-            O[l], LSE[l] = sattn.sa_forward(Q[l], K[l], V[l], L, R)
-        else:
-            O[l], LSE[l] = tshard.sa_forward_tsharded(Q[l], K[l], V[l], L, R)
-
-    def bwd(l):
-        if world == 1:
-            return sattn.sa_backward(Q[l], K[l], V[l], O[l], LSE[l], dO[l], L, R, ws=ws[0])
-        return tshard.sa_backward_tsharded(Q[l], K[l], V[l], O[l], LSE[l], dO[l], L, R)
-
-    import ctypes
-    ws[0] = torch.empty(sattn.lib().sa_backward_workspace(ctypes.byref(sattn.make_desc(Bh, H, t1 - t0, D, L, R,
-                                                                                        sattn.BF16))),
-                        device=dev, dtype=torch.uint8)
+    n = t1 - t0
+    d = sd.Dist()
+    L_ = sd._lib()
+    td = sd.tdesc(Bh, H, n, D, L, R, t0, Th)
+    tdp = ctypes.byref(td)
+    nws = int(L_.sa_tsharded_workspace(tdp, d._h))
+    if nws == 0:
+        raise RuntimeError(L_.sattn_last_error().decode())
+    ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    Qm, Km, Vm, dOm = ([sd.margined(Bh, H, n, D, device=dev) for _ in range(n_layers)] for _ in range(4))
+    for bufs in (Qm, Km, Vm, dOm):
+        for m in bufs:
+            sd.local(m, n).copy_(rnd(Bh, H, n, D))
+    Om = [sd.margined(Bh, H, n, D, device=dev) for _ in range(n_layers)]
+    LSEm = [sd.margined(Bh, H, n, None, dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    dQm, dKm, dVm = (sd.margined(Bh, H, n, D, device=dev) for _ in range(3))
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def step():
+        sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         for l in range(n_layers):
-            fwd(l)
+            st = L_.sa_forward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(Om[l]), P(LSEm[l]), P(ws), nws, sp)
+            assert st == 0, L_.sattn_last_error()
         for l in reversed(range(n_layers)):
-            bwd(l)
+            st = L_.sa_backward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(LSEm[l]), P(dOm[l]), P(dQm),
+                                         P(dKm), P(dVm), P(ws), nws, sp)
+            assert st == 0, L_.sattn_last_error()
 
-    for _ in range(max(1, min(args.warmup, 2))):
-        step()
+    step()
+    torch.cuda.synchronize()
+    graph = None
+    try:   # NCCL point-to-point and the library's fork/join streams are capturable
+        cap = torch.cuda.Stream(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            step()
+        graph = g
+    except Exception:
+        torch.cuda.synchronize()
+        graph = None
+    run = graph.replay if graph is not None else step
+    for _ in range(max(1, min(args.warmup, 3))):
+        run()
     barrier()
-    k = max(1, min(args.steps, 3))
+    k = max(1, min(args.steps, 5))
     a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
     a0.record(stream)
     for _ in range(k):
-        step()
+        run()
     a1.record(stream)
     barrier()
-    ms = a0.elapsed_time(a1) / k
-    if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    bytes_step = (FWD_BYTES + BWD_BYTES) * Bh * H * Th * n_layers
+    ms_loc = a0.elapsed_time(a1) / k
+    ms = _max_ms(ms_loc, world, dev)
+    d.close()
+    units = Bh * H * n
     return {"value": round(Bh * Th / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": k,
-            "hbm_frac": round(bytes_step / world / (ms / 1e3) / 1e9 / hbm, 4),
-            "workload": f"hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), {n_layers} layers x (SA fwd + bwd), "
-                        f"time-sharded x{world} (halo exchange {'NCCL P2P' if world > 1 else 'none'}), eager calls",
-            "frames_per_rank": t1 - t0}
+            "scaling": "strong", "hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * n_layers / (ms_loc / 1e3) / 1e9 / hbm, 4),
+            "workload": f"M4: hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), {n_layers} layers x (SA fwd + bwd) "
+                        f"through sa_forward_tsharded / sa_backward_tsharded, time-sharded x{world} "
+                        f"({'NCCL halo exchange overlapped with interior tiles' if world > 1 else 'no neighbours'}), "
+                        f"{'CUDA graph' if graph is not None else 'eager'}",
+            "frames_per_rank": n, "halo_exchange": "nccl" if world > 1 else None}
 
 
 def run_encoder(args, dev):
@@ -762,9 +943,26 @@ def main():
     ap.add_argument("--mode", default="band", choices=["band", "lse"],
                     help="headline SA mode: stored band a_t (paper P:L342) or LSE + recompute")
     ap.add_argument("--no-encoder", action="store_true")
+    ap.add_argument("--no-large", action="store_true")
+    ap.add_argument("--no-fa2", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    elif args.gpus > 1:
+        # not a rank yet: launch one rank per GPU (the driver's own torchrun command is equivalent)
+        if args.impl == "ours":
+            import torch
+            n = torch.cuda.device_count()
+            if n < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} requested but only {n} CUDA device(s) are visible")
+        import socket
+        so = socket.socket(); so.bind(("127.0.0.1", 0)); port = so.getsockname()[1]; so.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:
