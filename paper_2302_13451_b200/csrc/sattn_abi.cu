@@ -174,7 +174,7 @@ sattn_status ffma_backward_p(const sattn_desc* d, const AttnArgs& a, cudaStream_
 
 bool tc_ok(const sattn_desc* d, bool llsa, bool backward) {
   if (llsa)
-    return backward ? tc_llsa_bwd_supported(d->dtype, (int)d->D, d->L, d->R)
+    return backward ? tc_llsa_bwd_any_supported(d->dtype, (int)d->D, d->L, d->R, d->B * d->H, d->T, !d->in_broadcast)
                     : tc_llsa_supported(d->dtype, (int)d->D, d->L, d->R);
   return tc_supported(d->dtype, (int)d->D, d->L, d->R, false, backward);
 }
@@ -221,7 +221,7 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
   if (ws_bytes < attn_bwd_ws(d, llsa))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
   if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true))
-    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA backward needs bf16, D=64, 1 <= R <= 8, L <= 48"
+    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA backward needs bf16, D=64, L <= 48 and 1 <= R <= 8 (R <= 16 for dense inputs)"
                                          : "tensor-core SA backward needs bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
@@ -229,7 +229,7 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
   if (use_tc(d, llsa, true)) {
     sattn_status r = llsa ? tc_llsa_backward(a, st) : tc_backward(a, st);
     if (r != SATTN_OK) return fail(r, "tc_backward: %s", tc_last_error());
-    g_launches.fetch_add(llsa ? tc_llsa_backward_launches(d->R) : tc_backward_launches(), std::memory_order_relaxed);
+    g_launches.fetch_add(llsa ? tc_llsa_backward_launches(a) : tc_backward_launches(), std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_backward launch: %s", cudaGetErrorString(e));
     return SATTN_OK;

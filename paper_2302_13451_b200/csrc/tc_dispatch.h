@@ -26,5 +26,8 @@ sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st);
 const char* tc_llsa_last_error();
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R);
 sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st);
-int tc_llsa_backward_launches(int R);
+int tc_llsa_backward_launches(const AttnArgs& a);
+bool tc_llsa_bwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
+bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, cudaStream_t st);
 }  // namespace sattn

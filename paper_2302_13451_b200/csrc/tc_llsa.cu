@@ -25,6 +25,7 @@
 #include "tc_dispatch.h"
 #include "tc_ptx.cuh"
 #include "host_util.h"
+#include "llsa_stair.cuh"
 
 namespace sattn {
 namespace {
@@ -370,6 +371,432 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// LLSA backward, fused horizon-major pass (dense inputs).  Exact gradient of the
+// forward above (Eq. 14-16 in the horizon form, reading G8/G9), everything except the band
+// keys' dK / dV (channel R, which gather from L+1 horizons and are the key-major llsa_bwd_kv_tc):
+//
+// Item = HZ horizons x all C channels of one (b, h): row r = c HZ + i <-> output (t, c),
+// t = h0 + i - c (so the C rows of a horizon, and therefore every query of its staircase
+// keys, sit in one item).  Per item, with TMEM buffer b (256 columns) and stage b:
+//   MMA  S   = Q Kb^T -> X_b[0, NB)              WG  stair scores / dP on CUDA cores (FFMA2)
+//                                                     P = exp2(S sl2 - LSE log2e) (band + stair)
+//   MMA  dP  = dO Vb^T -> X_b[0, NB)             WG  delta = rowsum(P o dP) over band + stair (G26,
+//                                                     complete: no pre-pass), dS = P (dP - delta);
+//                                                     dS_band -> X_b (packed bf16 A operand);
+//                                                     dS_stair, P_stair -> DS, PS (smem, sparse)
+//   MMA  dQ  = [dS_band | DS] [Kb ; Ks]   -> X_b[NB, NB+64)     (complete: one rounding)
+//        dKs = DS^T Q  (A MN-major)        -> X_b[NB+64, NB+128) (staircase keys: complete)
+//        dVs = PS^T dO                     -> X_b[NB+128, NB+192)
+//                                             WG  epilogue: dQ, dK_stair, dV_stair rows -> global;
+//                                                 delta, LSE log2e rows -> workspace (llsa_bwd_kv_tc)
+// DS / PS are [2 K-atoms][128 rows][128 B] K-major SW128 tiles: row r holds its R staircase
+// entries at columns c' HZ + i (fixed per row), every other entry stays zero from the start.
+// Warp roles as in the forward: TMA producer, MMA issuer, two warpgroups alternating items.
+// ------------------------------------------------------------------------------------------
+struct LlsaBwdArgs {
+  int T, L, R, C, BH, HZ, Tp;
+  float scale, scale_log2;
+  const float* LSE;              // [C][BH][T]
+  bf16 *dQ, *dK, *dV;            // [C][BH][T][64]
+  float *ws_del, *ws_l2;         // [C][BH][Tp]
+};
+
+template <int NB, int RM> struct LBCfg {
+  static constexpr int QB = 128 * 128;             // Q / dO item tiles
+  static constexpr int KBB = NB * 128;             // band K / V tiles
+  static constexpr int SB = 112 * 128;             // stair K / V tiles (rows c' HZ + i, R HZ <= 112)
+  static constexpr int STAGE = 2 * QB + 2 * KBB + 2 * SB;
+  static constexpr int XB = 2 * 128 * 128;         // DS / PS
+  // staircase scores / dP on mma.sync (one 16 x 8 block per horizon) through a per-warpgroup fp32
+  // scratch [2][128][8], when it fits; otherwise packed-FFMA2 dot products
+  static constexpr bool SMMA = RM == 8 && 1024 + 2 * STAGE + 2 * XB + 2 * 2 * 128 * 8 * 4 + 128 + 256 <= 232448;
+  static constexpr int SCR = SMMA ? 2 * 128 * 8 * 4 : 0;   // per warpgroup
+  static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
+  static_assert(NB + 192 <= 256, "TMEM columns per item");
+  static_assert(SMEM <= 232448, "shared memory");
+};
+
+// byte address of element (row r, column k) of a [2][128][128 B] K-major SW128 tile
+__device__ __forceinline__ uint32_t xs_addr(uint32_t base, int r, int k) {
+  const int e = k & 63;
+  return base + (k >> 6) * 16384 + r * 128 + ((((e >> 3) ^ (r & 7))) << 4) + (e & 7) * 2;
+}
+
+__device__ __forceinline__ void tmem_ld64_l(uint32_t addr, float* v) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tc::tmem_ld16(addr + 16 * j, v + 16 * j);
+  tc::tmem_ld_wait();
+}
+// 64 fp32 -> bf16 (x sc) -> 128 contiguous bytes in global memory
+__device__ __forceinline__ void store_row64(bf16* dst, const float* v, float sc) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int ch = 0; ch < 8; ++ch)
+    d[ch] = make_uint4(pack_bf16(v[8 * ch] * sc, v[8 * ch + 1] * sc), pack_bf16(v[8 * ch + 2] * sc, v[8 * ch + 3] * sc),
+                       pack_bf16(v[8 * ch + 4] * sc, v[8 * ch + 5] * sc), pack_bf16(v[8 * ch + 6] * sc, v[8 * ch + 7] * sc));
+}
+
+template <int NB, int RM>
+__global__ void __launch_bounds__(320, 1)
+    llsa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
+                      const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
+                      const __grid_constant__ CUtensorMap tmKs, const __grid_constant__ CUtensorMap tmVs,
+                      LlsaBwdArgs a) {
+  using Cf = LBCfg<NB, RM>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage0 = smem;                                    // [Q | dO | Kb | Vb | Ks | Vs] x 2
+  uint8_t* xds = smem + 2 * Cf::STAGE;                       // DS
+  uint8_t* xps = xds + Cf::XB;                               // PS
+  uint8_t* scr0 = xps + Cf::XB;                              // stair S / dP scratch x 2 warpgroups
+  uint8_t* zrow = scr0 + 2 * Cf::SCR;                        // 128 zero bytes (ldmatrix padding rows)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zrow + 128);
+  uint64_t* full = bars;           // [2]
+  uint64_t* empty = full + 2;      // [2]
+  uint64_t* sfull = empty + 2;     // [2]
+  uint64_t* xfree = sfull + 2;     // [2] (128)
+  uint64_t* dpfull = xfree + 2;    // [2]
+  uint64_t* dsfull = dpfull + 2;   // [2] (128)
+  uint64_t* done = dsfull + 2;     // [2]
+  uint64_t* tfree = done + 2;      // [2] (128)
+  uint64_t* xsfree = tfree + 2;    // [1] DS / PS read by the item's MMAs
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xsfree + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, L = a.L, R = a.R, C = a.C, HZ = a.HZ;
+  const int nit = (T + R + HZ - 1) / HZ;                     // horizons 0 .. T-1+R per (b, h)
+  const int nitems = nit * a.BH;
+  const int nme = blockIdx.x < nitems ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int qbytes = C * HZ * 128, sbytes = R * HZ * 128;
+
+  // zero the operand tiles once: padding rows / columns that TMA and the warpgroups never write
+  for (int o = tid * 16; o < 2 * Cf::STAGE + 2 * Cf::XB + 2 * Cf::SCR + 128; o += 320 * 16)
+    *reinterpret_cast<uint4*>(smem + o) = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmKb);
+    tc::tma_prefetch_desc(&tmVb); tc::tma_prefetch_desc(&tmKs); tc::tma_prefetch_desc(&tmVs);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
+      tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&done[i], 1); tc::mbar_init(&tfree[i], 128);
+    }
+    tc::mbar_init(xsfree, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int k = 0; k < nme; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int s = k & 1;
+        if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
+        uint8_t* sb = stage0 + s * Cf::STAGE;
+        tc::mbar_expect_tx(&full[s], 2 * qbytes + 2 * Cf::KBB + 2 * sbytes);
+        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);                         // rows (h0+i-c, c)
+        tc::tma_load_4d(sb + Cf::QB, &tmdO, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb + 2 * Cf::QB, &tmKb, &full[s], 0, h0 - R - L, bh, R);   // band keys (u, R)
+        tc::tma_load_4d(sb + 2 * Cf::QB + Cf::KBB, &tmVb, &full[s], 0, h0 - R - L, bh, R);
+        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, h0, 0, bh);   // (h0+i-c', c')
+        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, h0, 0, bh);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nme > 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, NB, 0, 0);
+      constexpr uint32_t idQ = tc::idesc_bf16(128, kD, 0, 1);
+      constexpr uint32_t idK = tc::idesc_bf16(128, kD, 1, 1);
+      const int nks = (R * HZ + 15) / 16;                    // 16-key steps over the stair keys
+      int ns = 0, ndp = 0, ng = 0;
+      while (ng < nme) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&dsfull[ng & 1]), (ng >> 1) & 1,
+                                          tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
+                                          tc::smem_u32(&full[ns & 1]), (ns >> 1) & 1,
+                                          tc::smem_u32(&tfree[ns & 1]), ((ns + 2) >> 1) & 1);
+        if (ng < ndp && (m & 1)) {   // dQ, dK_stair, dV_stair of item ng
+          tc::tc_fence_after();
+          const int b = ng & 1;
+          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t q = sb, dO = sb + Cf::QB, kb = sb + 2 * Cf::QB, ks = kb + 2 * Cf::KBB;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t ds = tc::smem_u32(xds), ps = tc::smem_u32(xps);
+#pragma unroll
+          for (int j = 0; j < NB / 16; ++j)
+            tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(kb + 2048 * j), idQ, j > 0);
+          for (int j = 0; j < nks; ++j)
+            tc::mma_bf16(x + NB, tc::desc_kmajor_sw128(ds + (j >> 2) * 16384 + (j & 3) * 32),
+                         tc::desc_mnmajor_sw128(ks + 2048 * j), idQ, 1);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
+                         idK, j > 0);
+            tc::mma_bf16(x + NB + 128, tc::sdesc(ps + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(dO + 2048 * j),
+                         idK, j > 0);
+          }
+          tc::mma_commit(&done[b]);
+          tc::mma_commit(&empty[b]);
+          tc::mma_commit(xsfree);
+          ++ng;
+          continue;
+        }
+        if (ndp < ns && (m & 2)) {   // dP_band of item ndp (S consumed)
+          tc::tc_fence_after();
+          const int b = ndp & 1;
+          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t dO = sb + Cf::QB, vb = sb + 2 * Cf::QB + Cf::KBB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(vb + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&dpfull[b]);
+          ++ndp;
+          continue;
+        }
+        if (ns < nme && ns < ng + 2 && (m & 4) && (ns < 2 || (m & 8))) {   // S_band of item ns
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t q = sb, kb = sb + 2 * Cf::QB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kb + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&sfull[b]);
+          ++ns;
+          continue;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const int c = r / HZ, i = r - c * HZ;                  // output channel / horizon offset of row r
+    const bool in_item = c < C;
+    const uint32_t xdsa = tc::smem_u32(xds), xpsa = tc::smem_u32(xps);
+    // this row's LSE of item k (loaded one item ahead: the global load's latency is off the chain)
+    auto lse_of = [&](int k) -> float {
+      if (k >= nme || !in_item) return 0.f;
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / nit, t = (g % nit) * HZ + i - c;
+      return (t >= 0 && t < T) ? a.LSE[((long long)c * a.BH + bh) * T + t] : 0.f;
+    };
+    float lse_next = lse_of(wg);
+    uint8_t* scr = scr0 + wg * Cf::SCR;                       // [S | dP][128 rows][8] fp32
+    const int wq = warp & 3;                                  // warp within the warpgroup
+    for (int k = wg; k < nme; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / nit, h0 = (g % nit) * HZ;
+      const int b = wg, use = k >> 1;
+      const int h = h0 + i, t = h - c;
+      const bool row_ok = in_item && t >= 0 && t < T;
+      const long long crow = ((long long)c * a.BH + bh);
+      const float lse2 = lse_next * kLog2e;
+      lse_next = lse_of(k + 2);
+      const uint8_t* sbp = stage0 + b * Cf::STAGE;
+      const uint32_t sb = tc::smem_u32(sbp);
+      tc::mbar_wait(&full[b], use & 1);
+      float sst[RM], dst[RM];
+      if constexpr (Cf::SMMA) {
+        // ---- staircase on mma.sync: horizon ih's block S = Q_ih K_ih^T, dP = dO_ih V_ih^T
+        //      (rows c: Q rows c HZ + ih; cols c': stair rows c' HZ + ih), one warp per horizon,
+        //      scattered to the scratch rows r = c HZ + ih, then read back per thread
+        const uint32_t qt = sb, ot = sb + Cf::QB, ks = sb + 2 * Cf::QB + 2 * Cf::KBB, vs = ks + Cf::SB;
+        const uint32_t za = tc::smem_u32(zrow), sca = tc::smem_u32(scr);
+        const int gq = lane >> 2, t4 = lane & 3;
+        for (int ih = wq; ih < HZ; ih += 4) {
+          float sacc[4] = {0.f, 0.f, 0.f, 0.f}, dacc[4] = {0.f, 0.f, 0.f, 0.f};
+          const int am = lane & 15, bn = lane & 7;
+          const int arow = am < C ? am * HZ + ih : -1, brow = bn < R ? bn * HZ + ih : -1;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
+            const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
+            const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
+            uint32_t aq[4], ad[4], bk[2], bv[2];
+            ldsm_x4(arow < 0 ? za : qt + ao, aq);
+            ldsm_x4(arow < 0 ? za : ot + ao, ad);
+            ldsm_x2(brow < 0 ? za : ks + bo, bk);
+            ldsm_x2(brow < 0 ? za : vs + bo, bv);
+            mma16816(sacc, aq, bk);
+            mma16816(dacc, ad, bv);
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
+            if (cc < C) {
+              const uint32_t o = (uint32_t)((cc * HZ + ih) * 8 + cp) * 4;
+              tc::st_shared_u32(sca + o, __float_as_uint(sacc[e]));
+              tc::st_shared_u32(sca + 4096 + o, __float_as_uint(dacc[e]));
+            }
+          }
+        }
+        tc::named_bar(1 + wg, 128);
+        {
+          const uint32_t o = sca + (uint32_t)r * 32;
+          const uint4 s0 = tc::ld_shared_v4(o), s1 = tc::ld_shared_v4(o + 16);
+          const uint4 d0 = tc::ld_shared_v4(o + 4096), d1 = tc::ld_shared_v4(o + 4096 + 16);
+          const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          const uint32_t dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+          for (int cp = 0; cp < RM; ++cp) {
+            const int f = h - cp;
+            const bool ok = row_ok && cp < R && f >= 0 && f < T;
+            sst[cp] = ok ? tc::ex2(fmaf(__uint_as_float(sv[cp]), a.scale_log2, -lse2)) : 0.f;
+            dst[cp] = __uint_as_float(dv[cp]);
+          }
+        }
+        tc::named_bar(1 + wg, 128);   // the scratch is rewritten by this warpgroup's next item
+      } else {
+      // ---- staircase scores and dP on CUDA cores: key (h - c', c') = stair row c' HZ + i; two
+      //      passes (q . k_stair, then dO . v_stair) so one 64-float row is live at a time
+      {
+        const uint32_t ks = sb + 2 * Cf::QB + 2 * Cf::KBB, vs = ks + Cf::SB;
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+          float2 q2[kD / 2];
+          const uint32_t qrow = sb + pass * Cf::QB + r * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const uint4 x = tc::ld_shared_v4(qrow + ((ch ^ (r & 7)) << 4));
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              q2[4 * ch + e] = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+          }
+#pragma unroll
+          for (int cp = 0; cp < RM; ++cp) {
+            float2 acc = make_float2(0.f, 0.f);
+            if (cp < R) {
+              const int m = cp * HZ + i;
+              const uint32_t krow = (pass ? vs : ks) + m * 128;
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) {
+                const uint4 x = tc::ld_shared_v4(krow + ((ch ^ (m & 7)) << 4));
+                const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  acc = __ffma2_rn(q2[4 * ch + e],
+                                   make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u)), acc);
+              }
+            }
+            if (pass == 0) {
+              const int f = h - cp;
+              const bool ok = row_ok && cp < R && f >= 0 && f < T;
+              sst[cp] = ok ? tc::ex2(fmaf(acc.x + acc.y, a.scale_log2, -lse2)) : 0.f;   // P of the stair slot
+            } else {
+              dst[cp] = acc.x + acc.y;
+            }
+          }
+        }
+      }
+      }
+      // ---- band P from S
+      tc::mbar_wait(&sfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float p[NB];
+      const uint32_t x = tbase + lanes + b * 256;
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j) tc::tmem_ld8(x + 8 * j, p + 8 * j);
+      tc::tmem_ld_wait();
+      {
+        const int key0 = h0 - R - L;                       // frame of band column 0
+        const int jlo = max(i, -key0), jhi = min(i + L, T - 1 - key0);
+#pragma unroll
+        for (int j = 0; j < NB; ++j)
+          p[j] = (row_ok && j >= jlo && j <= jhi) ? tc::ex2(fmaf(p[j], a.scale_log2, -lse2)) : 0.f;
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&xfree[b]);
+      // ---- dP, delta, dS
+      tc::mbar_wait(&dpfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      // dP is read from TMEM twice (delta, then dS) instead of being held next to P
+      float delta = 0.f;
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) delta = fmaf(p[8 * j + e], dp[e], delta);
+      }
+#pragma unroll
+      for (int cp = 0; cp < RM; ++cp) delta = fmaf(sst[cp], dst[cp], delta);
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j) {
+        float dp[8];
+        tc::tmem_ld8(x + 8 * j, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 8; ++e) p[8 * j + e] *= dp[e] - delta;   // dS_band
+      }
+      // dS_band -> X_b columns [0, NB/2) as the packed bf16 A operand of the dQ MMA
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j)
+        tc::tmem_st4(x + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
+                     pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
+      // staircase dS / P -> DS / PS (row r, columns c' HZ + i); the previous item's MMAs must have
+      // read them (one buffer shared by both warpgroups)
+      if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
+      if (in_item) {
+#pragma unroll
+        for (int cp = 0; cp < RM; ++cp) {
+          if (cp < R) {
+            const float ds = sst[cp] * (dst[cp] - delta);
+            tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
+            tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
+          }
+        }
+      }
+      tc::tmem_st_wait();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&dsfull[b]);
+      // workspace rows for the key-major band pass (padded rows [T, Tp) zero)
+      if (row_ok) {
+        a.ws_del[crow * a.Tp + t] = delta;
+        a.ws_l2[crow * a.Tp + t] = lse2;
+        if (t == T - 1)
+          for (int tt = T; tt < a.Tp; ++tt) { a.ws_del[crow * a.Tp + tt] = 0.f; a.ws_l2[crow * a.Tp + tt] = 0.f; }
+      }
+      // ---- epilogue: dQ row (t, c); staircase key rows m = r: (u, c'), u = h0 + i' - c'
+      tc::mbar_wait(&done[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      {
+        float v[kD];
+        tmem_ld64_l(x + NB, v);
+        if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
+        const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
+        const bool key_ok = cq < R && u >= 0 && u < T;
+        const long long krow = ((long long)cq * a.BH + bh) * T + u;
+        tmem_ld64_l(x + NB + 64, v);
+        if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
+        tmem_ld64_l(x + NB + 128, v);
+        if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
 // host
 // ------------------------------------------------------------------------------------------
 // [C][BH][T][64] bf16 as a 4-D tensor (64, T, BH, C); box (64, rows, 1, 1); 128B swizzle.
@@ -453,6 +880,54 @@ sattn_status launch(const AttnArgs& a, cudaStream_t st) {
   return SATTN_OK;
 }
 
+// horizons per fused-backward item: all C channels of HZ horizons in <= 128 rows, and the band
+// window of the item (HZ + L keys) in NB <= 64 TMEM columns
+int fused_hz(int L, int R) {
+  const int C = R + 1;
+  int hz = 128 / C;
+  if (hz > 64 - L) hz = 64 - L;
+  if (R * hz > 112) hz = 112 / R;   // the stair tiles hold R HZ <= 112 rows
+  return hz;
+}
+
+template <int NB, int RM>
+sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, cudaStream_t st) {
+  using Cf = LBCfg<NB, RM>;
+  const int R = a.R, C = R + 1;
+  CUtensorMap mq, mdo, mkb, mvb, mks, mvs;
+  if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map_skew(&mdo, a.dO, a.T, a.BH, C, R, HZ, C) ||
+      !map4(&mkb, a.K, a.T, a.BH, C, NB) || !map4(&mvb, a.V, a.T, a.BH, C, NB) ||
+      !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) || !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R)) {
+    g_err = "tensor maps of the fused LLSA backward";
+    return SATTN_ECUDA;
+  }
+  LlsaBwdArgs la{};
+  la.T = a.T; la.L = a.L; la.R = R; la.C = C; la.BH = a.BH; la.HZ = HZ; la.Tp = (a.T + 3) & ~3;
+  la.scale = a.scale; la.scale_log2 = a.scale_log2;
+  la.LSE = a.LSE;
+  la.dQ = reinterpret_cast<bf16*>(a.dQ); la.dK = reinterpret_cast<bf16*>(a.dK); la.dV = reinterpret_cast<bf16*>(a.dV);
+  la.ws_del = ws_del; la.ws_l2 = ws_l2;
+  const int items = (a.T + R + HZ - 1) / HZ * a.BH;
+  const int grid = items < num_sms() ? items : num_sms();
+  set_smem(llsa_bwd_fused_tc<NB, RM>, Cf::SMEM);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM>, mq, mdo, mkb, mvb, mks, mvs, la);
+  if (e != cudaSuccess) {
+    g_err = std::string("fused LLSA backward launch: ") + cudaGetErrorString(e);
+    return SATTN_ECUDA;
+  }
+  return SATTN_OK;
+}
+
 }  // namespace
 
 bool tc_llsa_supported(int dtype, int D, int L, int R) {
@@ -468,6 +943,28 @@ sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
     case 64: return launch<64>(a, st);
   }
   g_err = "band too wide for the LLSA tensor-core kernel";
+  return SATTN_EUNSUPPORTED;
+}
+
+// fused horizon-major LLSA backward (dense inputs): dQ, staircase dK / dV, delta and LSE log2e
+// rows; the band keys' dK / dV are llsa_bwd_kv_tc's (tc_sa.cu)
+bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense) {
+  if (dtype != SATTN_BF16 || D != 64 || !dense || R < 1 || R > 16 || L < 0) return false;
+  const int hz = fused_hz(L, R);
+  return hz >= 4 && BH * T - 1 >= T + R;
+}
+
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, cudaStream_t st) {
+  const int HZ = fused_hz(a.L, a.R);
+  const int nb = (HZ + a.L + 15) / 16 * 16;
+  const bool r16 = a.R > 8;
+  switch (nb) {
+    case 16:
+    case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, st);
+    case 48: return r16 ? bwd_fused_launch<48, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<48, 8>(a, HZ, ws_del, ws_l2, st);
+    case 64: return r16 ? bwd_fused_launch<64, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<64, 8>(a, HZ, ws_del, ws_l2, st);
+  }
+  g_err = "band too wide for the fused LLSA backward";
   return SATTN_EUNSUPPORTED;
 }
 

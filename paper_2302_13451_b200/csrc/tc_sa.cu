@@ -1933,7 +1933,34 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st, int phase = 3) {
   return SATTN_OK;
 }
 
-// LLSA backward: band (channel-R keys) on the tensor-core kernels, staircase on CUDA cores.
+// LLSA key-major band pass: dK, dV of channel R's keys accumulated over the C query channels
+// (delta and LSE log2e rows from the workspace)
+template <int CW>
+sattn_status llsa_bwd_kv_launch(const AttnArgs& a, const bf16* Q, const bf16* dO, const bf16* Kr, const bf16* Vr,
+                                bf16* dK, bf16* dV, float* ws_del, float* ws_l2, cudaStream_t st) {
+  using LC = LkvCfg<CW>;
+  const int R = a.R, C = R + 1;
+  const bool bc = a.in_cs == 0;
+  const long long plane = (long long)a.BH * a.T * kD;
+  const int Tp = (a.T + 3) & ~3;
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  CUtensorMap mq4, mdo4, mk, mv, mdk, mdv, ml2, mdel;
+  if (!make_map4(&mq4, Q, a.T, a.BH, bc ? 1 : C, LC::NQ) || !make_map4(&mdo4, dO, a.T, a.BH, C, LC::NQ) ||
+      !make_map(&mk, Kr, a.T, a.BH, kM) || !make_map(&mv, Vr, a.T, a.BH, kM) ||
+      !make_map(&mdk, dK + plane * R, a.T, a.BH, kM) || !make_map(&mdv, dV + plane * R, a.T, a.BH, kM) ||
+      !make_map_f32_rows(&ml2, ws_l2, a.T, Tp, C * a.BH, LC::NQP) ||
+      !make_map_f32_rows(&mdel, ws_del, a.T, Tp, C * a.BH, LC::NQP))
+    return SATTN_ECUDA;
+  TcArgs t = tc_args(a);
+  set_smem(llsa_bwd_kv_tc<CW>, LC::SMEM);
+  launch_pdl(llsa_bwd_kv_tc<CW>, dim3(grid), dim3(320), LC::SMEM, st, mq4, mk, mv, mdo4, mdk, mdv, ml2, mdel, t, C,
+             bc ? 1 : 0);
+  return SATTN_OK;
+}
+
+// LLSA backward: band (channel-R keys) on the tensor-core kernels; the rest either in the fused
+// horizon-major pass (dense inputs) or, for a broadcast layer-1 input, staircase on mma.sync.
 template <int CW>
 sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   constexpr int NK = nk_of(CW);
@@ -1956,6 +1983,16 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   float* ws_dx = a.delta + 2LL * C * a.BH * Tp;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  if (tc_llsa_bwd_fused_supported(SATTN_BF16, kD, a.L, R, a.BH, a.T, !bc)) {
+    // fused horizon-major pass (tc_llsa.cu): dQ, staircase dK / dV, delta / LSE rows; then the
+    // key-major band pass below for channel R's dK / dV
+    sattn_status r = tc_llsa_bwd_fused(a, ws_del, ws_l2, st);
+    if (r != SATTN_OK) {
+      g_tc_err = tc_llsa_last_error();
+      return r;
+    }
+    return llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, st);
+  }
   StairArgs sa{};
   sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
   sa.dQ = dQ; sa.dK = dK; sa.dV = dV;
@@ -1996,17 +2033,8 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   }
   // (2) key-major band pass: dK, dV of channel R accumulated over the C query channels
   {
-    CUtensorMap mq4, mdo4, mk, mv, mdk, mdv, ml2, mdel;
-    if (!make_map4(&mq4, Q, a.T, a.BH, bc ? 1 : C, LC::NQ) || !make_map4(&mdo4, dO, a.T, a.BH, C, LC::NQ) ||
-        !make_map(&mk, Kr, a.T, a.BH, kM) || !make_map(&mv, Vr, a.T, a.BH, kM) ||
-        !make_map(&mdk, dK + plane * R, a.T, a.BH, kM) || !make_map(&mdv, dV + plane * R, a.T, a.BH, kM) ||
-        !make_map_f32_rows(&ml2, ws_l2, a.T, Tp, C * a.BH, LC::NQP) ||
-        !make_map_f32_rows(&mdel, ws_del, a.T, Tp, C * a.BH, LC::NQP))
-      return SATTN_ECUDA;
-    TcArgs t = tc_args(a);
-    set_smem(llsa_bwd_kv_tc<CW>, LC::SMEM);
-    launch_pdl(llsa_bwd_kv_tc<CW>, dim3(grid), dim3(320), LC::SMEM, st, mq4, mk, mv, mdo4, mdk, mdv, ml2, mdel, t, C,
-               bc ? 1 : 0);
+    const sattn_status r = llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, st);
+    if (r != SATTN_OK) return r;
   }
   // (3) staircase keys and the staircase part of dQ (mma.sync)
   {
@@ -2124,6 +2152,11 @@ bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {
   return dtype == SATTN_BF16 && D == 64 && R >= 1 && R <= 8 && L + 1 + 31 <= 80;
 }
 
+bool tc_llsa_bwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense) {
+  return tc_llsa_bwd_supported(dtype, D, L, R) ||
+         (L + 1 + 31 <= 80 && tc_llsa_bwd_fused_supported(dtype, D, L, R, BH, T, dense));
+}
+
 sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
   switch (cw_of(a.L + 1)) {
     case 32: return llsa_bwd_launch<32>(a, st);
@@ -2136,7 +2169,9 @@ sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
-int tc_llsa_backward_launches(int R) { (void)R; return 4; }
+int tc_llsa_backward_launches(const AttnArgs& a) {
+  return tc_llsa_bwd_fused_supported(SATTN_BF16, kD, a.L, a.R, a.BH, a.T, a.in_cs != 0) ? 2 : 4;
+}
 void tc_set_trace(void* p) { g_trace = static_cast<long long*>(p); }
 const char* tc_last_error() { return g_tc_err.c_str(); }
 
