@@ -476,7 +476,9 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmKb);
     tc::tma_prefetch_desc(&tmVb); tc::tma_prefetch_desc(&tmKs); tc::tma_prefetch_desc(&tmVs);
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1);
+      // SMMA: the warpgroup still reads Q / dO of the stage for its staircase dK / dV after the
+      // dQ MMAs complete, so its 128 threads also arrive before the stage is refilled
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], Cf::SMMA ? 129 : 1);
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&done[i], 1); tc::mbar_init(&tfree[i], 128);
     }
@@ -527,23 +529,26 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
           const uint32_t q = sb, dO = sb + Cf::QB, kb = sb + 2 * Cf::QB, ks = kb + 2 * Cf::KBB;
           const uint32_t x = tbase + b * 256;
-          const uint32_t ds = tc::smem_u32(xds), ps = tc::smem_u32(xps);
+          // SMMA: each warpgroup has its own DS (its staircase dK / dV are mma.sync in the WG)
+          const uint32_t ds = tc::smem_u32(Cf::SMMA ? xds + b * Cf::XB : xds), ps = tc::smem_u32(xps);
 #pragma unroll
           for (int j = 0; j < NB / 16; ++j)
             tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(kb + 2048 * j), idQ, j > 0);
           for (int j = 0; j < nks; ++j)
             tc::mma_bf16(x + NB, tc::desc_kmajor_sw128(ds + (j >> 2) * 16384 + (j & 3) * 32),
                          tc::desc_mnmajor_sw128(ks + 2048 * j), idQ, 1);
+          if constexpr (!Cf::SMMA) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
-                         idK, j > 0);
-            tc::mma_bf16(x + NB + 128, tc::sdesc(ps + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(dO + 2048 * j),
-                         idK, j > 0);
+            for (int j = 0; j < 8; ++j) {
+              tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
+                           idK, j > 0);
+              tc::mma_bf16(x + NB + 128, tc::sdesc(ps + 2048 * j, 16384, 1024, 2),
+                           tc::desc_mnmajor_sw128(dO + 2048 * j), idK, j > 0);
+            }
           }
           tc::mma_commit(&done[b]);
           tc::mma_commit(&empty[b]);
-          tc::mma_commit(xsfree);
+          if constexpr (!Cf::SMMA) tc::mma_commit(xsfree);
           ++ng;
           continue;
         }
@@ -747,16 +752,42 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < NB / 8; ++j)
         tc::tmem_st4(x + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
                      pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
-      // staircase dS / P -> DS / PS (row r, columns c' HZ + i); the previous item's MMAs must have
-      // read them (one buffer shared by both warpgroups)
-      if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
-      if (in_item) {
+      if constexpr (Cf::SMMA) {
+        // staircase dS -> this warpgroup's DS (row r, columns c' HZ + i; its previous item's dQ MMAs
+        // completed before that item's epilogue); dS and P of the staircase -> the scratch, for the
+        // per-horizon dK / dV below
+        const uint32_t dsa = tc::smem_u32(xds + wg * Cf::XB), sca = tc::smem_u32(scr);
+        if (in_item) {
 #pragma unroll
-        for (int cp = 0; cp < RM; ++cp) {
-          if (cp < R) {
-            const float ds = sst[cp] * (dst[cp] - delta);
-            tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
-            tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
+          for (int cp = 0; cp < RM; ++cp) {
+            if (cp < R) {
+              const float ds = sst[cp] * (dst[cp] - delta);
+              tc::st_shared_u16(xs_addr(dsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
+              dst[cp] = ds;
+            }
+          }
+          const uint32_t o = sca + (uint32_t)r * 32;
+          tc::st_shared_v4(o, make_uint4(__float_as_uint(dst[0]), __float_as_uint(dst[1]), __float_as_uint(dst[2]),
+                                         __float_as_uint(dst[3])));
+          tc::st_shared_v4(o + 16, make_uint4(__float_as_uint(dst[4]), __float_as_uint(dst[5]),
+                                              __float_as_uint(dst[6]), __float_as_uint(dst[7])));
+          tc::st_shared_v4(o + 4096, make_uint4(__float_as_uint(sst[0]), __float_as_uint(sst[1]),
+                                                __float_as_uint(sst[2]), __float_as_uint(sst[3])));
+          tc::st_shared_v4(o + 4096 + 16, make_uint4(__float_as_uint(sst[4]), __float_as_uint(sst[5]),
+                                                     __float_as_uint(sst[6]), __float_as_uint(sst[7])));
+        }
+      } else {
+        // staircase dS / P -> DS / PS (row r, columns c' HZ + i); the previous item's MMAs must have
+        // read them (one buffer shared by both warpgroups)
+        if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
+        if (in_item) {
+#pragma unroll
+          for (int cp = 0; cp < RM; ++cp) {
+            if (cp < R) {
+              const float ds = sst[cp] * (dst[cp] - delta);
+              tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
+              tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
+            }
           }
         }
       }
@@ -764,6 +795,49 @@ __global__ void __launch_bounds__(320, 1)
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       tc::mbar_arrive(&dsfull[b]);
+      if constexpr (Cf::SMMA) {
+        // ---- staircase dK / dV per horizon on mma.sync (while the dQ MMAs run):
+        //      dK_ih (keys c' x 64) = scale dS^T Q_ih,  dV_ih = P^T dO_ih   (K = the C channel rows)
+        tc::named_bar(1 + wg, 128);
+        const uint32_t qt = sb, ot = sb + Cf::QB, za = tc::smem_u32(zrow), sca = tc::smem_u32(scr);
+        const int gq = lane >> 2, t4 = lane & 3;
+        for (int ih = wq; ih < HZ; ih += 4) {
+          // A = dS^T / P^T: rows c' = gq (rows gq + 8 >= R are zero), columns c = 2 t4 (+1, +8, +9)
+          uint32_t ak[4] = {0u, 0u, 0u, 0u}, av[4] = {0u, 0u, 0u, 0u};
+          if (gq < R) {
+            float fk[4], fv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = 2 * t4 + (e & 1) + 8 * (e >> 1);
+              const uint32_t o = sca + (uint32_t)((cc * HZ + ih) * 8 + gq) * 4;
+              fk[e] = cc < C ? __uint_as_float(tc::ld_shared_u32(o)) : 0.f;
+              fv[e] = cc < C ? __uint_as_float(tc::ld_shared_u32(o + 4096)) : 0.f;
+            }
+            ak[0] = pack_bf16(fk[0], fk[1]); ak[2] = pack_bf16(fk[2], fk[3]);
+            av[0] = pack_bf16(fv[0], fv[1]); av[2] = pack_bf16(fv[2], fv[3]);
+          }
+          const int brow = (lane & 15) < C ? (lane & 15) * HZ + ih : -1;   // B rows: channel c = lane & 15
+          const int u = h0 + ih - gq;
+          const bool key_ok = gq < R && u >= 0 && u < T;
+          const long long krow = ((long long)gq * a.BH + bh) * T + u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((j ^ (brow & 7)) << 4));
+            uint32_t bq[2], bd[2];
+            ldsm_x2_t(brow < 0 ? za : qt + bo, bq);
+            ldsm_x2_t(brow < 0 ? za : ot + bo, bd);
+            float dk[4] = {0.f, 0.f, 0.f, 0.f}, dv[4] = {0.f, 0.f, 0.f, 0.f};
+            mma16816(dk, ak, bq);
+            mma16816(dv, av, bd);
+            if (key_ok) {
+              *reinterpret_cast<uint32_t*>(a.dK + krow * kD + 8 * j + 2 * t4) = pack_bf16(dk[0] * a.scale, dk[1] * a.scale);
+              *reinterpret_cast<uint32_t*>(a.dV + krow * kD + 8 * j + 2 * t4) = pack_bf16(dv[0], dv[1]);
+            }
+          }
+        }
+        tc::mbar_arrive(&empty[b]);    // this item's stage is no longer read by the warpgroup
+        tc::named_bar(1 + wg, 128);   // the scratch is rewritten by this warpgroup's next item
+      }
       // workspace rows for the key-major band pass (padded rows [T, Tp) zero)
       if (row_ok) {
         a.ws_del[crow * a.Tp + t] = delta;
@@ -779,13 +853,15 @@ __global__ void __launch_bounds__(320, 1)
         float v[kD];
         tmem_ld64_l(x + NB, v);
         if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
-        const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
-        const bool key_ok = cq < R && u >= 0 && u < T;
-        const long long krow = ((long long)cq * a.BH + bh) * T + u;
-        tmem_ld64_l(x + NB + 64, v);
-        if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
-        tmem_ld64_l(x + NB + 128, v);
-        if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
+        if constexpr (!Cf::SMMA) {
+          const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
+          const bool key_ok = cq < R && u >= 0 && u < T;
+          const long long krow = ((long long)cq * a.BH + bh) * T + u;
+          tmem_ld64_l(x + NB + 64, v);
+          if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
+          tmem_ld64_l(x + NB + 128, v);
+          if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
+        }
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&tfree[b]);
