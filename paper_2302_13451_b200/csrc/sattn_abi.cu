@@ -302,7 +302,7 @@ const char* sattn_last_error(void) { return g_err.c_str(); }
 const char* sattn_version(void) { return "sattn 0.1 (sm_100a)"; }
 int64_t sattn_launch_count(void) { return g_launches.load(); }
 // internal debug hook (not in sattn.h): device buffer of 8 x 64 int64 clock64 stamps of CTA 0
-void sattn_debug_trace(void* dev_buf) { tc_set_trace(dev_buf); }
+void sattn_debug_trace(void* dev_buf) { tc_set_trace(dev_buf); tc_llsa_set_trace(dev_buf); }
 
 sattn_status sa_forward(const sattn_desc* d, const void* Q, const void* K, const void* V, void* O, float* LSE,
                         void* stream) {

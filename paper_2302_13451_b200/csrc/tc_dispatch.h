@@ -24,6 +24,7 @@ void tc_set_trace(void* p);  // debug only
 bool tc_llsa_supported(int dtype, int D, int L, int R);
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st);
 const char* tc_llsa_last_error();
+void tc_llsa_set_trace(void* p);  // debug only
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R);
 sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st);
 int tc_llsa_backward_launches(const AttnArgs& a);

@@ -31,6 +31,7 @@ namespace sattn {
 namespace {
 
 thread_local std::string g_err;
+long long* g_llsa_trace = nullptr;   // debug: device buffer [16][64] for the fused backward's CTA 0
 constexpr int kD = 64;
 constexpr int kHT = 32;          // horizons per tile
 constexpr int kRmax = 8;
@@ -399,6 +400,7 @@ struct LlsaBwdArgs {
   const float* LSE;              // [C][BH][T]
   bf16 *dQ, *dK, *dV;            // [C][BH][T][64]
   float *ws_del, *ws_l2;         // [C][BH][Tp]
+  long long* trace;              // debug: per-item phase clock64 stamps of CTA 0 ([16][64]), or null
 };
 
 template <int NB, int RM> struct LBCfg {
@@ -427,6 +429,15 @@ __device__ __forceinline__ void tmem_ld64_l(uint32_t addr, float* v) {
   for (int j = 0; j < 4; ++j) tc::tmem_ld16(addr + 16 * j, v + 16 * j);
   tc::tmem_ld_wait();
 }
+// 64 fp32 values (x sc) -> bf16 row r of a 128-row x 128-byte smem tile with the 128B swizzle
+__device__ __forceinline__ void tmem_row64_to_smem_sw128_regs(const float* v, float sc, uint8_t* tile, int r) {
+  const uint32_t row = tc::smem_u32(tile) + r * 128;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    tc::st_shared_v4(row + ((c ^ (r & 7)) << 4),
+                     make_uint4(pack_bf16(v[8 * c] * sc, v[8 * c + 1] * sc), pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc),
+                                pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc), pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc)));
+}
 // 64 fp32 -> bf16 (x sc) -> 128 contiguous bytes in global memory
 __device__ __forceinline__ void store_row64(bf16* dst, const float* v, float sc) {
   uint4* d = reinterpret_cast<uint4*>(dst);
@@ -436,12 +447,13 @@ __device__ __forceinline__ void store_row64(bf16* dst, const float* v, float sc)
                        pack_bf16(v[8 * ch + 4] * sc, v[8 * ch + 5] * sc), pack_bf16(v[8 * ch + 6] * sc, v[8 * ch + 7] * sc));
 }
 
-template <int NB, int RM>
+template <int NB, int RM, bool KVH>
 __global__ void __launch_bounds__(320, 1)
     llsa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
                       const __grid_constant__ CUtensorMap tmKs, const __grid_constant__ CUtensorMap tmVs,
-                      LlsaBwdArgs a) {
+                      const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
+                      const __grid_constant__ CUtensorMap tmdV, LlsaBwdArgs a) {
   using Cf = LBCfg<NB, RM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -478,7 +490,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int i = 0; i < 2; ++i) {
       // SMMA: the warpgroup still reads Q / dO of the stage for its staircase dK / dV after the
       // dQ MMAs complete, so its 128 threads also arrive before the stage is refilled
-      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], Cf::SMMA ? 129 : 1);
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], KVH ? 129 : 1);
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&done[i], 1); tc::mbar_init(&tfree[i], 128);
     }
@@ -530,14 +542,14 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t q = sb, dO = sb + Cf::QB, kb = sb + 2 * Cf::QB, ks = kb + 2 * Cf::KBB;
           const uint32_t x = tbase + b * 256;
           // SMMA: each warpgroup has its own DS (its staircase dK / dV are mma.sync in the WG)
-          const uint32_t ds = tc::smem_u32(Cf::SMMA ? xds + b * Cf::XB : xds), ps = tc::smem_u32(xps);
+          const uint32_t ds = tc::smem_u32(KVH ? xds + b * Cf::XB : xds), ps = tc::smem_u32(xps);
 #pragma unroll
           for (int j = 0; j < NB / 16; ++j)
             tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(kb + 2048 * j), idQ, j > 0);
           for (int j = 0; j < nks; ++j)
             tc::mma_bf16(x + NB, tc::desc_kmajor_sw128(ds + (j >> 2) * 16384 + (j & 3) * 32),
                          tc::desc_mnmajor_sw128(ks + 2048 * j), idQ, 1);
-          if constexpr (!Cf::SMMA) {
+          if constexpr (!KVH) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
@@ -547,8 +559,8 @@ __global__ void __launch_bounds__(320, 1)
             }
           }
           tc::mma_commit(&done[b]);
-          tc::mma_commit(&empty[b]);
-          if constexpr (!Cf::SMMA) tc::mma_commit(xsfree);
+          if constexpr (KVH) tc::mma_commit(&empty[b]);   // !KVH: released by the epilogue's TMA stores
+          if constexpr (!KVH) tc::mma_commit(xsfree);
           ++ng;
           continue;
         }
@@ -609,7 +621,10 @@ __global__ void __launch_bounds__(320, 1)
       lse_next = lse_of(k + 2);
       const uint8_t* sbp = stage0 + b * Cf::STAGE;
       const uint32_t sb = tc::smem_u32(sbp);
+#define LTR(ev) do { if (a.trace && blockIdx.x == 0 && r == 0 && k < 64) a.trace[(ev) * 64 + k] = clock64(); } while (0)
+      LTR(0);
       tc::mbar_wait(&full[b], use & 1);
+      LTR(1);
       float sst[RM], dst[RM];
       if constexpr (Cf::SMMA) {
         // ---- staircase on mma.sync: horizon ih's block S = Q_ih K_ih^T, dP = dO_ih V_ih^T
@@ -705,8 +720,10 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
       }
+      LTR(2);
       // ---- band P from S
       tc::mbar_wait(&sfull[b], use & 1);
+      LTR(3);
       __syncwarp();
       tc::tc_fence_after();
       float p[NB];
@@ -723,8 +740,10 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
+      LTR(4);
       // ---- dP, delta, dS
       tc::mbar_wait(&dpfull[b], use & 1);
+      LTR(5);
       __syncwarp();
       tc::tc_fence_after();
       // dP is read from TMEM twice (delta, then dS) instead of being held next to P
@@ -752,7 +771,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < NB / 8; ++j)
         tc::tmem_st4(x + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
                      pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
-      if constexpr (Cf::SMMA) {
+      if constexpr (KVH) {
         // staircase dS -> this warpgroup's DS (row r, columns c' HZ + i; its previous item's dQ MMAs
         // completed before that item's epilogue); dS and P of the staircase -> the scratch, for the
         // per-horizon dK / dV below
@@ -795,7 +814,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       tc::mbar_arrive(&dsfull[b]);
-      if constexpr (Cf::SMMA) {
+      LTR(6);
+      if constexpr (KVH) {
         // ---- staircase dK / dV per horizon on mma.sync (while the dQ MMAs run):
         //      dK_ih (keys c' x 64) = scale dS^T Q_ih,  dV_ih = P^T dO_ih   (K = the C channel rows)
         tc::named_bar(1 + wg, 128);
@@ -845,28 +865,60 @@ __global__ void __launch_bounds__(320, 1)
         if (t == T - 1)
           for (int tt = T; tt < a.Tp; ++tt) { a.ws_del[crow * a.Tp + tt] = 0.f; a.ws_l2[crow * a.Tp + tt] = 0.f; }
       }
+      LTR(7);
       // ---- epilogue: dQ row (t, c); staircase key rows m = r: (u, c'), u = h0 + i' - c'
       tc::mbar_wait(&done[b], use & 1);
+      LTR(8);
       __syncwarp();
       tc::tc_fence_after();
-      {
+      if constexpr (!KVH) {
+        // interior items (every row of the item's skewed boxes inside [0, T)): rows staged in the
+        // stage's now-dead Q / Ks / Vs tiles (the layout their TMA loads had) and written by three
+        // TMA stores; edge items: direct row stores (a skewed box there would cross into the
+        // neighbouring channel planes).  The stage is released once the stores have read it.
+        const bool tma_out = h0 >= R && h0 + HZ <= T;
+        const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
+        const bool key_ok = cq < R && u >= 0 && u < T;
+        const long long krow = ((long long)cq * a.BH + bh) * T + u;
+        uint8_t* qst = const_cast<uint8_t*>(sbp);
+        uint8_t* kst = qst + 2 * Cf::QB + 2 * Cf::KBB;
+        uint8_t* vst = kst + Cf::SB;
+        float v[kD];
+        tmem_ld64_l(x + NB, v);
+        if (tma_out) tmem_row64_to_smem_sw128_regs(v, a.scale, qst, r);
+        else if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
+        tmem_ld64_l(x + NB + 64, v);
+        if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, a.scale, kst, r); }
+        else if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
+        tmem_ld64_l(x + NB + 128, v);
+        if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, 1.f, vst, r); }
+        else if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tfree[b]);
+        if (tma_out) tc::fence_proxy_async_smem();
+        tc::named_bar(1 + wg, 128);
+        if (r == 0) {
+          if (tma_out) {
+            tc::tma_store_4d(&tmdQ, qst, 0, h0, 0, bh);
+            tc::tma_store_4d(&tmdK, kst, 0, h0, 0, bh);
+            tc::tma_store_4d(&tmdV, vst, 0, h0, 0, bh);
+            tc::bulk_commit();
+            tc::bulk_wait_read0();
+          }
+          tc::mbar_arrive(&empty[b]);
+        }
+      } else {
         float v[kD];
         tmem_ld64_l(x + NB, v);
         if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
-        if constexpr (!Cf::SMMA) {
-          const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
-          const bool key_ok = cq < R && u >= 0 && u < T;
-          const long long krow = ((long long)cq * a.BH + bh) * T + u;
-          tmem_ld64_l(x + NB + 64, v);
-          if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
-          tmem_ld64_l(x + NB + 128, v);
-          if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
-        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tfree[b]);
       }
-      tc::tc_fence_before();
-      tc::mbar_arrive(&tfree[b]);
+      LTR(9);
+#undef LTR
     }
   }
+  tc::bulk_wait0();
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tbase, 512);
@@ -970,10 +1022,12 @@ template <int NB, int RM>
 sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, cudaStream_t st) {
   using Cf = LBCfg<NB, RM>;
   const int R = a.R, C = R + 1;
-  CUtensorMap mq, mdo, mkb, mvb, mks, mvs;
+  CUtensorMap mq, mdo, mkb, mvb, mks, mvs, mdq, mdk, mdv;
   if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map_skew(&mdo, a.dO, a.T, a.BH, C, R, HZ, C) ||
       !map4(&mkb, a.K, a.T, a.BH, C, NB) || !map4(&mvb, a.V, a.T, a.BH, C, NB) ||
-      !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) || !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R)) {
+      !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) || !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) ||
+      !map_skew(&mdq, a.dQ, a.T, a.BH, C, R, HZ, C) || !map_skew(&mdk, a.dK, a.T, a.BH, C, R, HZ, R) ||
+      !map_skew(&mdv, a.dV, a.T, a.BH, C, R, HZ, R)) {
     g_err = "tensor maps of the fused LLSA backward";
     return SATTN_ECUDA;
   }
@@ -983,9 +1037,11 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   la.LSE = a.LSE;
   la.dQ = reinterpret_cast<bf16*>(a.dQ); la.dK = reinterpret_cast<bf16*>(a.dK); la.dV = reinterpret_cast<bf16*>(a.dV);
   la.ws_del = ws_del; la.ws_l2 = ws_l2;
+  la.trace = g_llsa_trace;
   const int items = (a.T + R + HZ - 1) / HZ * a.BH;
   const int grid = items < num_sms() ? items : num_sms();
-  set_smem(llsa_bwd_fused_tc<NB, RM>, Cf::SMEM);
+  constexpr bool KVH = false;
+  set_smem(llsa_bwd_fused_tc<NB, RM, KVH>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);
@@ -996,7 +1052,8 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM>, mq, mdo, mkb, mvb, mks, mvs, la);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM, KVH>, mq, mdo, mkb, mvb, mks, mvs, mdq, mdk,
+                                           mdv, la);
   if (e != cudaSuccess) {
     g_err = std::string("fused LLSA backward launch: ") + cudaGetErrorString(e);
     return SATTN_ECUDA;
@@ -1045,5 +1102,6 @@ sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, c
 }
 
 const char* tc_llsa_last_error() { return g_err.c_str(); }
+void tc_llsa_set_trace(void* p) { g_llsa_trace = static_cast<long long*>(p); }
 
 }  // namespace sattn
