@@ -447,7 +447,7 @@ __device__ __forceinline__ void store_row64(bf16* dst, const float* v, float sc)
                        pack_bf16(v[8 * ch + 4] * sc, v[8 * ch + 5] * sc), pack_bf16(v[8 * ch + 6] * sc, v[8 * ch + 7] * sc));
 }
 
-template <int NB, int RM, bool KVH>
+template <int NB, int RM>
 __global__ void __launch_bounds__(320, 1)
     llsa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
@@ -488,9 +488,8 @@ __global__ void __launch_bounds__(320, 1)
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmKb);
     tc::tma_prefetch_desc(&tmVb); tc::tma_prefetch_desc(&tmKs); tc::tma_prefetch_desc(&tmVs);
     for (int i = 0; i < 2; ++i) {
-      // SMMA: the warpgroup still reads Q / dO of the stage for its staircase dK / dV after the
-      // dQ MMAs complete, so its 128 threads also arrive before the stage is refilled
-      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], KVH ? 129 : 1);
+      // the stage is released by the epilogue (after its TMA stores have read the staging rows)
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1);
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&done[i], 1); tc::mbar_init(&tfree[i], 128);
     }
@@ -508,10 +507,24 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // L2 prefetch of item k + 2's boxes when item k's loads are issued: its stage frees only after
+      // item k's epilogue stores have read it, so the TMA loads then mostly hit L2
+      auto prefetch = [&](int k) {
+        if (k >= nme) return;
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / nit, h0 = (g % nit) * HZ;
+        tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
+        tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
+        tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+      };
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / nit, h0 = (g % nit) * HZ;
         const int s = k & 1;
+        prefetch(k + 2);
         if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
         uint8_t* sb = stage0 + s * Cf::STAGE;
         tc::mbar_expect_tx(&full[s], 2 * qbytes + 2 * Cf::KBB + 2 * sbytes);
@@ -541,26 +554,22 @@ __global__ void __launch_bounds__(320, 1)
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
           const uint32_t q = sb, dO = sb + Cf::QB, kb = sb + 2 * Cf::QB, ks = kb + 2 * Cf::KBB;
           const uint32_t x = tbase + b * 256;
-          // SMMA: each warpgroup has its own DS (its staircase dK / dV are mma.sync in the WG)
-          const uint32_t ds = tc::smem_u32(KVH ? xds + b * Cf::XB : xds), ps = tc::smem_u32(xps);
+          const uint32_t ds = tc::smem_u32(xds), ps = tc::smem_u32(xps);
 #pragma unroll
           for (int j = 0; j < NB / 16; ++j)
             tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(kb + 2048 * j), idQ, j > 0);
           for (int j = 0; j < nks; ++j)
             tc::mma_bf16(x + NB, tc::desc_kmajor_sw128(ds + (j >> 2) * 16384 + (j & 3) * 32),
                          tc::desc_mnmajor_sw128(ks + 2048 * j), idQ, 1);
-          if constexpr (!KVH) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
-                           idK, j > 0);
-              tc::mma_bf16(x + NB + 128, tc::sdesc(ps + 2048 * j, 16384, 1024, 2),
-                           tc::desc_mnmajor_sw128(dO + 2048 * j), idK, j > 0);
-            }
+          for (int j = 0; j < 8; ++j) {
+            tc::mma_bf16(x + NB + 64, tc::sdesc(ds + 2048 * j, 16384, 1024, 2), tc::desc_mnmajor_sw128(q + 2048 * j),
+                         idK, j > 0);
+            tc::mma_bf16(x + NB + 128, tc::sdesc(ps + 2048 * j, 16384, 1024, 2),
+                         tc::desc_mnmajor_sw128(dO + 2048 * j), idK, j > 0);
           }
           tc::mma_commit(&done[b]);
-          if constexpr (KVH) tc::mma_commit(&empty[b]);   // !KVH: released by the epilogue's TMA stores
-          if constexpr (!KVH) tc::mma_commit(xsfree);
+          tc::mma_commit(xsfree);   // the stage itself is released by the epilogue's TMA stores
           ++ng;
           continue;
         }
@@ -633,30 +642,41 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t qt = sb, ot = sb + Cf::QB, ks = sb + 2 * Cf::QB + 2 * Cf::KBB, vs = ks + Cf::SB;
         const uint32_t za = tc::smem_u32(zrow), sca = tc::smem_u32(scr);
         const int gq = lane >> 2, t4 = lane & 3;
-        for (int ih = wq; ih < HZ; ih += 4) {
-          float sacc[4] = {0.f, 0.f, 0.f, 0.f}, dacc[4] = {0.f, 0.f, 0.f, 0.f};
+        // two horizons per iteration (ih, ih + 4): independent accumulator chains for ILP
+        for (int ih0 = wq; ih0 < HZ; ih0 += 8) {
+          float sacc[2][4] = {}, dacc[2][4] = {};
           const int am = lane & 15, bn = lane & 7;
-          const int arow = am < C ? am * HZ + ih : -1, brow = bn < R ? bn * HZ + ih : -1;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
-            const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
-            const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
-            uint32_t aq[4], ad[4], bk[2], bv[2];
-            ldsm_x4(arow < 0 ? za : qt + ao, aq);
-            ldsm_x4(arow < 0 ? za : ot + ao, ad);
-            ldsm_x2(brow < 0 ? za : ks + bo, bk);
-            ldsm_x2(brow < 0 ? za : vs + bo, bv);
-            mma16816(sacc, aq, bk);
-            mma16816(dacc, ad, bv);
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int ih = ih0 + 4 * u2;
+            const bool hv = ih < HZ;
+            const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
+              const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
+              const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
+              uint32_t aq[4], ad[4], bk[2], bv[2];
+              ldsm_x4(arow < 0 ? za : qt + ao, aq);
+              ldsm_x4(arow < 0 ? za : ot + ao, ad);
+              ldsm_x2(brow < 0 ? za : ks + bo, bk);
+              ldsm_x2(brow < 0 ? za : vs + bo, bv);
+              mma16816(sacc[u2], aq, bk);
+              mma16816(dacc[u2], ad, bv);
+            }
           }
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
-            if (cc < C) {
-              const uint32_t o = (uint32_t)((cc * HZ + ih) * 8 + cp) * 4;
-              tc::st_shared_u32(sca + o, __float_as_uint(sacc[e]));
-              tc::st_shared_u32(sca + 4096 + o, __float_as_uint(dacc[e]));
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int ih = ih0 + 4 * u2;
+            if (ih >= HZ) break;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
+              if (cc < C) {
+                const uint32_t o = (uint32_t)((cc * HZ + ih) * 8 + cp) * 4;
+                tc::st_shared_u32(sca + o, __float_as_uint(sacc[u2][e]));
+                tc::st_shared_u32(sca + 4096 + o, __float_as_uint(dacc[u2][e]));
+              }
             }
           }
         }
@@ -771,93 +791,26 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < NB / 8; ++j)
         tc::tmem_st4(x + 4 * j, pack_bf16(p[8 * j], p[8 * j + 1]), pack_bf16(p[8 * j + 2], p[8 * j + 3]),
                      pack_bf16(p[8 * j + 4], p[8 * j + 5]), pack_bf16(p[8 * j + 6], p[8 * j + 7]));
-      if constexpr (KVH) {
-        // staircase dS -> this warpgroup's DS (row r, columns c' HZ + i; its previous item's dQ MMAs
-        // completed before that item's epilogue); dS and P of the staircase -> the scratch, for the
-        // per-horizon dK / dV below
-        const uint32_t dsa = tc::smem_u32(xds + wg * Cf::XB), sca = tc::smem_u32(scr);
-        if (in_item) {
+      // staircase dS / P -> DS / PS (row r, columns c' HZ + i); the previous item's MMAs must have
+      // read them (one buffer shared by both warpgroups)
+      if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
+      if (in_item) {
 #pragma unroll
-          for (int cp = 0; cp < RM; ++cp) {
-            if (cp < R) {
-              const float ds = sst[cp] * (dst[cp] - delta);
-              tc::st_shared_u16(xs_addr(dsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
-              dst[cp] = ds;
-            }
-          }
-          const uint32_t o = sca + (uint32_t)r * 32;
-          tc::st_shared_v4(o, make_uint4(__float_as_uint(dst[0]), __float_as_uint(dst[1]), __float_as_uint(dst[2]),
-                                         __float_as_uint(dst[3])));
-          tc::st_shared_v4(o + 16, make_uint4(__float_as_uint(dst[4]), __float_as_uint(dst[5]),
-                                              __float_as_uint(dst[6]), __float_as_uint(dst[7])));
-          tc::st_shared_v4(o + 4096, make_uint4(__float_as_uint(sst[0]), __float_as_uint(sst[1]),
-                                                __float_as_uint(sst[2]), __float_as_uint(sst[3])));
-          tc::st_shared_v4(o + 4096 + 16, make_uint4(__float_as_uint(sst[4]), __float_as_uint(sst[5]),
-                                                     __float_as_uint(sst[6]), __float_as_uint(sst[7])));
-        }
-      } else {
-        // staircase dS / P -> DS / PS (row r, columns c' HZ + i); the previous item's MMAs must have
-        // read them (one buffer shared by both warpgroups)
-        if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
-        if (in_item) {
-#pragma unroll
-          for (int cp = 0; cp < RM; ++cp) {
-            if (cp < R) {
-              const float ds = sst[cp] * (dst[cp] - delta);
-              tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
-              tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
-            }
+        for (int cp = 0; cp < RM; ++cp) {
+          if (cp < R) {
+            const float ds = sst[cp] * (dst[cp] - delta);
+            tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
+            tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
           }
         }
       }
+      
       tc::tmem_st_wait();
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       tc::mbar_arrive(&dsfull[b]);
       LTR(6);
-      if constexpr (KVH) {
-        // ---- staircase dK / dV per horizon on mma.sync (while the dQ MMAs run):
-        //      dK_ih (keys c' x 64) = scale dS^T Q_ih,  dV_ih = P^T dO_ih   (K = the C channel rows)
-        tc::named_bar(1 + wg, 128);
-        const uint32_t qt = sb, ot = sb + Cf::QB, za = tc::smem_u32(zrow), sca = tc::smem_u32(scr);
-        const int gq = lane >> 2, t4 = lane & 3;
-        for (int ih = wq; ih < HZ; ih += 4) {
-          // A = dS^T / P^T: rows c' = gq (rows gq + 8 >= R are zero), columns c = 2 t4 (+1, +8, +9)
-          uint32_t ak[4] = {0u, 0u, 0u, 0u}, av[4] = {0u, 0u, 0u, 0u};
-          if (gq < R) {
-            float fk[4], fv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = 2 * t4 + (e & 1) + 8 * (e >> 1);
-              const uint32_t o = sca + (uint32_t)((cc * HZ + ih) * 8 + gq) * 4;
-              fk[e] = cc < C ? __uint_as_float(tc::ld_shared_u32(o)) : 0.f;
-              fv[e] = cc < C ? __uint_as_float(tc::ld_shared_u32(o + 4096)) : 0.f;
-            }
-            ak[0] = pack_bf16(fk[0], fk[1]); ak[2] = pack_bf16(fk[2], fk[3]);
-            av[0] = pack_bf16(fv[0], fv[1]); av[2] = pack_bf16(fv[2], fv[3]);
-          }
-          const int brow = (lane & 15) < C ? (lane & 15) * HZ + ih : -1;   // B rows: channel c = lane & 15
-          const int u = h0 + ih - gq;
-          const bool key_ok = gq < R && u >= 0 && u < T;
-          const long long krow = ((long long)gq * a.BH + bh) * T + u;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((j ^ (brow & 7)) << 4));
-            uint32_t bq[2], bd[2];
-            ldsm_x2_t(brow < 0 ? za : qt + bo, bq);
-            ldsm_x2_t(brow < 0 ? za : ot + bo, bd);
-            float dk[4] = {0.f, 0.f, 0.f, 0.f}, dv[4] = {0.f, 0.f, 0.f, 0.f};
-            mma16816(dk, ak, bq);
-            mma16816(dv, av, bd);
-            if (key_ok) {
-              *reinterpret_cast<uint32_t*>(a.dK + krow * kD + 8 * j + 2 * t4) = pack_bf16(dk[0] * a.scale, dk[1] * a.scale);
-              *reinterpret_cast<uint32_t*>(a.dV + krow * kD + 8 * j + 2 * t4) = pack_bf16(dv[0], dv[1]);
-            }
-          }
-        }
-        tc::mbar_arrive(&empty[b]);    // this item's stage is no longer read by the warpgroup
-        tc::named_bar(1 + wg, 128);   // the scratch is rewritten by this warpgroup's next item
-      }
+
       // workspace rows for the key-major band pass (padded rows [T, Tp) zero)
       if (row_ok) {
         a.ws_del[crow * a.Tp + t] = delta;
@@ -871,49 +824,42 @@ __global__ void __launch_bounds__(320, 1)
       LTR(8);
       __syncwarp();
       tc::tc_fence_after();
-      if constexpr (!KVH) {
-        // interior items (every row of the item's skewed boxes inside [0, T)): rows staged in the
-        // stage's now-dead Q / Ks / Vs tiles (the layout their TMA loads had) and written by three
-        // TMA stores; edge items: direct row stores (a skewed box there would cross into the
-        // neighbouring channel planes).  The stage is released once the stores have read it.
-        const bool tma_out = h0 >= R && h0 + HZ <= T;
-        const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
-        const bool key_ok = cq < R && u >= 0 && u < T;
-        const long long krow = ((long long)cq * a.BH + bh) * T + u;
-        uint8_t* qst = const_cast<uint8_t*>(sbp);
-        uint8_t* kst = qst + 2 * Cf::QB + 2 * Cf::KBB;
-        uint8_t* vst = kst + Cf::SB;
-        float v[kD];
-        tmem_ld64_l(x + NB, v);
-        if (tma_out) tmem_row64_to_smem_sw128_regs(v, a.scale, qst, r);
-        else if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
-        tmem_ld64_l(x + NB + 64, v);
-        if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, a.scale, kst, r); }
-        else if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
-        tmem_ld64_l(x + NB + 128, v);
-        if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, 1.f, vst, r); }
-        else if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
-        tc::tc_fence_before();
-        tc::mbar_arrive(&tfree[b]);
-        if (tma_out) tc::fence_proxy_async_smem();
-        tc::named_bar(1 + wg, 128);
-        if (r == 0) {
-          if (tma_out) {
-            tc::tma_store_4d(&tmdQ, qst, 0, h0, 0, bh);
-            tc::tma_store_4d(&tmdK, kst, 0, h0, 0, bh);
-            tc::tma_store_4d(&tmdV, vst, 0, h0, 0, bh);
-            tc::bulk_commit();
-            tc::bulk_wait_read0();
-          }
-          tc::mbar_arrive(&empty[b]);
+      // interior items (every row of the item's skewed boxes inside [0, T)): rows staged in the
+      // stage's now-dead Q / Ks / Vs tiles (the layout their TMA loads had) and written by three
+      // TMA stores; edge items: direct row stores (a skewed box there would cross into the
+      // neighbouring channel planes).  The stage is released once the stores have read it.
+      const bool tma_out = h0 >= R && h0 + HZ <= T;
+      const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
+      const bool key_ok = cq < R && u >= 0 && u < T;
+      const long long krow = ((long long)cq * a.BH + bh) * T + u;
+      uint8_t* qst = const_cast<uint8_t*>(sbp);
+      uint8_t* kst = qst + 2 * Cf::QB + 2 * Cf::KBB;
+      uint8_t* vst = kst + Cf::SB;
+      float v[kD];
+      tmem_ld64_l(x + NB, v);
+      if (tma_out) tmem_row64_to_smem_sw128_regs(v, a.scale, qst, r);
+      else if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
+      tmem_ld64_l(x + NB + 64, v);
+      if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, a.scale, kst, r); }
+      else if (key_ok) store_row64(a.dK + krow * kD, v, a.scale);
+      tmem_ld64_l(x + NB + 128, v);
+      if (tma_out) { if (r < R * HZ) tmem_row64_to_smem_sw128_regs(v, 1.f, vst, r); }
+      else if (key_ok) store_row64(a.dV + krow * kD, v, 1.f);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+      if (tma_out) tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (r == 0) {
+        if (tma_out) {
+          tc::tma_store_4d(&tmdQ, qst, 0, h0, 0, bh);
+          tc::tma_store_4d(&tmdK, kst, 0, h0, 0, bh);
+          tc::tma_store_4d(&tmdV, vst, 0, h0, 0, bh);
+          tc::bulk_commit();
+          tc::bulk_wait_read0();
         }
-      } else {
-        float v[kD];
-        tmem_ld64_l(x + NB, v);
-        if (row_ok) store_row64(a.dQ + (crow * T + t) * kD, v, a.scale);
-        tc::tc_fence_before();
-        tc::mbar_arrive(&tfree[b]);
+        tc::mbar_arrive(&empty[b]);
       }
+      
       LTR(9);
 #undef LTR
     }
@@ -1040,8 +986,7 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   la.trace = g_llsa_trace;
   const int items = (a.T + R + HZ - 1) / HZ * a.BH;
   const int grid = items < num_sms() ? items : num_sms();
-  constexpr bool KVH = false;
-  set_smem(llsa_bwd_fused_tc<NB, RM, KVH>, Cf::SMEM);
+  set_smem(llsa_bwd_fused_tc<NB, RM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);
@@ -1052,7 +997,7 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM, KVH>, mq, mdo, mkb, mvb, mks, mvs, mdq, mdk,
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM>, mq, mdo, mkb, mvb, mks, mvs, mdq, mdk,
                                            mdv, la);
   if (e != cudaSuccess) {
     g_err = std::string("fused LLSA backward launch: ") + cudaGetErrorString(e);
