@@ -175,7 +175,7 @@ sattn_status ffma_backward_p(const sattn_desc* d, const AttnArgs& a, cudaStream_
 bool tc_ok(const sattn_desc* d, bool llsa, bool backward) {
   if (llsa)
     return backward ? tc_llsa_bwd_any_supported(d->dtype, (int)d->D, d->L, d->R, d->B * d->H, d->T, !d->in_broadcast)
-                    : tc_llsa_supported(d->dtype, (int)d->D, d->L, d->R);
+                    : tc_llsa_fwd_any_supported(d->dtype, (int)d->D, d->L, d->R, d->B * d->H, d->T, !d->in_broadcast);
   return tc_supported(d->dtype, (int)d->D, d->L, d->R, false, backward);
 }
 
@@ -190,7 +190,7 @@ sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const v
   if (!aligned16(Q) || !aligned16(K) || !aligned16(V) || !aligned16(O) || !aligned16(LSE))
     return fail(SATTN_EARG, "tensor pointers must be 16-byte aligned");
   if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, false))
-    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA forward needs bf16, D=64, 4 <= R <= 8, L <= 32"
+    return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA forward needs bf16, D=64, R <= 8 (4 <= R, L <= 32 for broadcast inputs)"
                                          : "tensor-core SA forward needs bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE;

@@ -22,6 +22,7 @@ const char* tc_last_error();
 void tc_set_trace(void* p);  // debug only
 // tensor-core LLSA forward (tc_llsa.cu)
 bool tc_llsa_supported(int dtype, int D, int L, int R);
+bool tc_llsa_fwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st);
 const char* tc_llsa_last_error();
 void tc_llsa_set_trace(void* p);  // debug only

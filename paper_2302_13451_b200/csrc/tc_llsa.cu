@@ -871,6 +871,302 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
+// LLSA forward, item form (dense inputs, R <= 8): the same item as the fused backward below —
+// HZ horizons x all C channels, row r = c HZ + i <-> output (t, c), t = h0 + i - c — so the
+// staircase of a horizon is one 16 x 8 mma.sync block and every row's stair probabilities land
+// in a per-warpgroup smem tile read by the PV MMA:
+//   MMA  S   = Q Kb^T -> X_b[0, NB)            WG  stair scores (mma.sync per horizon, scratch),
+//                                                   band strip from TMEM, joint softmax; P_band ->
+//                                                   X_b (packed bf16), P_stair -> PS_wg (smem)
+//   MMA  O   = [P_band | PS] [Vb ; Vs] -> X_b[NB, NB + 64)
+//                                              WG  O / l, LSE; interior items: O rows staged in
+//                                                  the dead Q tile, one skewed TMA store
+// ------------------------------------------------------------------------------------------
+struct LlsaFwdArgs {
+  int T, L, R, C, BH, HZ;
+  float scale, scale_log2;
+  float* LSE;                    // [C][BH][T]
+  bf16* O;                       // [C][BH][T][64]
+};
+
+template <int NB> struct LFCfg {
+  static constexpr int QB = 128 * 128;
+  static constexpr int KBB = NB * 128;
+  static constexpr int SB = 112 * 128;
+  static constexpr int STAGE = QB + 2 * KBB + 2 * SB;      // Q | Kb | Vb | Ks | Vs
+  static constexpr int XB = 2 * 128 * 128;                 // PS per warpgroup
+  static constexpr int SCR = 128 * 8 * 4;                  // stair scores per warpgroup
+  static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
+  static_assert(NB + 64 <= 256 && SMEM <= 232448, "TMEM / shared memory");
+};
+
+template <int NB>
+__global__ void __launch_bounds__(320, 1)
+    llsa_fwd_item_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKb,
+                     const __grid_constant__ CUtensorMap tmVb, const __grid_constant__ CUtensorMap tmKs,
+                     const __grid_constant__ CUtensorMap tmVs, const __grid_constant__ CUtensorMap tmO,
+                     LlsaFwdArgs a) {
+  using Cf = LFCfg<NB>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage0 = smem;
+  uint8_t* xps0 = smem + 2 * Cf::STAGE;
+  uint8_t* scr0 = xps0 + 2 * Cf::XB;
+  uint8_t* zrow = scr0 + 2 * Cf::SCR;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zrow + 128);
+  uint64_t* full = bars;          // [2]
+  uint64_t* empty = full + 2;     // [2] (released by the epilogue leader)
+  uint64_t* sfull = empty + 2;    // [2]
+  uint64_t* pfull = sfull + 2;    // [2] (128)
+  uint64_t* ofull = pfull + 2;    // [2]
+  uint64_t* tfree = ofull + 2;    // [2] (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int T = a.T, L = a.L, R = a.R, C = a.C, HZ = a.HZ;
+  const int nit = (T + R + HZ - 1) / HZ;
+  const int nitems = nit * a.BH;
+  const int nme = blockIdx.x < nitems ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int qbytes = C * HZ * 128, sbytes = R * HZ * 128;
+
+  for (int o = tid * 16; o < 2 * Cf::STAGE + 2 * Cf::XB + 2 * Cf::SCR + 128; o += 320 * 16)
+    *reinterpret_cast<uint4*>(smem + o) = make_uint4(0u, 0u, 0u, 0u);
+  if (tid == 0) {
+    tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmKb); tc::tma_prefetch_desc(&tmVb);
+    tc::tma_prefetch_desc(&tmKs); tc::tma_prefetch_desc(&tmVs); tc::tma_prefetch_desc(&tmO);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&sfull[i], 1); tc::mbar_init(&pfull[i], 128);
+      tc::mbar_init(&ofull[i], 1); tc::mbar_init(&tfree[i], 128);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  tc::pdl_wait();
+  tc::pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      auto prefetch = [&](int k) {
+        if (k >= nme) return;
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / nit, h0 = (g % nit) * HZ;
+        tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
+        tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
+        tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+      };
+      for (int k = 0; k < nme; ++k) {
+        const int g = blockIdx.x + k * gridDim.x;
+        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int s = k & 1;
+        prefetch(k + 2);
+        if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
+        uint8_t* sb = stage0 + s * Cf::STAGE;
+        tc::mbar_expect_tx(&full[s], qbytes + 2 * Cf::KBB + 2 * sbytes);
+        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb + Cf::QB, &tmKb, &full[s], 0, h0 - R - L, bh, R);
+        tc::tma_load_4d(sb + Cf::QB + Cf::KBB, &tmVb, &full[s], 0, h0 - R - L, bh, R);
+        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, h0, 0, bh);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nme > 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, NB, 0, 0);
+      constexpr uint32_t idO = tc::idesc_bf16(128, kD, 0, 1);
+      const int nks = (R * HZ + 15) / 16;
+      int ns = 0, no = 0;
+      while (no < nme) {
+        const uint32_t m = tc::mbar_test4(tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1,
+                                          tc::smem_u32(&full[ns & 1]), (ns >> 1) & 1,
+                                          tc::smem_u32(&tfree[ns & 1]), ((ns + 2) >> 1) & 1,
+                                          tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1);
+        if (no < ns && (m & 1)) {   // O of item no
+          tc::tc_fence_after();
+          const int b = no & 1;
+          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t vb = sb + Cf::QB + Cf::KBB, vs = sb + Cf::QB + 2 * Cf::KBB + Cf::SB;
+          const uint32_t x = tbase + b * 256;
+          const uint32_t ps = tc::smem_u32(xps0 + b * Cf::XB);
+#pragma unroll
+          for (int j = 0; j < NB / 16; ++j)
+            tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(vb + 2048 * j), idO, j > 0);
+          for (int j = 0; j < nks; ++j)
+            tc::mma_bf16(x + NB, tc::desc_kmajor_sw128(ps + (j >> 2) * 16384 + (j & 3) * 32),
+                         tc::desc_mnmajor_sw128(vs + 2048 * j), idO, 1);
+          tc::mma_commit(&ofull[b]);
+          ++no;
+          continue;
+        }
+        if (ns < nme && ns < no + 2 && (m & 2) && (ns < 2 || (m & 4))) {   // S_band of item ns
+          tc::tc_fence_after();
+          const int b = ns & 1;
+          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t q = sb, kb = sb + Cf::QB;
+#pragma unroll
+          for (int j = 0; j < kD / 16; ++j)
+            tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kb + 32 * j), idS,
+                         j > 0);
+          tc::mma_commit(&sfull[b]);
+          ++ns;
+          continue;
+        }
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;
+    const uint32_t lanes = uint32_t(32 * q4) << 16;
+    const int c = r / HZ, i = r - c * HZ;
+    const bool in_item = c < C;
+    const int wq = warp & 3;
+    const uint32_t psa = tc::smem_u32(xps0 + wg * Cf::XB), sca = tc::smem_u32(scr0 + wg * Cf::SCR);
+    const uint32_t za = tc::smem_u32(zrow);
+    for (int k = wg; k < nme; k += 2) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / nit, h0 = (g % nit) * HZ;
+      const int b = wg, use = k >> 1;
+      const int h = h0 + i, t = h - c;
+      const bool row_ok = in_item && t >= 0 && t < T;
+      uint8_t* sbp = stage0 + b * Cf::STAGE;
+      const uint32_t sb = tc::smem_u32(sbp);
+      tc::mbar_wait(&full[b], use & 1);
+      // ---- staircase scores S[c][c'] = q_(h-c, c) . k_(h-c', c') on mma.sync, one 16 x 8 block
+      //      per horizon (two horizons per iteration), through the scratch [128 rows][8]
+      {
+        const uint32_t qt = sb, ks = sb + Cf::QB + 2 * Cf::KBB;
+        const int gq = lane >> 2, t4 = lane & 3;
+        for (int ih0 = wq; ih0 < HZ; ih0 += 8) {
+          float sacc[2][4] = {};
+          const int am = lane & 15, bn = lane & 7;
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int ih = ih0 + 4 * u2;
+            const bool hv = ih < HZ;
+            const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
+              const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
+              const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
+              uint32_t aq[4], bk[2];
+              ldsm_x4(arow < 0 ? za : qt + ao, aq);
+              ldsm_x2(brow < 0 ? za : ks + bo, bk);
+              mma16816(sacc[u2], aq, bk);
+            }
+          }
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const int ih = ih0 + 4 * u2;
+            if (ih >= HZ) break;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
+              if (cc < C) tc::st_shared_u32(sca + (uint32_t)((cc * HZ + ih) * 8 + cp) * 4, __float_as_uint(sacc[u2][e]));
+            }
+          }
+        }
+      }
+      tc::named_bar(1 + wg, 128);
+      float sst[8];
+      {
+        const uint32_t o = sca + (uint32_t)r * 32;
+        const uint4 s0 = tc::ld_shared_v4(o), s1 = tc::ld_shared_v4(o + 16);
+        const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+        for (int cp = 0; cp < 8; ++cp) {
+          const int f = h - cp;
+          sst[cp] = (row_ok && cp < R && f >= 0 && f < T) ? __uint_as_float(sv[cp]) : neg_inf();
+        }
+      }
+      tc::named_bar(1 + wg, 128);   // scratch rewritten by this warpgroup's next item
+      // ---- band strip + joint softmax
+      tc::mbar_wait(&sfull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      float s[NB];
+      const uint32_t x = tbase + lanes + b * 256;
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j) tc::tmem_ld8(x + 8 * j, s + 8 * j);
+      tc::tmem_ld_wait();
+      const int key0 = h0 - R - L;
+      const int jlo = max(i, -key0), jhi = min(i + L, T - 1 - key0);
+      float mx = neg_inf();
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        s[j] = (row_ok && j >= jlo && j <= jhi) ? s[j] : neg_inf();
+        mx = fmaxf(mx, s[j]);
+      }
+#pragma unroll
+      for (int cp = 0; cp < 8; ++cp) mx = fmaxf(mx, sst[cp]);
+      const float mref = mx == neg_inf() ? 0.f : mx;
+      const float mb = mref * a.scale_log2;
+      float l = 0.f;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        s[j] = tc::ex2(fmaf(s[j], a.scale_log2, -mb));
+        l += s[j];
+      }
+#pragma unroll
+      for (int cp = 0; cp < 8; ++cp) {
+        sst[cp] = tc::ex2(fmaf(sst[cp], a.scale_log2, -mb));
+        l += sst[cp];
+      }
+#pragma unroll
+      for (int j = 0; j < NB / 8; ++j)
+        tc::tmem_st4(x + 4 * j, pack_bf16(s[8 * j], s[8 * j + 1]), pack_bf16(s[8 * j + 2], s[8 * j + 3]),
+                     pack_bf16(s[8 * j + 4], s[8 * j + 5]), pack_bf16(s[8 * j + 6], s[8 * j + 7]));
+      // P_stair -> this warpgroup's PS (its previous item's PV MMA completed before that epilogue)
+      if (in_item) {
+#pragma unroll
+        for (int cp = 0; cp < 8; ++cp)
+          if (cp < R) tc::st_shared_u16(xs_addr(psa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
+      }
+      tc::tmem_st_wait();
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&pfull[b]);
+      // ---- epilogue
+      tc::mbar_wait(&ofull[b], use & 1);
+      __syncwarp();
+      tc::tc_fence_after();
+      const bool tma_out = h0 >= R && h0 + HZ <= T;
+      float v[kD];
+      tmem_ld64_l(x + NB, v);
+      const float inv = 1.f / l;
+      const long long crow = (long long)c * a.BH + bh;
+      if (tma_out) tmem_row64_to_smem_sw128_regs(v, inv, sbp, r);
+      else if (row_ok) store_row64(a.O + (crow * T + t) * kD, v, inv);
+      if (row_ok) a.LSE[crow * T + t] = mref * a.scale + __log2f(l) * kLn2;
+      tc::tc_fence_before();
+      tc::mbar_arrive(&tfree[b]);
+      if (tma_out) tc::fence_proxy_async_smem();
+      tc::named_bar(1 + wg, 128);
+      if (r == 0) {
+        if (tma_out) {
+          tc::tma_store_4d(&tmO, sbp, 0, h0, 0, bh);
+          tc::bulk_commit();
+          tc::bulk_wait_read0();
+        }
+        tc::mbar_arrive(&empty[b]);
+      }
+    }
+  }
+  tc::bulk_wait0();
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tbase, 512);
+}
+
+// ------------------------------------------------------------------------------------------
 // host
 // ------------------------------------------------------------------------------------------
 // [C][BH][T][64] bf16 as a 4-D tensor (64, T, BH, C); box (64, rows, 1, 1); 128B swizzle.
@@ -1008,6 +1304,50 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
 
 }  // namespace
 
+template <int NB>
+sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
+  using Cf = LFCfg<NB>;
+  const int R = a.R, C = R + 1;
+  CUtensorMap mq, mkb, mvb, mks, mvs, mo;
+  if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map4(&mkb, a.K, a.T, a.BH, C, NB) ||
+      !map4(&mvb, a.V, a.T, a.BH, C, NB) || !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) ||
+      !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) || !map_skew(&mo, a.Out, a.T, a.BH, C, R, HZ, C)) {
+    g_err = "tensor maps of the item-form LLSA forward";
+    return SATTN_ECUDA;
+  }
+  LlsaFwdArgs la{};
+  la.T = a.T; la.L = a.L; la.R = R; la.C = C; la.BH = a.BH; la.HZ = HZ;
+  la.scale = a.scale; la.scale_log2 = a.scale_log2;
+  la.LSE = a.LSEout;
+  la.O = reinterpret_cast<bf16*>(a.Out);
+  const int items = (a.T + R + HZ - 1) / HZ * a.BH;
+  const int grid = items < num_sms() ? items : num_sms();
+  set_smem(llsa_fwd_item_tc<NB>, Cf::SMEM);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = Cf::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_fwd_item_tc<NB>, mq, mkb, mvb, mks, mvs, mo, la);
+  if (e != cudaSuccess) {
+    g_err = std::string("item-form LLSA forward launch: ") + cudaGetErrorString(e);
+    return SATTN_ECUDA;
+  }
+  return SATTN_OK;
+}
+
+// item form (dense inputs): R <= 8, the item's band window HZ + L in NB <= 64 columns
+bool fwd_item_ok(const AttnArgs& a) {
+  if (a.in_cs == 0 || a.R < 1 || a.R > 8) return false;
+  const int hz = fused_hz(a.L, a.R);
+  return hz >= 4 && (long long)a.BH * a.T - 1 >= (long long)a.T + a.R && (hz + a.L + 15) / 16 * 16 <= 64;
+}
+
 bool tc_llsa_supported(int dtype, int D, int L, int R) {
   // one warp per channel of a 4-channel item needs >= 2 items per tile (C >= 5); the P row
   // (NB + 32 R packed / 2 <= 192 columns) and the 8 staged stair tiles need R <= 8; NB <= 64
@@ -1015,6 +1355,15 @@ bool tc_llsa_supported(int dtype, int D, int L, int R) {
 }
 
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
+  if (fwd_item_ok(a)) {
+    const int hz = fused_hz(a.L, a.R);
+    switch ((hz + a.L + 15) / 16 * 16) {
+      case 16:
+      case 32: return fwd_item_launch<32>(a, hz, st);
+      case 48: return fwd_item_launch<48>(a, hz, st);
+      case 64: return fwd_item_launch<64>(a, hz, st);
+    }
+  }
   const int nb = (32 + a.L + 15) / 16 * 16;
   switch (nb) {
     case 48: return launch<48>(a, st);
@@ -1022,6 +1371,14 @@ sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
   }
   g_err = "band too wide for the LLSA tensor-core kernel";
   return SATTN_EUNSUPPORTED;
+}
+
+// the item form (dense inputs, 1 <= R <= 8) or the 4-channel-item kernel (4 <= R <= 8, L <= 32)
+bool tc_llsa_fwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense) {
+  if (tc_llsa_supported(dtype, D, L, R)) return true;
+  if (dtype != SATTN_BF16 || D != 64 || !dense || R < 1 || R > 8 || L < 0) return false;
+  const int hz = fused_hz(L, R);
+  return hz >= 4 && BH * T - 1 >= T + R && (hz + L + 15) / 16 * 16 <= 64;
 }
 
 // fused horizon-major LLSA backward (dense inputs): dQ, staircase dK / dV, delta and LSE log2e
