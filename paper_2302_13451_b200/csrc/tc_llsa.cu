@@ -889,24 +889,24 @@ struct LlsaFwdArgs {
   bf16* O;                       // [C][BH][T][64]
 };
 
-template <int NB> struct LFCfg {
+template <int NB, int RM> struct LFCfg {
   static constexpr int QB = 128 * 128;
   static constexpr int KBB = NB * 128;
   static constexpr int SB = 112 * 128;
   static constexpr int STAGE = QB + 2 * KBB + 2 * SB;      // Q | Kb | Vb | Ks | Vs
   static constexpr int XB = 2 * 128 * 128;                 // PS per warpgroup
-  static constexpr int SCR = 128 * 8 * 4;                  // stair scores per warpgroup
+  static constexpr int SCR = 128 * RM * 4;                 // stair scores per warpgroup
   static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
   static_assert(NB + 64 <= 256 && SMEM <= 232448, "TMEM / shared memory");
 };
 
-template <int NB>
+template <int NB, int RM>
 __global__ void __launch_bounds__(320, 1)
     llsa_fwd_item_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKb,
                      const __grid_constant__ CUtensorMap tmVb, const __grid_constant__ CUtensorMap tmKs,
                      const __grid_constant__ CUtensorMap tmVs, const __grid_constant__ CUtensorMap tmO,
                      LlsaFwdArgs a) {
-  using Cf = LFCfg<NB>;
+  using Cf = LFCfg<NB, RM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;
@@ -1039,52 +1039,62 @@ __global__ void __launch_bounds__(320, 1)
       uint8_t* sbp = stage0 + b * Cf::STAGE;
       const uint32_t sb = tc::smem_u32(sbp);
       tc::mbar_wait(&full[b], use & 1);
-      // ---- staircase scores S[c][c'] = q_(h-c, c) . k_(h-c', c') on mma.sync, one 16 x 8 block
-      //      per horizon (two horizons per iteration), through the scratch [128 rows][8]
+      // ---- staircase scores S[c][c'] = q_(h-c, c) . k_(h-c', c') on mma.sync: per horizon ceil(C/16)
+      //      x RM/8 blocks of 16 x 8 (two horizons per iteration), through the scratch [128][RM]
       {
         const uint32_t qt = sb, ks = sb + Cf::QB + 2 * Cf::KBB;
         const int gq = lane >> 2, t4 = lane & 3;
+        const int nmb = (C + 15) / 16;
         for (int ih0 = wq; ih0 < HZ; ih0 += 8) {
-          float sacc[2][4] = {};
-          const int am = lane & 15, bn = lane & 7;
+          for (int mb = 0; mb < nmb; ++mb) {
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            const int ih = ih0 + 4 * u2;
-            const bool hv = ih < HZ;
-            const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
+            for (int nb = 0; nb < RM / 8; ++nb) {
+              float sacc[2][4] = {};
+              const int am = 16 * mb + (lane & 15), bn = 8 * nb + (lane & 7);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
-              const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
-              const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
-              uint32_t aq[4], bk[2];
-              ldsm_x4(arow < 0 ? za : qt + ao, aq);
-              ldsm_x2(brow < 0 ? za : ks + bo, bk);
-              mma16816(sacc[u2], aq, bk);
-            }
-          }
+              for (int u2 = 0; u2 < 2; ++u2) {
+                const int ih = ih0 + 4 * u2;
+                const bool hv = ih < HZ;
+                const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            const int ih = ih0 + 4 * u2;
-            if (ih >= HZ) break;
+                for (int kk = 0; kk < 4; ++kk) {
+                  const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
+                  const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
+                  const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
+                  uint32_t aq[4], bk[2];
+                  ldsm_x4(arow < 0 ? za : qt + ao, aq);
+                  ldsm_x2(brow < 0 ? za : ks + bo, bk);
+                  mma16816(sacc[u2], aq, bk);
+                }
+              }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
-              if (cc < C) tc::st_shared_u32(sca + (uint32_t)((cc * HZ + ih) * 8 + cp) * 4, __float_as_uint(sacc[u2][e]));
+              for (int u2 = 0; u2 < 2; ++u2) {
+                const int ih = ih0 + 4 * u2;
+                if (ih >= HZ) break;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int cc = 16 * mb + gq + 8 * (e >> 1), cp = 8 * nb + 2 * t4 + (e & 1);
+                  if (cc < C)
+                    tc::st_shared_u32(sca + (uint32_t)((cc * HZ + ih) * RM + cp) * 4, __float_as_uint(sacc[u2][e]));
+                }
+              }
             }
           }
         }
       }
       tc::named_bar(1 + wg, 128);
-      float sst[8];
+      float sst[RM];
       {
-        const uint32_t o = sca + (uint32_t)r * 32;
-        const uint4 s0 = tc::ld_shared_v4(o), s1 = tc::ld_shared_v4(o + 16);
-        const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const uint32_t o = sca + (uint32_t)r * RM * 4;
 #pragma unroll
-        for (int cp = 0; cp < 8; ++cp) {
-          const int f = h - cp;
-          sst[cp] = (row_ok && cp < R && f >= 0 && f < T) ? __uint_as_float(sv[cp]) : neg_inf();
+        for (int q = 0; q < RM / 4; ++q) {
+          const uint4 s4 = tc::ld_shared_v4(o + 16 * q);
+          const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int cp = 4 * q + e, f = h - cp;
+            sst[cp] = (row_ok && cp < R && f >= 0 && f < T) ? __uint_as_float(sv[e]) : neg_inf();
+          }
         }
       }
       tc::named_bar(1 + wg, 128);   // scratch rewritten by this warpgroup's next item
@@ -1106,7 +1116,7 @@ __global__ void __launch_bounds__(320, 1)
         mx = fmaxf(mx, s[j]);
       }
 #pragma unroll
-      for (int cp = 0; cp < 8; ++cp) mx = fmaxf(mx, sst[cp]);
+      for (int cp = 0; cp < RM; ++cp) mx = fmaxf(mx, sst[cp]);
       const float mref = mx == neg_inf() ? 0.f : mx;
       const float mb = mref * a.scale_log2;
       float l = 0.f;
@@ -1116,7 +1126,7 @@ __global__ void __launch_bounds__(320, 1)
         l += s[j];
       }
 #pragma unroll
-      for (int cp = 0; cp < 8; ++cp) {
+      for (int cp = 0; cp < RM; ++cp) {
         sst[cp] = tc::ex2(fmaf(sst[cp], a.scale_log2, -mb));
         l += sst[cp];
       }
@@ -1127,7 +1137,7 @@ __global__ void __launch_bounds__(320, 1)
       // P_stair -> this warpgroup's PS (its previous item's PV MMA completed before that epilogue)
       if (in_item) {
 #pragma unroll
-        for (int cp = 0; cp < 8; ++cp)
+        for (int cp = 0; cp < RM; ++cp)
           if (cp < R) tc::st_shared_u16(xs_addr(psa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
       }
       tc::tmem_st_wait();
@@ -1304,9 +1314,9 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
 
 }  // namespace
 
-template <int NB>
+template <int NB, int RM>
 sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
-  using Cf = LFCfg<NB>;
+  using Cf = LFCfg<NB, RM>;
   const int R = a.R, C = R + 1;
   CUtensorMap mq, mkb, mvb, mks, mvs, mo;
   if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map4(&mkb, a.K, a.T, a.BH, C, NB) ||
@@ -1322,7 +1332,7 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
   la.O = reinterpret_cast<bf16*>(a.Out);
   const int items = (a.T + R + HZ - 1) / HZ * a.BH;
   const int grid = items < num_sms() ? items : num_sms();
-  set_smem(llsa_fwd_item_tc<NB>, Cf::SMEM);
+  set_smem(llsa_fwd_item_tc<NB, RM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);
@@ -1333,7 +1343,7 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_fwd_item_tc<NB>, mq, mkb, mvb, mks, mvs, mo, la);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_fwd_item_tc<NB, RM>, mq, mkb, mvb, mks, mvs, mo, la);
   if (e != cudaSuccess) {
     g_err = std::string("item-form LLSA forward launch: ") + cudaGetErrorString(e);
     return SATTN_ECUDA;
@@ -1341,9 +1351,9 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
   return SATTN_OK;
 }
 
-// item form (dense inputs): R <= 8, the item's band window HZ + L in NB <= 64 columns
+// item form (dense inputs): R <= 16, the item's band window HZ + L in NB <= 64 columns
 bool fwd_item_ok(const AttnArgs& a) {
-  if (a.in_cs == 0 || a.R < 1 || a.R > 8) return false;
+  if (a.in_cs == 0 || a.R < 1 || a.R > 16) return false;
   const int hz = fused_hz(a.L, a.R);
   return hz >= 4 && (long long)a.BH * a.T - 1 >= (long long)a.T + a.R && (hz + a.L + 15) / 16 * 16 <= 64;
 }
@@ -1357,11 +1367,12 @@ bool tc_llsa_supported(int dtype, int D, int L, int R) {
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
   if (fwd_item_ok(a)) {
     const int hz = fused_hz(a.L, a.R);
+    const bool r16 = a.R > 8;
     switch ((hz + a.L + 15) / 16 * 16) {
       case 16:
-      case 32: return fwd_item_launch<32>(a, hz, st);
-      case 48: return fwd_item_launch<48>(a, hz, st);
-      case 64: return fwd_item_launch<64>(a, hz, st);
+      case 32: return r16 ? fwd_item_launch<32, 16>(a, hz, st) : fwd_item_launch<32, 8>(a, hz, st);
+      case 48: return r16 ? fwd_item_launch<48, 16>(a, hz, st) : fwd_item_launch<48, 8>(a, hz, st);
+      case 64: return r16 ? fwd_item_launch<64, 16>(a, hz, st) : fwd_item_launch<64, 8>(a, hz, st);
     }
   }
   const int nb = (32 + a.L + 15) / 16 * 16;
@@ -1376,7 +1387,7 @@ sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
 // the item form (dense inputs, 1 <= R <= 8) or the 4-channel-item kernel (4 <= R <= 8, L <= 32)
 bool tc_llsa_fwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense) {
   if (tc_llsa_supported(dtype, D, L, R)) return true;
-  if (dtype != SATTN_BF16 || D != 64 || !dense || R < 1 || R > 8 || L < 0) return false;
+  if (dtype != SATTN_BF16 || D != 64 || !dense || R < 1 || R > 16 || L < 0) return false;
   const int hz = fused_hz(L, R);
   return hz >= 4 && BH * T - 1 >= T + R && (hz + L + 15) / 16 * 16 <= 64;
 }

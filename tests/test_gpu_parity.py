@@ -112,6 +112,9 @@ LLSA_CASES = [
     # tensor-core LLSA (forward: 4 <= R <= 8, L <= 32; backward: 1 <= R <= 8) incl. ragged tails
     ("bf16", (1, 3, 777, 64), 32, 8), ("bf16", (1, 2, 200, 64), 16, 4), ("bf16", (1, 1, 130, 64), 5, 1),
     ("bf16", (1, 1, 96, 64), 16, 6),
+    # item-form forward / fused backward (dense inputs, 1 <= R <= 16): small R, L = 0, R = 16 with L = 48
+    ("bf16", (2, 2, 300, 64), 32, 1), ("bf16", (1, 3, 257, 64), 8, 2), ("bf16", (2, 1, 150, 64), 0, 3),
+    ("bf16", (1, 2, 400, 64), 48, 16), ("bf16", (2, 2, 513, 64), 20, 12),
 ]
 
 
