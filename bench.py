@@ -245,9 +245,13 @@ def run_gpu(args):
     kern = {KF: (fwd_ms, FB * units), KB: (bwd_ms, BB * units)}
     dom = max(kern, key=lambda k: kern[k][0])
     achieved = kern[dom][1] / (kern[dom][0] / 1e3) / 1e9
-    traffic = load_traffic(dom, args.kernels)
+    tr = load_traffic(dom, args.kernels) or {}
+    traffic = tr.get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "traffic_note": "dram read + max(dram write, output bytes) per launch (profiles/traffic.json)",
+                "traffic_ratio": tr.get("traffic_ratio"), "dram_read_bytes": tr.get("dram_read_bytes"),
+                "read_ratio_vs_algorithmic_reads": tr.get("read_ratio"),
                 "algorithmic_bytes_per_launch": kern[dom][1],
                 "per_call_ms": {k: round(v[0], 4) for k, v in kern.items()},
                 "step_frac": {k: round(v[0] * NL / ms_per_step, 3) for k, v in kern.items()},
@@ -333,7 +337,7 @@ def run_gpu(args):
         del hin, hout, sets
 
     # ---------------- LLSA step (same shape, C = R+1 channels), reported alongside
-    llsa = None
+    llsa = llsa_r16 = None
     if not args.no_llsa:
         del Qs, Ks, Vs, dOs, Os, dQs, dKs, dVs
         torch.cuda.empty_cache()
@@ -341,6 +345,11 @@ def run_gpu(args):
             llsa = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm)
         except Exception as e:
             llsa = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
+        try:   # Table 3's second band, l32_r16 (C = 17 channels)
+            llsa_r16 = run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm, R=16)
+        except Exception as e:
+            llsa_r16 = {"error": f"{type(e).__name__}: {e}"[:300]}
 
     alt = None   # the other SA mode, same workload
     if not args.no_alt:
@@ -404,7 +413,7 @@ def run_gpu(args):
                       "B": B, "H": H, "T": T, "D": D, "L": L, "R": R, "layers": NL, "global_batch": B * world,
                       "frames_per_step": B * T * world, "parallelism": f"batch-sharded x{world} (no collective)",
                       "kernels": args.kernels, "l2": "working set 2.3 GB/rank >> 126 MB L2 (no flush)"},
-           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, ("lse_mode" if band else "band_mode"): alt,
+           "roofline": roofline, "clocks": clocks, "gpu_launches": launches, "e2e": e2e, "llsa": llsa, "llsa_r16": llsa_r16, ("lse_mode" if band else "band_mode"): alt,
            "large": large, "hour": hour, "fa2_local_context": fa2, "comm": comm, "encoder": enc, "stream": stream_lat, "latency": latency_check(sattn, dev) if not args.no_stream else None,
            "cpu_baseline": cpu}
     print(json.dumps(out))
@@ -427,7 +436,7 @@ def _max_ms(ms, world, dev):
     return float(tt.item())
 
 
-def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
+def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm, R=R):
     """M2 (BASELINE configs[2]): the 12-layer LLSA step (C = R+1 = 9 channels) at the base shape with
     the B*H = 96 (b, h) units split over the ranks - strong scaling (B/N sequences per rank, every
     rank all H heads); value = B*T frames / max-over-ranks step time."""
@@ -488,7 +497,8 @@ def run_llsa(args, sattn, dev, rnd, barrier, world, stream, hbm):
             "per_call_ms": {"llsa_forward": round(f_ms / n_layers, 4), "llsa_backward": round(b_ms / n_layers, 4)},
             "hbm_frac_per_call": {"llsa_forward": round(FWD_BYTES * units / (f_ms / n_layers / 1e3) / 1e9 / hbm, 4),
                                   "llsa_backward": round(BWD_BYTES * units / (b_ms / n_layers / 1e3) / 1e9 / hbm, 4)},
-            "workload": f"M2: 12 layers x (LLSA fwd + LLSA bwd), untied per-layer [C,B,H,T,D] inputs, B*H = {B * H} "
+            "band": [L, R],
+            "workload": f"M2: 12 layers x (LLSA fwd + LLSA bwd), (L,R)=({L},{R}), untied per-layer [C,B,H,T,D] inputs, B*H = {B * H} "
                         f"(b,h) units split over {world} rank(s) ({Br * H} per rank)"}
 
 
@@ -850,8 +860,7 @@ def load_traffic(kernel, impl):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         j = json.load(open(p))
-        e = j.get(f"{kernel}:{impl}") or j.get(kernel)
-        return e["dram_bytes_per_launch"] if e else None
+        return j.get(f"{kernel}:{impl}") or j.get(kernel)
     except Exception:
         return None
 

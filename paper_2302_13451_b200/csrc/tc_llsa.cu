@@ -409,10 +409,12 @@ template <int NB, int RM> struct LBCfg {
   static constexpr int SB = 112 * 128;             // stair K / V tiles (rows c' HZ + i, R HZ <= 112)
   static constexpr int STAGE = 2 * QB + 2 * KBB + 2 * SB;
   static constexpr int XB = 2 * 128 * 128;         // DS / PS
-  // staircase scores / dP on mma.sync (one 16 x 8 block per horizon) through a per-warpgroup fp32
-  // scratch [2][128][8], when it fits; otherwise packed-FFMA2 dot products
-  static constexpr bool SMMA = RM == 8 && 1024 + 2 * STAGE + 2 * XB + 2 * 2 * 128 * 8 * 4 + 128 + 256 <= 232448;
-  static constexpr int SCR = SMMA ? 2 * 128 * 8 * 4 : 0;   // per warpgroup
+  // staircase scores / dP on mma.sync (16 x 8 blocks per horizon) through a per-warpgroup fp32
+  // scratch [128][RM] (S, then dP), when it fits; otherwise packed-FFMA2 dot products
+  static constexpr bool SMMA = 1024 + 2 * STAGE + 2 * XB + 2 * 128 * RM * 4 + 128 + 256 <= 232448;
+  // both products in one pass through a [2][128][RM] scratch when that fits too (R <= 8)
+  static constexpr bool SFUSE = SMMA && 1024 + 2 * STAGE + 2 * XB + 2 * 2 * 128 * RM * 4 + 128 + 256 <= 232448;
+  static constexpr int SCR = SMMA ? (SFUSE ? 2 : 1) * 128 * RM * 4 : 0;   // per warpgroup
   static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
   static_assert(NB + 192 <= 256, "TMEM columns per item");
   static_assert(SMEM <= 232448, "shared memory");
@@ -636,66 +638,87 @@ __global__ void __launch_bounds__(320, 1)
       LTR(1);
       float sst[RM], dst[RM];
       if constexpr (Cf::SMMA) {
-        // ---- staircase on mma.sync: horizon ih's block S = Q_ih K_ih^T, dP = dO_ih V_ih^T
-        //      (rows c: Q rows c HZ + ih; cols c': stair rows c' HZ + ih), one warp per horizon,
-        //      scattered to the scratch rows r = c HZ + ih, then read back per thread
-        const uint32_t qt = sb, ot = sb + Cf::QB, ks = sb + 2 * Cf::QB + 2 * Cf::KBB, vs = ks + Cf::SB;
+        // ---- staircase on mma.sync: horizon ih's blocks S = Q_ih K_ih^T, then dP = dO_ih V_ih^T
+        //      (rows c: Q rows c HZ + ih; cols c': stair rows c' HZ + ih; ceil(C/16) x RM/8 blocks of
+        //      16 x 8), two horizons per warp iteration, scattered to the scratch rows r = c HZ + ih
+        //      and read back per thread (S pass, then dP pass through the same scratch)
+        const uint32_t ks = sb + 2 * Cf::QB + 2 * Cf::KBB, vs = ks + Cf::SB;
         const uint32_t za = tc::smem_u32(zrow), sca = tc::smem_u32(scr);
         const int gq = lane >> 2, t4 = lane & 3;
-        // two horizons per iteration (ih, ih + 4): independent accumulator chains for ILP
-        for (int ih0 = wq; ih0 < HZ; ih0 += 8) {
-          float sacc[2][4] = {}, dacc[2][4] = {};
-          const int am = lane & 15, bn = lane & 7;
+        const int nmb = (C + 15) / 16;
+        // SFUSE: one pass computing both products (scratch halves); else S pass, then dP pass
+        constexpr int NPASS = Cf::SFUSE ? 1 : 2, NPROD = Cf::SFUSE ? 2 : 1;
+        constexpr uint32_t HALF = 128 * RM * 4;
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            const int ih = ih0 + 4 * u2;
-            const bool hv = ih < HZ;
-            const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
+        for (int pass = 0; pass < NPASS; ++pass) {
+          for (int ih0 = wq; ih0 < HZ; ih0 += 8) {
+            for (int mb = 0; mb < nmb; ++mb) {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
-              const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
-              const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
-              uint32_t aq[4], ad[4], bk[2], bv[2];
-              ldsm_x4(arow < 0 ? za : qt + ao, aq);
-              ldsm_x4(arow < 0 ? za : ot + ao, ad);
-              ldsm_x2(brow < 0 ? za : ks + bo, bk);
-              ldsm_x2(brow < 0 ? za : vs + bo, bv);
-              mma16816(sacc[u2], aq, bk);
-              mma16816(dacc[u2], ad, bv);
-            }
-          }
+              for (int nb = 0; nb < RM / 8; ++nb) {
+                float acc[NPROD][2][4] = {};
+                const int am = 16 * mb + (lane & 15), bn = 8 * nb + (lane & 7);
 #pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            const int ih = ih0 + 4 * u2;
-            if (ih >= HZ) break;
+                for (int u2 = 0; u2 < 2; ++u2) {
+                  const int ih = ih0 + 4 * u2;
+                  const bool hv = ih < HZ;
+                  const int arow = (hv && am < C) ? am * HZ + ih : -1, brow = (hv && bn < R) ? bn * HZ + ih : -1;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int cc = gq + 8 * (e >> 1), cp = 2 * t4 + (e & 1);
-              if (cc < C) {
-                const uint32_t o = (uint32_t)((cc * HZ + ih) * 8 + cp) * 4;
-                tc::st_shared_u32(sca + o, __float_as_uint(sacc[u2][e]));
-                tc::st_shared_u32(sca + 4096 + o, __float_as_uint(dacc[u2][e]));
+                  for (int kk = 0; kk < 4; ++kk) {
+                    const int ach = 2 * kk + (lane >> 4), bch = 2 * kk + ((lane >> 3) & 1);
+                    const uint32_t ao = arow < 0 ? 0u : (uint32_t)(arow * 128 + ((ach ^ (arow & 7)) << 4));
+                    const uint32_t bo = brow < 0 ? 0u : (uint32_t)(brow * 128 + ((bch ^ (brow & 7)) << 4));
+#pragma unroll
+                    for (int pr = 0; pr < NPROD; ++pr) {
+                      const int pp = pass + pr;                  // 0: Q . K_stair, 1: dO . V_stair
+                      uint32_t af[4], bf[2];
+                      ldsm_x4(arow < 0 ? za : sb + pp * Cf::QB + ao, af);
+                      ldsm_x2(brow < 0 ? za : (pp ? vs : ks) + bo, bf);
+                      mma16816(acc[pr][u2], af, bf);
+                    }
+                  }
+                }
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2) {
+                  const int ih = ih0 + 4 * u2;
+                  if (ih >= HZ) break;
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int cc = 16 * mb + gq + 8 * (e >> 1), cp = 8 * nb + 2 * t4 + (e & 1);
+                    if (cc < C) {
+#pragma unroll
+                      for (int pr = 0; pr < NPROD; ++pr)
+                        tc::st_shared_u32(sca + pr * HALF + (uint32_t)((cc * HZ + ih) * RM + cp) * 4,
+                                          __float_as_uint(acc[pr][u2][e]));
+                    }
+                  }
+                }
               }
             }
           }
-        }
-        tc::named_bar(1 + wg, 128);
-        {
-          const uint32_t o = sca + (uint32_t)r * 32;
-          const uint4 s0 = tc::ld_shared_v4(o), s1 = tc::ld_shared_v4(o + 16);
-          const uint4 d0 = tc::ld_shared_v4(o + 4096), d1 = tc::ld_shared_v4(o + 4096 + 16);
-          const uint32_t sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-          const uint32_t dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+          tc::named_bar(1 + wg, 128);
+          const uint32_t o = sca + (uint32_t)r * RM * 4;
 #pragma unroll
-          for (int cp = 0; cp < RM; ++cp) {
-            const int f = h - cp;
-            const bool ok = row_ok && cp < R && f >= 0 && f < T;
-            sst[cp] = ok ? tc::ex2(fmaf(__uint_as_float(sv[cp]), a.scale_log2, -lse2)) : 0.f;
-            dst[cp] = __uint_as_float(dv[cp]);
+          for (int pr = 0; pr < NPROD; ++pr) {
+            const int pp = pass + pr;
+#pragma unroll
+            for (int q = 0; q < RM / 4; ++q) {
+              const uint4 s4 = tc::ld_shared_v4(o + pr * HALF + 16 * q);
+              const uint32_t sv[4] = {s4.x, s4.y, s4.z, s4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int cp = 4 * q + e;
+                if (pp == 0) {
+                  const int f = h - cp;
+                  const bool ok = row_ok && cp < R && f >= 0 && f < T;
+                  sst[cp] = ok ? tc::ex2(fmaf(__uint_as_float(sv[e]), a.scale_log2, -lse2)) : 0.f;
+                } else {
+                  dst[cp] = __uint_as_float(sv[e]);
+                }
+              }
+            }
           }
+          tc::named_bar(1 + wg, 128);   // the scratch is rewritten (dP pass / next item)
         }
-        tc::named_bar(1 + wg, 128);   // the scratch is rewritten by this warpgroup's next item
       } else {
       // ---- staircase scores and dP on CUDA cores: key (h - c', c') = stair row c' HZ + i; two
       //      passes (q . k_stair, then dO . v_stair) so one 64-float row is live at a time

@@ -3,7 +3,8 @@ import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2302_13451_b200 as s
-B, H, T, D, L, R = 8, 12, 1750, 64, 32, 8
+B, H, T, D, L = 8, 12, 1750, 64, 32
+R = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 C = R + 1
 N = 4
 x = [[torch.randn(C, B, H, T, D, device="cuda").to(torch.bfloat16) for _ in range(4)] for _ in range(N)]
