@@ -70,12 +70,22 @@ typedef struct {
 sattn_status sa_forward(const sattn_desc* desc, const void* Q, const void* K, const void* V,
                         void* O, float* LSE, void* stream);
 
+/* sa_forward_ws: sa_forward with a workspace of >= sa_forward_workspace(desc) bytes (0 when none
+ * is needed).  Bands wider than the narrow tensor-core kernels (bf16, D = 64, W = L+R+1 > 65: the
+ * paper's Fig. 5 sweep reaches W = 490) then also run on tensor cores: the band is
+ * split into ceil(W / 49) sub-bands whose (O, max, sum) rows are merged by log-sum-exp in fp32
+ * (exact softmax over the union); sa_forward keeps such bands on the CUDA-core kernels.        */
+size_t sa_forward_workspace(const sattn_desc* desc);
+sattn_status sa_forward_ws(const sattn_desc* desc, const void* Q, const void* K, const void* V,
+                           void* O, float* LSE, void* ws, size_t ws_bytes, void* stream);
+
 /* sa_backward: exact gradients dQ, dK, dV of <dO, O> (Eq. 7-13 with Eq. 7's
  * index condition, G3).  O and LSE must come from sa_forward on the same
  * inputs (not checked: undefined results otherwise).  ws >= sa_backward_workspace(desc)
  * bytes of device memory (holds delta_t = sum_u P_tu dP_tu, fp32, which equals
  * dO_t . O_t for the exact O: the tensor-core path forms it from P and dP (G26),
- * the CUDA-core path from dO and O).  Deterministic (no atomics): bitwise
+ * the CUDA-core path from dO and O; wide tensor-core bands (W > 65) take delta = dO . O and
+ * sum the sub-bands' gradients in fp32 accumulators also held in ws).  Deterministic (no atomics): bitwise
  * reproducible run to run.                                                    */
 size_t sa_backward_workspace(const sattn_desc* desc);
 sattn_status sa_backward(const sattn_desc* desc, const void* Q, const void* K, const void* V,

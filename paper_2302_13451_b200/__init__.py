@@ -45,6 +45,8 @@ _PD = ctypes.POINTER(Desc)
 EXPORTS = {
     "sa_forward": (_I, [_PD, _P, _P, _P, _P, _P, _P]),
     "sa_backward_workspace": (_SZ, [_PD]),
+    "sa_forward_workspace": (_SZ, [_PD]),
+    "sa_forward_ws": (_I, [_PD, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_backward": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_p_ld": (ctypes.c_int64, [_PD]),
     "sa_forward_p": (_I, [_PD, _P, _P, _P, _P, _P, _P, _P]),
@@ -157,6 +159,12 @@ def sa_forward(q, k, v, L: int, R: int, scale=None, impl="auto"):
     d = _desc_from(q, L, R, scale, impl)
     o = torch.empty_like(q)
     lse = torch.empty(q.shape[:-1], device=q.device, dtype=torch.float32)
+    nws = lib().sa_forward_workspace(ctypes.byref(d))
+    if nws:   # wide bands on tensor cores (sub-bands merged by log-sum-exp)
+        ws = torch.empty(nws, device=q.device, dtype=torch.uint8)
+        _check(lib().sa_forward_ws(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _ptr(ws), nws,
+                                   _stream()), "sa_forward_ws")
+        return o, lse
     _check(lib().sa_forward(ctypes.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), _stream()), "sa_forward")
     return o, lse
 

@@ -202,12 +202,21 @@ sattn_status attn_forward(const sattn_desc* d, bool llsa, const void* Q, const v
   return ffma_forward(d, llsa, a, st);
 }
 
+bool wide_tc(const sattn_desc* d, bool llsa) {
+  return !llsa && d->impl != SATTN_IMPL_FFMA && tc_wide_supported(d->dtype, (int)d->D, d->L, d->R);
+}
+
 size_t attn_bwd_ws(const sattn_desc* d, bool llsa) {
   // delta and LSE*log2(e) (+ for LLSA the staircase part of delta), fp32, per channel, rows
-  // padded to a multiple of 4 frames (16-byte TMA rows)
+  // padded to a multiple of 4 frames (16-byte TMA rows); wide SA bands on tensor cores: + the
+  // fp32 dQ / dK / dV accumulators of the sub-band launches
   const size_t C = llsa ? d->R + 1 : 1;
   const size_t Tp = (size_t)((d->T + 3) & ~3LL);
   const size_t rows = (llsa ? 3 : 2) * C * d->B * d->H * Tp * sizeof(float);
+  if (wide_tc(d, llsa)) {
+    const size_t w = tc_wide_bwd_ws(d->B * d->H, d->T);
+    return w > rows ? w : rows;
+  }
   return rows;
 }
 
@@ -220,12 +229,20 @@ sattn_status attn_backward(const sattn_desc* d, bool llsa, const void* Q, const 
     if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
   if (ws_bytes < attn_bwd_ws(d, llsa))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, attn_bwd_ws(d, llsa));
-  if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true))
+  if (d->impl == SATTN_IMPL_TC && !tc_ok(d, llsa, true) && !wide_tc(d, llsa))
     return fail(SATTN_EUNSUPPORTED, llsa ? "tensor-core LLSA backward needs bf16, D=64, L <= 48 and 1 <= R <= 8 (R <= 16 for dense inputs)"
                                          : "tensor-core SA backward needs bf16, D=64, L+R+1 <= 65");
   AttnArgs a = make_args(d, llsa);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
+  if (wide_tc(d, llsa)) {
+    sattn_status r = tc_backward_wide(a, st);
+    if (r != SATTN_OK) return fail(r, "tc_backward_wide: %s", tc_last_error());
+    g_launches.fetch_add(4 + 2 * tc_wide_parts(d->L, d->R), std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_backward_wide launch: %s", cudaGetErrorString(e));
+    return SATTN_OK;
+  }
   if (use_tc(d, llsa, true)) {
     sattn_status r = llsa ? tc_llsa_backward(a, st) : tc_backward(a, st);
     if (r != SATTN_OK) return fail(r, "tc_backward: %s", tc_last_error());
@@ -312,6 +329,32 @@ sattn_status sa_forward(const sattn_desc* d, const void* Q, const void* K, const
 }
 
 size_t sa_backward_workspace(const sattn_desc* d) { return validate(d) == SATTN_OK ? attn_bwd_ws(d, false) : 0; }
+
+size_t sa_forward_workspace(const sattn_desc* d) {
+  if (validate(d) != SATTN_OK) return 0;
+  return wide_tc(d, false) ? tc_wide_fwd_ws(d->B * d->H, d->T) : 0;
+}
+
+sattn_status sa_forward_ws(const sattn_desc* d, const void* Q, const void* K, const void* V, void* O, float* LSE,
+                           void* ws, size_t ws_bytes, void* stream) {
+  sattn_status r = validate(d);
+  if (r != SATTN_OK) return r;
+  if (!wide_tc(d, false)) return attn_forward(d, false, Q, K, V, O, LSE, (cudaStream_t)stream);
+  if (!Q || !K || !V || !O || !LSE || !ws) return fail(SATTN_EARG, "NULL pointer");
+  const void* ps[] = {Q, K, V, O, LSE, ws};
+  for (const void* p : ps)
+    if (!aligned16(p)) return fail(SATTN_EARG, "pointers must be 16-byte aligned");
+  if (ws_bytes < sa_forward_workspace(d))
+    return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, sa_forward_workspace(d));
+  AttnArgs a = make_args(d, false);
+  a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE;
+  r = tc_forward_wide(a, ws, (cudaStream_t)stream);
+  if (r != SATTN_OK) return fail(r, "tc_forward_wide: %s", tc_last_error());
+  g_launches.fetch_add(1 + tc_wide_parts(d->L, d->R), std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_forward_wide launch: %s", cudaGetErrorString(e));
+  return SATTN_OK;
+}
 
 sattn_status sa_backward(const sattn_desc* d, const void* Q, const void* K, const void* V, const void* O,
                          const float* LSE, const void* dO, void* dQ, void* dK, void* dV, void* ws, size_t ws_bytes,

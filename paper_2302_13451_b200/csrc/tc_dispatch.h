@@ -13,6 +13,13 @@ sattn_status tc_backward(const AttnArgs& a, cudaStream_t st);
 // phase bit 0: K1 (dQ, delta) over the args' query-tile subset; bit 1: K2 (dK, dV) over every tile
 sattn_status tc_backward_phase(const AttnArgs& a, cudaStream_t st, int phase);
 int tc_backward_launches();
+// wide bands (W > 65) as log-sum-exp-merged sub-bands of the narrow tensor-core kernels
+bool tc_wide_supported(int dtype, int D, int L, int R);
+int tc_wide_parts(int L, int R);
+size_t tc_wide_fwd_ws(long long BH, long long T);
+size_t tc_wide_bwd_ws(long long BH, long long T);
+sattn_status tc_forward_wide(const AttnArgs& a, void* ws, cudaStream_t st);
+sattn_status tc_backward_wide(const AttnArgs& a, cudaStream_t st);
 int tc_key_box_rows(int L, int R);   // rows of the K / V box a query tile loads (NK)
 size_t tc_backward_ws_bytes();
 bool tc_p_supported(int dtype, int D, int L, int R, bool backward);   // stored-band mode (NEXT-4)

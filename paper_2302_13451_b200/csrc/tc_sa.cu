@@ -75,7 +75,25 @@ struct TcArgs {
   // query tiles of this launch per head: kt = kt0 + i + (i >= kt_split ? kt_jump : 0), i < nkt
   // (all tiles: kt0 = 0, nkt = ceil(T/128); a time shard launches interior and edge tiles apart)
   int nkt, kt0, kt_split, kt_jump;
+  // wide bands (W > 65) as sub-bands of the narrow kernels, accumulated in fp32 (ACC instances):
+  // forward (o, m, l) rows merged by log-sum-exp; K1 dQ / K2 dK, dV rows summed; K1 reads the
+  // global delta = dO . O from ws_del instead of forming it over its sub-band (G28)
+  float *acc_o, *acc_m, *acc_l;                  // [BH][T][64], [BH][T], [BH][T]
+  float *acc_dq, *acc_dk, *acc_dv;               // [BH][T][64]
+  int acc_first;                                 // first sub-band: store instead of merge / add
 };
+
+// r += s * v (or r = s * v when first) for one 64-float fp32 row in global memory
+__device__ __forceinline__ void acc_row64(float* row, const float* v, float s, bool first) {
+  float4* d = reinterpret_cast<float4*>(row);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    float4 x = first ? make_float4(0.f, 0.f, 0.f, 0.f) : d[c];
+    x.x = fmaf(v[4 * c], s, x.x); x.y = fmaf(v[4 * c + 1], s, x.y);
+    x.z = fmaf(v[4 * c + 2], s, x.z); x.w = fmaf(v[4 * c + 3], s, x.w);
+    d[c] = x;
+  }
+}
 
 __device__ __forceinline__ int tile_t0(int i, const TcArgs& a) {
   return (a.kt0 + i + (i >= a.kt_split ? a.kt_jump : 0)) * 128;
@@ -201,7 +219,7 @@ __device__ __forceinline__ void tmem_row64_to_smem_sw128(uint32_t taddr, float s
 // PST: the stored-band mode (NEXT-4) -- the softmax warpgroup also writes its row of
 // a_t (bf16, band layout [BH][T][ldp], zeros outside the clipped window) through the O staging
 // tile and a TMA store (tmP: box (ldp, 128, 1)) before the O epilogue.
-template <int CW, bool PST = false>
+template <int CW, bool PST = false, bool ACC = false>
 __global__ void __launch_bounds__(320, 1)
     sa_fwd_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
               const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
@@ -378,6 +396,40 @@ __global__ void __launch_bounds__(320, 1)
       if (tr) trace_at(a.trace, 6, k);
       __syncwarp();
       tc::tc_fence_after();
+      if constexpr (ACC) {
+        // sub-band of a wide band: merge (o, m, l) into the fp32 accumulator rows (log-sum-exp)
+        float v[64];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tc::tmem_ld16(pa + NK + 16 * j, v + 16 * j);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tfree[b]);
+        if (t < T) {
+          const long long row = (long long)bh * T + t;
+          const float mn = l > 0.f ? m : neg_inf();          // no valid key in this sub-band: weight 0
+          const float mo = a.acc_first ? neg_inf() : a.acc_m[row];
+          const float M = fmaxf(mo, mn);
+          if (M != neg_inf()) {
+            const float wo = a.acc_first ? 0.f : tc::ex2((mo - M) * a.scale_log2);
+            const float wn = tc::ex2((mn - M) * a.scale_log2);
+            float4* d = reinterpret_cast<float4*>(a.acc_o + row * 64);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              float4 x = a.acc_first ? make_float4(0.f, 0.f, 0.f, 0.f) : d[c];
+              x.x = fmaf(v[4 * c], wn, x.x * wo); x.y = fmaf(v[4 * c + 1], wn, x.y * wo);
+              x.z = fmaf(v[4 * c + 2], wn, x.z * wo); x.w = fmaf(v[4 * c + 3], wn, x.w * wo);
+              d[c] = x;
+            }
+            a.acc_l[row] = (a.acc_first ? 0.f : a.acc_l[row] * wo) + l * wn;
+            a.acc_m[row] = M;
+          } else if (a.acc_first) {
+            a.acc_m[row] = neg_inf();
+            a.acc_l[row] = 0.f;
+          }
+        }
+        if (tr) trace_at(a.trace, 7, k);
+        continue;
+      }
       if (leader) tc::bulk_wait_read0();        // the previous TMA store has read the staging tile
       tc::named_bar(1 + wg, 128);
       tmem_row64_to_smem_sw128(pa + NK, 1.f / l, ostage, r);
@@ -445,7 +497,7 @@ template <int CW> struct DqCfg {
 
 // PST (stored-band mode): tmQ maps the band P [BH][T][ldp] (box (ldp, 128, 1)) and the tile's
 // P rows are staged in the Q slot; no S MMA, no exponentials: the warpgroup reads P from smem.
-template <int CW, bool PST = false>
+template <int CW, bool PST = false, bool ACC = false>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dq_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -655,14 +707,16 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_wait(&dpfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
-      float delta = dx;
+      // ACC (sub-band of a wide band): the global delta = dO . O, precomputed in ws_del
+      float delta = ACC ? (row_ok ? a.ws_del[cbh * a.Tp + t] : 0.f) : dx;
       if constexpr (CW <= 72) {   // dP held in registers
         float dp[CW];
 #pragma unroll
         for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + 32 * q4 + 8 * j, dp + 8 * j);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < CW; ++i) delta = fmaf(p[i], dp[i], delta);
+        if constexpr (!ACC)
+          for (int i = 0; i < CW; ++i) delta = fmaf(p[i], dp[i], delta);
 #pragma unroll
         for (int i = 0; i < CW; ++i) p[i] *= dp[i] - delta;
       } else {                    // wide bands: read dP from TMEM twice instead of spilling
@@ -672,7 +726,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tmem_ld8(x + 32 * q4 + 8 * j, dp);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 8; ++e) delta = fmaf(p[8 * j + e], dp[e], delta);
+          for (int e = 0; e < 8; ++e) delta = ACC ? delta : fmaf(p[8 * j + e], dp[e], delta);
         }
 #pragma unroll
         for (int j = 0; j < CW / 8; ++j) {
@@ -692,13 +746,21 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_arrive(&dsfull[b]);
       // padded rows for K2's TMA loads; rows in [T, Tp) get zeros
       if (t < a.Tp) {
-        a.ws_del[cbh * a.Tp + t] = row_ok ? delta : 0.f;
+        if (!ACC) a.ws_del[cbh * a.Tp + t] = row_ok ? delta : 0.f;
         if (!PST) a.ws_l2[cbh * a.Tp + t] = row_ok ? lse2 : 0.f;
       }
       // dQ epilogue
       tc::mbar_wait(&dqfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
+      if constexpr (ACC) {
+        float v[64];
+        tmem_ld64(x + NK, v);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&tfree[b]);
+        if (row_ok) acc_row64(a.acc_dq + ((long long)bh * T + t) * 64, v, a.scale, a.acc_first);
+        continue;
+      }
       if (leader) tc::bulk_wait_read0();
       tc::named_bar(1 + wg, 128);
       tmem_row64_to_smem_sw128(x + NK, a.scale, ostage, r);
@@ -750,7 +812,7 @@ template <int CW> struct DkvCfg {
 // PST (stored-band mode): tmK maps the band P [BH][T][ldp] with box (ldp, NQ, 1); the stage is
 // [P window | V | Q | dO | delta]; no S MMA, no LSE, no exponentials: the warpgroup reads
 // P^T[u][n] = P[n][u - n + L] from the staged rows.
-template <int CW, bool PST = false>
+template <int CW, bool PST = false, bool ACC = false>
 __global__ void __launch_bounds__(320, 1)
     sa_bwd_dkdv_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
@@ -1019,6 +1081,20 @@ __global__ void __launch_bounds__(320, 1)
       if (tr) trace_at(a.trace, 6, k);
       __syncwarp();
       tc::tc_fence_after();
+      if constexpr (ACC) {   // sub-band of a wide band: add into the fp32 dK / dV rows
+        float dvr[64], dkr[64];
+        tmem_ld64(DV + lanes, dvr);
+        tmem_ld64(DK + lanes, dkr);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&kvfree[b]);
+        const int u = u0 + r;
+        if (u < T) {
+          const long long row = (long long)bh * T + u;
+          acc_row64(a.acc_dv + row * 64, dvr, 1.f, a.acc_first);
+          acc_row64(a.acc_dk + row * 64, dkr, a.scale, a.acc_first);
+        }
+        continue;
+      }
       if (leader) tc::bulk_wait_read0();
       tc::named_bar(1 + wg, 128);
       if constexpr (ONE) {
@@ -1874,19 +1950,25 @@ int num_sms() {
   return n;
 }
 
-template <int CW, bool PST = false>
-sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st) {
+struct WideAcc {   // fp32 accumulators of a wide band's sub-band launches (ACC instances)
+  float *o, *m, *l, *dq, *dk, *dv;
+  int first;
+};
+
+template <int CW, bool PST = false, bool ACC = false>
+sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st, const WideAcc* wa = nullptr) {
   using C = FwdCfg<CW, PST>;
   TcArgs ta = tc_args(a);
+  if (wa) { ta.acc_o = wa->o; ta.acc_m = wa->m; ta.acc_l = wa->l; ta.acc_first = wa->first; }
   CUtensorMap mq, mk, mv, mo, mp;
   if (!make_map(&mq, a.Q, a.T, a.BH, kM, a.ld) || !make_map(&mk, a.K, a.T, a.BH, C::NK, a.ld) ||
       !make_map(&mv, a.V, a.T, a.BH, C::NK, a.ld) || !make_map(&mo, a.Out, a.T, a.BH, kM, a.ld))
     return SATTN_ECUDA;
   if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
-  set_smem(sa_fwd_tc<CW, PST>, C::SMEM);
+  set_smem(sa_fwd_tc<CW, PST, ACC>, C::SMEM);
   const int ntiles = ta.nkt * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  launch_pdl(sa_fwd_tc<CW, PST>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, PST ? mp : mo, ta);
+  launch_pdl(sa_fwd_tc<CW, PST, ACC>, dim3(grid), dim3(C::THREADS), C::SMEM, st, mq, mk, mv, mo, PST ? mp : mo, ta);
   return SATTN_OK;
 }
 
@@ -1931,6 +2013,87 @@ sattn_status bwd_launch(const AttnArgs& a, cudaStream_t st, int phase = 3) {
                mdoN, mdk, mdv, ml2, mdel, tc_args(a));
   }
   return SATTN_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// wide bands (W > 65: NEXT-1, the Fig. 5 sweep to W = 490) on the tensor-core kernels.  The band
+// [t - L, t + R] is split into S sub-bands of width <= 49; sub-band j (offsets o_j .. o_j + w_j - 1
+// from t - L) is an SA band of its own with (L_j, R_j) = (L - o_j, o_j + w_j - 1 - L), either of
+// which may be negative.  Softmax over the union is exact by the log-sum-exp merge of the
+// sub-bands' (o, m, l) (forward; the split-K combine), and the gradient is exactly the sum of the
+// sub-bands' gradients when each uses the global LSE and delta = dO . O (Eq. 9; G28), so every
+// sub-band runs the narrow kernels' ACC instances into fp32 accumulators, then one kernel rounds.
+// ------------------------------------------------------------------------------------------
+constexpr int kWideSub = 49;   // sub-band width: the two-stage K2's limit
+
+__global__ void wide_delta_kernel(const bf16* dO, const bf16* O, float* del, int T, int Tp, long long nrows) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nrows; i += (long long)gridDim.x * blockDim.x) {
+    const long long bh = i / Tp;
+    const int t = (int)(i - bh * Tp);
+    float s = 0.f;
+    if (t < T) {
+      const uint4* a = reinterpret_cast<const uint4*>(dO + (bh * T + t) * 64);
+      const uint4* b = reinterpret_cast<const uint4*>(O + (bh * T + t) * 64);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) s += dot8_bf16(a[c], b[c]);
+    }
+    del[i] = s;
+  }
+}
+
+__global__ void wide_fwd_finalize(const float* acc_o, const float* acc_m, const float* acc_l, bf16* O, float* LSE,
+                                  float scale, long long nrows) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nrows; i += (long long)gridDim.x * blockDim.x) {
+    const float l = acc_l[i];
+    float v[64];
+    const float4* s = reinterpret_cast<const float4*>(acc_o + i * 64);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) { const float4 x = s[c]; v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w; }
+    store_row_bf16(O + i * 64, v, 1.f / l);
+    LSE[i] = acc_m[i] * scale + __logf(l);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* a, bf16* o, long long n8) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const float4 x = reinterpret_cast<const float4*>(a)[2 * i], y = reinterpret_cast<const float4*>(a)[2 * i + 1];
+    reinterpret_cast<uint4*>(o)[i] = make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y),
+                                                pack_bf16(y.z, y.w));
+  }
+}
+
+template <int CW>
+sattn_status bwd_wide_sub(const AttnArgs& a, cudaStream_t st, const WideAcc& wa) {
+  static_assert(DkvCfg<CW>::SMEM <= 232448, "sub-bands use the two-stage K2");
+  constexpr int NK = nk_of(CW);
+  const int Tp = (a.T + 3) & ~3;
+  const float* l2ws = a.delta + (long long)a.BH * Tp;
+  constexpr int NQP = DkvCfg<CW>::NQP;
+  CUtensorMap mq, mk, mv, mdo, mqN, mdoN, mk128, mv128, ml2, mdel;
+  if (!make_map(&mq, a.Q, a.T, a.BH, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) || !make_map(&mv, a.V, a.T, a.BH, NK) ||
+      !make_map(&mdo, a.dO, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, NK) ||
+      !make_map(&mdoN, a.dO, a.T, a.BH, NK) || !make_map(&mk128, a.K, a.T, a.BH, kM) ||
+      !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map_f32_rows(&ml2, l2ws, a.T, Tp, a.BH, NQP) ||
+      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, NQP))
+    return SATTN_ECUDA;
+  TcArgs t = tc_args(a);
+  t.acc_dq = wa.dq; t.acc_dk = wa.dk; t.acc_dv = wa.dv; t.acc_first = wa.first;
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  set_smem(sa_bwd_dq_tc<CW, false, true>, DqCfg<CW>::SMEM);
+  launch_pdl(sa_bwd_dq_tc<CW, false, true>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mq, mk, mv,
+             mdo, mq, t);
+  set_smem(sa_bwd_dkdv_tc<CW, false, true>, DkvCfg<CW>::SMEM);
+  launch_pdl(sa_bwd_dkdv_tc<CW, false, true>, dim3(grid), dim3(DkvCfg<CW>::THREADS), DkvCfg<CW>::SMEM, st, mqN,
+             mk128, mv128, mdoN, mk128, mk128, ml2, mdel, t);
+  return SATTN_OK;
+}
+
+// sub-band j of a band of width W split into S parts: offset and width
+void wide_split(int W, int j, int S, int& o, int& w) {
+  const int base = (W + S - 1) / S;
+  o = j * base;
+  w = W - o < base ? W - o : base;
 }
 
 // LLSA key-major band pass: dK, dV of channel R's keys accumulated over the C query channels
@@ -2046,6 +2209,80 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool tc_wide_supported(int dtype, int D, int L, int R) {
+  return dtype == SATTN_BF16 && D == 64 && L + R + 1 > 65 && L + R + 1 <= 4096;
+}
+int tc_wide_parts(int L, int R) { return (L + R + 1 + kWideSub - 1) / kWideSub; }
+size_t tc_wide_fwd_ws(long long BH, long long T) { return (size_t)BH * T * (64 + 2) * sizeof(float); }
+size_t tc_wide_bwd_ws(long long BH, long long T) {
+  return (size_t)2 * BH * ((T + 3) & ~3LL) * sizeof(float) + (size_t)3 * BH * T * 64 * sizeof(float);
+}
+
+sattn_status tc_forward_wide(const AttnArgs& a, void* ws, cudaStream_t st) {
+  const int W = a.L + a.R + 1, S = tc_wide_parts(a.L, a.R);
+  const long long rows = (long long)a.BH * a.T;
+  WideAcc wa{};
+  wa.o = static_cast<float*>(ws);
+  wa.m = wa.o + rows * 64;
+  wa.l = wa.m + rows;
+  for (int j = 0; j < S; ++j) {
+    int o, w;
+    wide_split(W, j, S, o, w);
+    AttnArgs aj = a;
+    aj.L = a.L - o;
+    aj.R = o + w - 1 - a.L;
+    wa.first = j == 0;
+    sattn_status r;
+    switch (cw_of(w)) {
+      case 32: r = fwd_launch<32, false, true>(aj, st, &wa); break;
+      case 48: r = fwd_launch<48, false, true>(aj, st, &wa); break;
+      case 64: r = fwd_launch<64, false, true>(aj, st, &wa); break;
+      case 72: r = fwd_launch<72, false, true>(aj, st, &wa); break;
+      case 80: r = fwd_launch<80, false, true>(aj, st, &wa); break;
+      default: g_tc_err = "wide sub-band"; return SATTN_EUNSUPPORTED;
+    }
+    if (r != SATTN_OK) return r;
+  }
+  wide_fwd_finalize<<<4 * num_sms(), 128, 0, st>>>(wa.o, wa.m, wa.l, reinterpret_cast<bf16*>(a.Out), a.LSEout, a.scale,
+                                                   rows);
+  return SATTN_OK;
+}
+
+sattn_status tc_backward_wide(const AttnArgs& a, cudaStream_t st) {
+  const int W = a.L + a.R + 1, S = tc_wide_parts(a.L, a.R);
+  const long long rows = (long long)a.BH * a.T;
+  const int Tp = (a.T + 3) & ~3;
+  WideAcc wa{};
+  wa.dq = a.delta + 2LL * a.BH * Tp;
+  wa.dk = wa.dq + rows * 64;
+  wa.dv = wa.dk + rows * 64;
+  wide_delta_kernel<<<4 * num_sms(), 256, 0, st>>>(reinterpret_cast<const bf16*>(a.dO), reinterpret_cast<const bf16*>(a.O),
+                                                   a.delta, a.T, Tp, (long long)a.BH * Tp);
+  for (int j = 0; j < S; ++j) {
+    int o, w;
+    wide_split(W, j, S, o, w);
+    AttnArgs aj = a;
+    aj.L = a.L - o;
+    aj.R = o + w - 1 - a.L;
+    wa.first = j == 0;
+    sattn_status r;
+    switch (cw_of(w)) {
+      case 32: r = bwd_wide_sub<32>(aj, st, wa); break;
+      case 48: r = bwd_wide_sub<48>(aj, st, wa); break;
+      case 64: r = bwd_wide_sub<64>(aj, st, wa); break;
+      case 72: r = bwd_wide_sub<72>(aj, st, wa); break;
+      case 80: r = bwd_wide_sub<80>(aj, st, wa); break;
+      default: g_tc_err = "wide sub-band"; return SATTN_EUNSUPPORTED;
+    }
+    if (r != SATTN_OK) return r;
+  }
+  const long long n8 = rows * 64 / 8;
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dq, reinterpret_cast<bf16*>(a.dQ), n8);
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dk, reinterpret_cast<bf16*>(a.dK), n8);
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dv, reinterpret_cast<bf16*>(a.dV), n8);
+  return SATTN_OK;
+}
 
 bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward) {
   if (llsa || dtype != SATTN_BF16 || D != 64) return false;

@@ -67,7 +67,9 @@ def test_sa_fp32(shape, L, R, impl):
 
 
 SA_BF16 = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16),
-           ((1, 2, 600, 64), 32, 32), ((1, 2, 300, 64), 200, 150), ((1, 3, 777, 64), 32, 8), ((1, 1, 50, 16), 5, 2)]
+           ((1, 2, 600, 64), 32, 32), ((1, 2, 300, 64), 200, 150), ((1, 3, 777, 64), 32, 8), ((1, 1, 50, 16), 5, 2),
+           # wide bands on tensor cores (sub-bands merged by log-sum-exp): Fig. 5's top end W = 490, asymmetric
+           ((1, 2, 1000, 64), 245, 244), ((2, 3, 600, 64), 100, 30), ((1, 2, 257, 64), 0, 90)]
 
 
 @pytest.mark.parametrize("shape,L,R", SA_BF16)
@@ -136,6 +138,28 @@ def test_llsa(dt, shape, L, R, broadcast):
     G = oracle.llsa.llsa_backward(Q, K, V, do, L, R)
     for name, got, ref in (("O", o, O), ("LSE", lse, LSE), ("dQ", dq, G[0]), ("dK", dk, G[1]), ("dV", dv, G[2])):
         assert excess(got, ref, dt, name) <= 0, (name, maxerr(got, ref))
+
+
+def test_wide_band_tensor_core_path_deterministic():
+    # W > 65 on tensor cores: the launch count shows the sub-band kernels ran (not the CUDA-core
+    # fallback), and the fp32 sub-band accumulation is bitwise reproducible run to run
+    s = sattn()
+    shape, L, R = (1, 2, 1000, 64), 245, 244
+    q, k, v = synth.qkv(7, shape, "bf16")
+    do = synth.grad_out(7, shape, "bf16")
+    tq, tk, tv, tdo = (dev(x, "bf16") for x in (q, k, v, do))
+    n0 = s.launch_count()
+    o, lse = s.sa_forward(tq, tk, tv, L, R)
+    nf = s.launch_count() - n0
+    g1 = s.sa_backward(tq, tk, tv, o, lse, tdo, L, R)
+    nb = s.launch_count() - n0 - nf
+    S = -(-(L + R + 1) // 49)
+    assert nf == S + 1 and nb == 2 * S + 4, (nf, nb)
+    o2, lse2 = s.sa_forward(tq, tk, tv, L, R)
+    g2 = s.sa_backward(tq, tk, tv, o2, lse2, tdo, L, R)
+    assert torch.equal(o, o2) and torch.equal(lse, lse2)
+    for a, b in zip(g1, g2):
+        assert torch.equal(a, b)
 
 
 def test_deterministic_bitwise():
