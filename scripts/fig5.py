@@ -3,7 +3,8 @@
 d_k = 64, N_T = 1000 frames, H in {8, 16} heads, receptive field W = A + B + 1 = 10 ... 490 in
 steps of 10 (look-back B = ceil((W-1)/2), look-ahead A = floor((W-1)/2)), 5 repeats, mean.
 For each point: peak device memory of one SA forward + backward through the C ABI (bf16; the
-tensor-core kernels for W <= 65, the CUDA-core kernels beyond) per training vector (frame),
+tensor-core kernels at every W: W <= 65 in one launch, wider bands as log-sum-exp-merged sub-bands
+of width <= 49) per training vector (frame),
 and its time, for both SA modes -- LSE + recompute (sa_forward / sa_backward) and the paper's own
 stored band a_t (sa_forward_p / sa_backward_p; tensor cores for W <= 49) -- next to masked
 acausal attention (MAA) as PyTorch computes it (dense T x T scores,
@@ -71,7 +72,7 @@ def run(H, B=8):
         m_sb, t_sb = measure(sa_band)
         m_maa, t_maa = measure(maa)
         frames = B * T
-        rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 65 else "ffma",
+        rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 65 else f"tcgen05 x {-(-W // 49)} sub-bands",
                      "band_kernels": "tcgen05" if W <= 49 else ("tcgen05 fwd + ffma bwd" if W <= 64 else "ffma"),
                      "sa_bytes_per_frame": m_sa / frames, "maa_bytes_per_frame": m_maa / frames,
                      "sa_band_bytes_per_frame": m_sb / frames,
@@ -85,16 +86,21 @@ def main():
            "T": T, "D": D, "B": 8, "repeats": REP, "dtype": "bf16", "rows": []}
     for H in (8, 16):
         out["rows"] += run(H)
-    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r1", "fig5.json")
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r2", "fig5.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
     json.dump(out, open(path, "w"), indent=1)
-    print("| H | W | kernels (lse / band) | SA KB/frame | SA-band KB/frame | MAA KB/frame | SA ms | SA-band ms | MAA ms |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    lines = ["| H | W | kernels (lse / band) | SA KB/frame | SA-band KB/frame | MAA KB/frame | SA ms | SA-band ms | MAA ms |",
+             "|---|---|---|---|---|---|---|---|---|"]
     for r in out["rows"]:
-        if r["W"] in (10, 20, 40, 50, 100, 200, 300, 490):
-            print(f"| {r['H']} | {r['W']} | {r['kernels']} / {r['band_kernels']} | {r['sa_bytes_per_frame'] / 1024:.1f} | "
-                  f"{r['sa_band_bytes_per_frame'] / 1024:.1f} | {r['maa_bytes_per_frame'] / 1024:.1f} | "
-                  f"{r['sa_ms']:.3f} | {r['sa_band_ms']:.3f} | {r['maa_ms']:.3f} |")
+        if r["W"] in (10, 20, 40, 50, 70, 100, 150, 200, 300, 400, 490):
+            lines.append(f"| {r['H']} | {r['W']} | {r['kernels']} / {r['band_kernels']} | {r['sa_bytes_per_frame'] / 1024:.1f} | "
+                         f"{r['sa_band_bytes_per_frame'] / 1024:.1f} | {r['maa_bytes_per_frame'] / 1024:.1f} | "
+                         f"{r['sa_ms']:.3f} | {r['sa_band_ms']:.3f} | {r['maa_ms']:.3f} |")
+    slower = [(r["H"], r["W"]) for r in out["rows"] if r["sa_ms"] >= r["maa_ms"]]
+    lines.append("")
+    lines.append(f"SA (LSE mode) slower than MAA at: {slower or 'no W'}")
+    print("\n".join(lines))
+    open(path.replace(".json", ".md"), "w").write("# Fig. 5 sweep on B200 (scripts/fig5.py, round 2)\n\n" + "\n".join(lines) + "\n")
 
 
 if __name__ == "__main__":
