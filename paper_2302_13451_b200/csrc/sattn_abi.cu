@@ -562,7 +562,48 @@ struct sattn_stream {
 };
 
 namespace {
+// the tensor-core step (bf16, D = 64, window <= 64 rows): one warp per (batch, head)
+sattn_status stream_mma_launch(sattn_stream* s, bool sa, const void* x, void* y, long long h, long long last,
+                               cudaStream_t st, bool* launched) {
+  *launched = false;
+  int nrw = 0, nb = 0, nt = 0;
+  size_t smem = 0;
+  if (s->d.dtype != SATTN_BF16 || s->d.D != 64 ||
+      !stream_mma_geometry(sa, s->d.L, s->d.R, s->n_layers, &nrw, &nb, &nt, &smem))
+    return SATTN_OK;
+  StreamMmaArgs a{};
+  a.x_new = static_cast<const bf16*>(x);
+  a.raw = static_cast<bf16*>(s->raw);
+  a.ring = static_cast<bf16*>(s->ring);
+  a.y_out = static_cast<bf16*>(y);
+  a.h = h;
+  a.last = last;
+  a.n_layers = s->n_layers;
+  a.L = s->d.L;
+  a.R = s->d.R;
+  a.BH = (int)(s->d.B * s->d.H);
+  a.nrw = nrw;
+  a.nb = nb;
+  a.scale_log2 = eff_scale(&s->d) * kLog2e;
+  auto go = [&](auto kern) -> sattn_status {
+    set_smem(kern, smem);
+    kern<<<a.BH, 32 * kMmaWarps, smem, st>>>(a);
+    *launched = true;
+    return after_launch(sa ? "sa_stream_mma" : "llsa_stream_mma");
+  };
+  switch (nt) {
+    case 2: return sa ? go(stream_mma_kernel<true, 2>) : go(stream_mma_kernel<false, 2>);
+    case 4: return sa ? go(stream_mma_kernel<true, 4>) : go(stream_mma_kernel<false, 4>);
+    case 6: return sa ? go(stream_mma_kernel<true, 6>) : go(stream_mma_kernel<false, 6>);
+    case 8: return sa ? go(stream_mma_kernel<true, 8>) : go(stream_mma_kernel<false, 8>);
+  }
+  return SATTN_OK;
+}
+
 sattn_status stream_launch(sattn_stream* s, const void* x, void* y, long long h, long long last, cudaStream_t st) {
+  bool done = false;
+  sattn_status r = stream_mma_launch(s, false, x, y, h, last, st, &done);
+  if (r != SATTN_OK || done) return r;
   StreamArgs a{};
   a.x_new = x;
   a.raw = s->raw;
@@ -575,22 +616,25 @@ sattn_status stream_launch(sattn_stream* s, const void* x, void* y, long long h,
   a.R = s->d.R;
   a.BH = (int)(s->d.B * s->d.H);
   a.scale_log2 = eff_scale(&s->d) * kLog2e;
-  size_t smem = stream_smem_bytes((int)s->d.D, a.L, a.R, a.n_layers, elem_size(s->d.dtype));
-  a.preload = 1;
-  if (smem > 160 * 1024) {   // rings too large to stage: each layer reads its ring rows from global memory
-    a.preload = 0;
-    smem = stream_smem_bytes((int)s->d.D, a.L, a.R);
-  }
-  if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
   return dispatch(s->d.D, s->d.dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
     constexpr int D = decltype(dc)::value;
     using T = decltype(tv);
+    size_t smem = stream_smem_bytes<D, T>(a.L, a.R, a.n_layers);
+    a.preload = 1;
+    if (smem > 160 * 1024) {   // rings too large to stage at once: each layer stages its own rows
+      a.preload = 0;
+      smem = stream_smem_bytes<D, T>(a.L, a.R, 1);
+    }
+    if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
     set_smem(llsa_stream_step_kernel<D, T>, smem);
-    llsa_stream_step_kernel<D, T><<<a.BH, 256, smem, st>>>(a);
+    llsa_stream_step_kernel<D, T><<<a.BH, 32 * stream_warps(a.R), smem, st>>>(a);
     return after_launch("llsa_stream_step");
   });
 }
 sattn_status sa_stream_launch(sattn_stream* s, const void* x, void* y, long long h, long long last, cudaStream_t st) {
+  bool done = false;
+  sattn_status r = stream_mma_launch(s, true, x, y, h, last, st, &done);
+  if (r != SATTN_OK || done) return r;
   SAStreamArgs a{};
   a.x_new = x;
   a.ring = s->ring;
@@ -602,18 +646,18 @@ sattn_status sa_stream_launch(sattn_stream* s, const void* x, void* y, long long
   a.R = s->d.R;
   a.BH = (int)(s->d.B * s->d.H);
   a.scale_log2 = eff_scale(&s->d) * kLog2e;
-  size_t smem = sa_stream_smem_bytes((int)s->d.D, a.L, a.R, a.n_layers, elem_size(s->d.dtype));
-  a.preload = 1;
-  if (smem > 160 * 1024) {
-    a.preload = 0;
-    smem = sa_stream_smem_bytes((int)s->d.D, a.L, a.R);
-  }
-  if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
   return dispatch(s->d.D, s->d.dtype, false, [&](auto dc, auto, auto tv) -> sattn_status {
     constexpr int D = decltype(dc)::value;
     using T = decltype(tv);
+    size_t smem = sa_stream_smem_bytes<D, T>(a.L, a.R, a.n_layers);
+    a.preload = 1;
+    if (smem > 160 * 1024) {
+      a.preload = 0;
+      smem = sa_stream_smem_bytes<D, T>(a.L, a.R, 1);
+    }
+    if (smem > 200 * 1024) return fail(SATTN_EUNSUPPORTED, "stream window too large for shared memory");
     set_smem(sa_stream_step_kernel<D, T>, smem);
-    sa_stream_step_kernel<D, T><<<a.BH, 128, smem, st>>>(a);
+    sa_stream_step_kernel<D, T><<<a.BH, kSAStreamThreads, smem, st>>>(a);
     return after_launch("sa_stream_step");
   });
 }

@@ -1383,8 +1383,9 @@ bool fwd_item_ok(const AttnArgs& a) {
 
 bool tc_llsa_supported(int dtype, int D, int L, int R) {
   // one warp per channel of a 4-channel item needs >= 2 items per tile (C >= 5); the P row
-  // (NB + 32 R packed / 2 <= 192 columns) and the 8 staged stair tiles need R <= 8; NB <= 64
-  return dtype == SATTN_BF16 && D == 64 && R >= 4 && R <= kRmax && L + 32 <= 64;
+  // (NB + 32 R packed / 2 <= 192 columns) and the 8 staged stair tiles need R <= 8; the band
+  // MMA's N = 16-rounded 32 + L is instantiated for 48 and 64 (1 <= L <= 32)
+  return dtype == SATTN_BF16 && D == 64 && R >= 4 && R <= kRmax && L >= 1 && L + 32 <= 64;
 }
 
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
