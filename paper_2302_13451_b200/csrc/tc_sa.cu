@@ -517,7 +517,11 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dsfull = dpfull + 2;      // [2] (128)
   uint64_t* dqfull = dsfull + 2;      // [2]
   uint64_t* tfree = dqfull + 2;       // [2] (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfree + 2);
+  // PST: the stage's K region has its own barriers, so that band / dO / V (dead once dP is issued
+  // and the warpgroup has read its band rows) are released before the dQ MMA retires K
+  uint64_t* fullK = tfree + 2;        // [NS]
+  uint64_t* emptyK = fullK + NS;      // [NS]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyK + NS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
@@ -532,7 +536,10 @@ __global__ void __launch_bounds__(320, 1)
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdQ);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], PST ? 1 + 128 : 1);
+      tc::mbar_init(&fullK[i], 1); tc::mbar_init(&emptyK[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&dqfull[i], 1); tc::mbar_init(&tfree[i], 128);
@@ -559,9 +566,14 @@ __global__ void __launch_bounds__(320, 1)
         uint8_t* b0 = stage0 + st * C::STAGE;
         if (k >= NS) tc::mbar_wait(&empty[st], ((k - NS) / NS) & 1);
         if constexpr (PST) {
-          tc::mbar_expect_tx(&full[st], kM * a.ldp * 2 + C::QB + 2 * C::KB);
+          tc::mbar_expect_tx(&full[st], kM * a.ldp * 2 + C::QB + C::KB);
           tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
           tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
+          tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - ksh, bh);
+          if (k >= NS) tc::mbar_wait(&emptyK[st], ((k - NS) / NS) & 1);
+          tc::mbar_expect_tx(&fullK[st], C::KB);
+          tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &fullK[st], 0, t0 - a.L - ksh, bh);
+          continue;
         } else {
         tc::mbar_expect_tx(&full[st], 2 * C::QB + 2 * C::KB);
         if (nch > 1) {   // LLSA: [C][BH][T][64] maps
@@ -586,12 +598,12 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t m = PST ? tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
                                                 tc::smem_u32(&tfree[ndq & 1]), ((ndq + 2) >> 1) & 1,
                                                 tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1,
-                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1)
+                                                tc::smem_u32(&fullK[ndq % NS]), (ndq / NS) & 1)
                                : tc::mbar_test4(tc::smem_u32(&dsfull[ndq & 1]), (ndq >> 1) & 1,
                                           tc::smem_u32(&tfree[ndq & 1]), ((ndq + 2) >> 1) & 1,   // = (ndq-2)>>1 parity
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
                                           tc::smem_u32(&full[ns % NS]), (ns / NS) & 1);
-        if (ndq < ndp && (m & 1) && (ndq < 2 || (m & 2))) {
+        if (ndq < ndp && (m & 1) && (ndq < 2 || (m & 2)) && (!PST || (m & 8))) {
           tc::tc_fence_after();
           const int b = ndq & 1, st = ndq % NS;
           const uint32_t x = tbase + b * 256;
@@ -605,7 +617,7 @@ __global__ void __launch_bounds__(320, 1)
               tc::mma_bf16_ts(x + NK, x + NK / 2 + 8 * j, tc::desc_mnmajor_sw128(kk + 2048 * j), idQ, true);
           }
           tc::mma_commit(&dqfull[b]);
-          tc::mma_commit(&empty[st]);
+          tc::mma_commit(PST ? &emptyK[st] : &empty[st]);
           ++ndq;
           continue;
         }
@@ -619,6 +631,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(v + 32 * j), idS,
                          j > 0);
           tc::mma_commit(&dpfull[b]);
+          if (PST) tc::mma_commit(&empty[st]);   // band / dO / V: free once dP has read them
           ++ndp;
           continue;
         }
@@ -685,6 +698,7 @@ __global__ void __launch_bounds__(320, 1)
           if (odd) { p[2 * m] = nx; p[2 * m + 1] = lo; nx = hi; }
           else { p[2 * m] = lo; p[2 * m + 1] = hi; }
         }
+        tc::mbar_arrive(&empty[st]);   // this row of the staged band has been read
       } else {
       // P from S
       tc::mbar_wait(&sfull[b], use & 1);
@@ -842,7 +856,11 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* kvfull = pdsfull + 2;     // [2]
   uint64_t* kvfree = kvfull + 2;      // [2] (128)
   uint64_t* dfull = kvfree + 2;       // [NS] PST: the stage's delta rows landed (K1's output)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + NS);
+  // PST: the stage's Q / dO region has its own barriers: the band window, V and delta (dead once
+  // dP is issued and the warpgroup has formed dS) are released before dV / dK retire Q and dO
+  uint64_t* fullB = dfull + NS;       // [NS]
+  uint64_t* emptyB = fullB + NS;      // [NS]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyB + NS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
@@ -853,7 +871,10 @@ __global__ void __launch_bounds__(320, 1)
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NS; ++i) {
+      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], PST ? 1 + 128 : 1);
+      tc::mbar_init(&fullB[i], 1); tc::mbar_init(&emptyB[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&pdsfull[i], 128);
@@ -890,15 +911,20 @@ __global__ void __launch_bounds__(320, 1)
         trace_at(a.trace, 0, k);
         const int na = (u0 - a.R) & ~3;   // floor to a multiple of 4 (also for negatives)
         if constexpr (PST) {
-          tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB + 2 * C::QB);
+          tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0 - a.R, bh);   // P rows of the query window
+          tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
+          if (k >= NS) tc::mbar_wait(&emptyB[st], ((k - NS) / NS) & 1);
+          tc::mbar_expect_tx(&fullB[st], 2 * C::QB);
+          tc::tma_load_3d(b0 + OFF_Q, &tmQ, &fullB[st], 0, u0 - a.R, bh);
+          tc::tma_load_3d(b0 + OFF_DO, &tmdO, &fullB[st], 0, u0 - a.R, bh);
         } else {
           tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
+          tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
+          tc::tma_load_3d(b0 + OFF_Q, &tmQ, &full[st], 0, u0 - a.R, bh);
+          tc::tma_load_3d(b0 + OFF_DO, &tmdO, &full[st], 0, u0 - a.R, bh);
         }
-        tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
-        tc::tma_load_3d(b0 + OFF_Q, &tmQ, &full[st], 0, u0 - a.R, bh);
-        tc::tma_load_3d(b0 + OFF_DO, &tmdO, &full[st], 0, u0 - a.R, bh);
         // workspace rows trail: once the first NS stages' other loads are in flight, wait for K1
         // (PDL) and from then on load each stage's rows right after its other boxes.  LSE*log2e
         // and delta of the NQ query columns (padded rows written by K1; columns outside [0, T)
@@ -927,7 +953,7 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t m = PST ? tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                                 tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
                                                 tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1,
-                                                tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1)
+                                                tc::smem_u32(&fullB[ndp % NS]), (ndp / NS) & 1)
                                : tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                           tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,  // = (nkv-1)>>1 parity
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
@@ -945,11 +971,11 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < NQ / 16; ++j)
             tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
           tc::mma_commit(&kvfull[b]);
-          tc::mma_commit(&empty[st]);
+          tc::mma_commit(PST ? &emptyB[st] : &empty[st]);
           ++nkv;
           continue;
         }
-        if (ndp < ns && (m & 4) && (!PST || ndp < nkv + 2)) {
+        if (ndp < ns && (m & 4) && (!PST || (ndp < nkv + 2 && (m & 8)))) {
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * STG);
@@ -959,6 +985,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
                          j > 0);
           tc::mma_commit(&dpfull[b]);
+          if (PST) tc::mma_commit(&empty[st]);   // V: free once dP has read it
           ++ndp;
           continue;
         }
@@ -1036,6 +1063,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = 0; c < NQ / 2; c += 4)
             if (c < pc0 || c >= pc0 + CW / 2) tc::tmem_st4(x + c, 0u, 0u, 0u, 0u);
         }
+        tc::mbar_arrive(&empty[st]);   // this warpgroup's reads of the band window and delta are done
         tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);      // dS^T -> packed columns [NQ/2, NQ)
         tc::tmem_st_wait();
         tc::tc_fence_before();
