@@ -818,9 +818,14 @@ template <int CW> struct DkvCfg {
   static constexpr int PLD = ((CW - 31) + 7) / 8 * 8;
   static constexpr int PB = (NQ * PLD * 2 + 1023) / 1024 * 1024;
   static constexpr int STAGE_P = (PB + KB + 2 * QB + NQP * 4 + 1023) / 1024 * 1024;
-  // wide bands (W > 41): one staging tile per warpgroup (dV, then dK through the same tile)
-  static constexpr bool P1 = 1024 + NS * STAGE_P + 4 * KB + 512 > 232448;
-  static constexpr int SMEM_P = 1024 + NS * STAGE_P + (P1 ? 2 : 4) * KB + 512;
+  // the stored-band stage is two rings: A = [P window | V | delta] (2 slots, free once dP is
+  // issued and dS formed), B = [Q | dO] (3 slots, free once dV / dK are stored: the dV / dK rows
+  // are staged in the slot's dead Q / dO tiles, so there are no separate staging tiles)
+  static constexpr int STAGE_A = (PB + KB + NQP * 4 + 1023) / 1024 * 1024;
+  static constexpr int STAGE_B = 2 * QB;
+  static constexpr int NSB = 3;
+  static constexpr int SMEM_P = 1024 + NS * STAGE_A + NSB * STAGE_B + 512;
+  static_assert(QB >= KB && QB % 1024 == 0, "dV / dK staging in the Q / dO tiles");
 };
 
 // PST (stored-band mode): tmK maps the band P [BH][T][ldp] with box (ldp, NQ, 1); the stage is
@@ -835,16 +840,18 @@ __global__ void __launch_bounds__(320, 1)
   using C = DkvCfg<CW>;
   constexpr int NQ = C::NQ, NS = C::NS;
   constexpr int DVCOL = 176 <= 256 - 64 ? NQ : 0;   // dV after X_0, dK after X_1
-  constexpr int STG = PST ? C::STAGE_P : C::STAGE;
-  constexpr int OFF_V = PST ? C::PB : C::KB, OFF_Q = OFF_V + C::KB, OFF_DO = OFF_Q + C::QB;
-  constexpr int OFF_L2 = OFF_DO + C::QB, OFF_DEL = PST ? OFF_L2 : OFF_L2 + C::NQP * 4;
+  constexpr int STG = PST ? C::STAGE_A : C::STAGE;
+  // PST: ring A [P window | V | delta]; ring B [Q | dO] (OFF_Q / OFF_DO relative to a B slot)
+  constexpr int OFF_V = PST ? C::PB : C::KB, OFF_Q = PST ? 0 : OFF_V + C::KB, OFF_DO = OFF_Q + C::QB;
+  constexpr int OFF_L2 = PST ? 0 : OFF_DO + C::QB, OFF_DEL = PST ? C::PB + C::KB : OFF_L2 + C::NQP * 4;
+  constexpr int NSB = PST ? C::NSB : NS;
   static_assert(NQ + 64 <= 256, "TMEM layout needs NQ <= 192");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage0 = smem;                       // [K | V | Q | dO]
-  uint8_t* obuf0 = smem + NS * STG;             // per warpgroup: [dV | dK] staging
-  constexpr bool ONE = PST && C::P1;             // one staging tile per warpgroup
-  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + (ONE ? 2 : 4) * C::KB);
+  uint8_t* stage0 = smem;                       // [K | V | Q | dO] (PST: ring A)
+  uint8_t* stageB0 = smem + NS * STG;           // PST: ring B
+  uint8_t* obuf0 = smem + NS * STG;             // per warpgroup: [dV | dK] staging (not PST)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(PST ? stageB0 + NSB * C::STAGE_B : obuf0 + 4 * C::KB);
   uint64_t* full = bars;              // [NS]
   uint64_t* empty = full + NS;        // [NS]
   uint64_t* sfull = empty + NS;       // [2]
@@ -858,9 +865,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dfull = kvfree + 2;       // [NS] PST: the stage's delta rows landed (K1's output)
   // PST: the stage's Q / dO region has its own barriers: the band window, V and delta (dead once
   // dP is issued and the warpgroup has formed dS) are released before dV / dK retire Q and dO
-  uint64_t* fullB = dfull + NS;       // [NS]
-  uint64_t* emptyB = fullB + NS;      // [NS]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyB + NS);
+  uint64_t* fullB = dfull + NS;       // [NSB]
+  uint64_t* emptyB = fullB + NSB;     // [NSB]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyB + NSB);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, W = a.L + a.R + 1;
@@ -871,10 +878,8 @@ __global__ void __launch_bounds__(320, 1)
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
-    for (int i = 0; i < NS; ++i) {
-      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], PST ? 1 + 128 : 1);
-      tc::mbar_init(&fullB[i], 1); tc::mbar_init(&emptyB[i], 1);
-    }
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], PST ? 1 + 128 : 1); }
+    for (int i = 0; i < NSB; ++i) { tc::mbar_init(&fullB[i], 1); tc::mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&pdsfull[i], 128);
@@ -914,10 +919,12 @@ __global__ void __launch_bounds__(320, 1)
           tc::mbar_expect_tx(&full[st], NQ * a.ldp * 2 + C::KB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0 - a.R, bh);   // P rows of the query window
           tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
-          if (k >= NS) tc::mbar_wait(&emptyB[st], ((k - NS) / NS) & 1);
-          tc::mbar_expect_tx(&fullB[st], 2 * C::QB);
-          tc::tma_load_3d(b0 + OFF_Q, &tmQ, &fullB[st], 0, u0 - a.R, bh);
-          tc::tma_load_3d(b0 + OFF_DO, &tmdO, &fullB[st], 0, u0 - a.R, bh);
+          const int sb = k % NSB;
+          uint8_t* bb = stageB0 + sb * C::STAGE_B;
+          if (k >= NSB) tc::mbar_wait(&emptyB[sb], ((k - NSB) / NSB) & 1);
+          tc::mbar_expect_tx(&fullB[sb], 2 * C::QB);
+          tc::tma_load_3d(bb + OFF_Q, &tmQ, &fullB[sb], 0, u0 - a.R, bh);
+          tc::tma_load_3d(bb + OFF_DO, &tmdO, &fullB[sb], 0, u0 - a.R, bh);
         } else {
           tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
@@ -953,7 +960,7 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t m = PST ? tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                                 tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,
                                                 tc::smem_u32(&full[ndp % NS]), (ndp / NS) & 1,
-                                                tc::smem_u32(&fullB[ndp % NS]), (ndp / NS) & 1)
+                                                tc::smem_u32(&fullB[ndp % NSB]), (ndp / NSB) & 1)
                                : tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                           tc::smem_u32(&kvfree[(nkv + 1) & 1]), ((nkv + 3) >> 1) & 1,  // = (nkv-1)>>1 parity
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
@@ -962,7 +969,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = nkv & 1, st = nkv % NS;
           const uint32_t x = tbase + b * 256;
-          const uint32_t base = tc::smem_u32(stage0 + st * STG);
+          const uint32_t base = PST ? tc::smem_u32(stageB0 + (nkv % NSB) * C::STAGE_B) : tc::smem_u32(stage0 + st * STG);
           const uint32_t q = base + OFF_Q, dO = base + OFF_DO;
 #pragma unroll
           for (int j = 0; j < NQ / 16; ++j)
@@ -971,7 +978,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < NQ / 16; ++j)
             tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
           tc::mma_commit(&kvfull[b]);
-          tc::mma_commit(PST ? &emptyB[st] : &empty[st]);
+          if (!PST) tc::mma_commit(&empty[st]);   // PST: ring B is released after the dV / dK stores
           ++nkv;
           continue;
         }
@@ -979,7 +986,8 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = ndp & 1, st = ndp % NS;
           const uint32_t base = tc::smem_u32(stage0 + st * STG);
-          const uint32_t v = base + OFF_V, dO = base + OFF_DO;
+          const uint32_t v = base + OFF_V;
+          const uint32_t dO = (PST ? tc::smem_u32(stageB0 + (ndp % NSB) * C::STAGE_B) : base) + OFF_DO;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
@@ -1010,7 +1018,7 @@ __global__ void __launch_bounds__(320, 1)
     const int r = 32 * q4 + lane;
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
-    uint8_t* ostage = obuf0 + wg * (ONE ? 1 : 2) * C::KB;  // [dV | dK] (ONE: dV, then dK)
+    uint8_t* ostage = obuf0 + wg * 2 * C::KB;  // [dV | dK] (not PST)
     for (int k = wg; k < ntile_me; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
       const int bh = g / ntq, u0 = (g % ntq) * kM;
@@ -1123,30 +1131,25 @@ __global__ void __launch_bounds__(320, 1)
         }
         continue;
       }
-      if (leader) tc::bulk_wait_read0();
-      tc::named_bar(1 + wg, 128);
-      if constexpr (ONE) {
-        float dkr[64];
-        tmem_ld64(DK + lanes, dkr);
-        tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
+      if constexpr (PST) {   // dV, dK staged in this tile's ring-B slot (Q, dO dead: the MMAs completed)
+        uint8_t* bb = stageB0 + (k % NSB) * C::STAGE_B;
+        tmem_row64_to_smem_sw128(DV + lanes, 1.f, bb + OFF_Q, r);
+        tmem_row64_to_smem_sw128(DK + lanes, a.scale, bb + OFF_DO, r);
         tc::tc_fence_before();
         tc::mbar_arrive(&kvfree[b]);
         tc::fence_proxy_async_smem();
         tc::named_bar(1 + wg, 128);
         if (leader) {
-          tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
+          tc::tma_store_3d(&tmdV, bb + OFF_Q, 0, u0, bh);
+          tc::tma_store_3d(&tmdK, bb + OFF_DO, 0, u0, bh);
           tc::bulk_commit();
           tc::bulk_wait_read0();
+          tc::mbar_arrive(&emptyB[k % NSB]);
         }
-        tc::named_bar(1 + wg, 128);
-        tmem_row64_to_smem_sw128_regs(dkr, a.scale, ostage, r);
-        tc::fence_proxy_async_smem();
-        tc::named_bar(1 + wg, 128);
-        if (leader) {
-          tc::tma_store_3d(&tmdK, ostage, 0, u0, bh);
-          tc::bulk_commit();
-        }
-      } else {
+        continue;
+      }
+      if (leader) tc::bulk_wait_read0();
+      tc::named_bar(1 + wg, 128);
       tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
       tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + C::KB, r);
       tc::tc_fence_before();
@@ -1157,7 +1160,6 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
         tc::tma_store_3d(&tmdK, ostage + C::KB, 0, u0, bh);
         tc::bulk_commit();
-      }
       }
       if (tr) trace_at(a.trace, 7, k);
     }
