@@ -19,7 +19,8 @@ B=8 batch, no data-path collective ("weak"); value = frames of all ranks / max-o
 time.  Sub-objects: "llsa" = M2, the LLSA step with the B*H = 96 (b, h) units split over the
 ranks (strong scaling); "large" = M3, wav2vec2-large (B=64, H=16, 24 layers) batch-sharded
 (strong); "hour" = M4, one hour-long stream time-sharded through the library's NCCL halo
-exchange (sa_forward_tsharded / sa_backward_tsharded, strong).
+exchange (sa_forward_tsharded / sa_backward_tsharded, strong), with "hour.llsa" the same stream
+through the LLSA time-sharded calls (llsa_forward_tsharded / llsa_backward_tsharded).
 
 --impl reference runs the CPU oracle (oracle/, numpy fp64) on a bounded sample of
 the same workload (the task's reference arm for this paper-only reference).
@@ -382,6 +383,13 @@ def run_gpu(args):
             hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
         except Exception as e:   # the headline line must not depend on this sub-measurement
             hour = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
+        try:
+            hour_llsa = run_hour_llsa(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
+        except Exception as e:
+            hour_llsa = {"error": f"{type(e).__name__}: {e}"[:300]}
+        if isinstance(hour, dict):
+            hour["llsa"] = hour_llsa
 
     enc = None
     if not args.no_encoder and world == 1:
@@ -754,6 +762,72 @@ def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
                         f"through sa_forward_tsharded / sa_backward_tsharded, time-sharded x{world} "
                         f"({'NCCL halo exchange overlapped with interior tiles' if world > 1 else 'no neighbours'}), "
                         f"{'CUDA graph' if graph is not None else 'eager'}",
+            "frames_per_rank": n, "halo_exchange": "nccl" if world > 1 else None}
+
+
+def run_hour_llsa(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
+    """M4, LLSA: the hour-long stream (B=1, H=12, T=180,000) through 12 layers x (LLSA fwd + bwd),
+    C = R+1 = 9 channels, bf16, time-sharded over the ranks through llsa_forward_tsharded /
+    llsa_backward_tsharded (contiguous slabs with L+2R-frame margins exchanged over NCCL before
+    each call; at N = 1 no neighbours).  One buffer set serves every layer (the 20 GB per-layer
+    working set is far beyond L2 either way).  Strong scaling: value = T / max-over-ranks time."""
+    import ctypes
+    import torch
+    from paper_2302_13451_b200 import dist as sd
+    from paper_2302_13451_b200 import tshard
+    Th, Bh, n_layers, C = 180_000, 1, NL, R + 1
+    t0, t1 = tshard.shard_bounds(Th, world, rank, 1)
+    n = t1 - t0
+    hl, hr = sd.llsa_slab_rows(n, L, R, t0, Th)
+    Ts = hl + n + hr
+    d = sd.Dist()
+    L_ = sd._lib()
+    td = sd.tdesc(Bh, H, n, D, L, R, t0, Th)
+    tdp = ctypes.byref(td)
+    nws = int(L_.llsa_tsharded_workspace(tdp, d._h))
+    if nws == 0:
+        raise RuntimeError(L_.sattn_last_error().decode())
+    ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    shp = (C, Bh, H, Ts, D)
+    Q, K, V, dO = (torch.zeros(shp, device=dev, dtype=torch.bfloat16) for _ in range(4))
+    for x in (Q, K, V, dO):
+        x[:, :, :, hl:hl + n].copy_(rnd(C, Bh, H, n, D))
+    O, dQ, dK, dV = (torch.zeros(shp, device=dev, dtype=torch.bfloat16) for _ in range(4))
+    LSE = torch.zeros(shp[:-1], device=dev, dtype=torch.float32)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+
+    def step():
+        sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for _ in range(n_layers):
+            st = L_.llsa_forward_tsharded(tdp, d._h, P(Q), P(K), P(V), P(O), P(LSE), P(ws), nws, sp)
+            assert st == 0, L_.sattn_last_error()
+        for _ in range(n_layers):
+            st = L_.llsa_backward_tsharded(tdp, d._h, P(Q), P(K), P(V), P(O), P(LSE), P(dO), P(dQ), P(dK), P(dV),
+                                           P(ws), nws, sp)
+            assert st == 0, L_.sattn_last_error()
+
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    k = max(1, min(args.steps, 3))
+    a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(k):
+        step()
+    a1.record(stream)
+    barrier()
+    ms_loc = a0.elapsed_time(a1) / k
+    ms = _max_ms(ms_loc, world, dev)
+    d.close()
+    units = Bh * H * n * C
+    del Q, K, V, dO, O, dQ, dK, dV, LSE, ws
+    torch.cuda.empty_cache()
+    return {"value": round(Bh * Th / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": k,
+            "scaling": "strong", "channels": C,
+            "hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * n_layers / (ms_loc / 1e3) / 1e9 / hbm, 4),
+            "workload": f"M4 LLSA: hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), C={C}, {n_layers} layers x "
+                        f"(LLSA fwd + bwd) through llsa_forward_tsharded / llsa_backward_tsharded, time-sharded "
+                        f"x{world} ({'NCCL halo exchange of L+2R-frame margins' if world > 1 else 'no neighbours'}), eager",
             "frames_per_rank": n, "halo_exchange": "nccl" if world > 1 else None}
 
 

@@ -241,6 +241,28 @@ sattn_status sa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, co
 /* host-only: out6 = {hl, hr, slab frames, query tiles, first interior tile, first right-edge tile} */
 sattn_status sattn_tshard_geometry(const sattn_tshard_desc* td, int rank, int world, int64_t* out6);
 
+/* Time-sharded LLSA (Eq. 14-16).  Output (t, c) reads frames
+ * [t-R-L, t+R] of every channel (horizon t+c: band keys of channel R, staircase keys), and the
+ * local dQ/dK/dV also receive from the halo outputs t in [t0-R, t0) and [t1, t1+L+R), whose P
+ * and delta are exact when their own windows lie in the slab.  So every tensor of these calls
+ * is a contiguous SLAB [C][B][H][hl + T + hr][D] (LSE [C][B][H][hl + T + hr] fp32), hl = hr =
+ * llsa_tshard_margin(L, R) = L + 2R where a left / right neighbour exists (else 0), local
+ * frames at rows [hl, hl + T).  The forward fills the Q, K, V margins from the neighbours (L+2R
+ * rows of every channel) and runs llsa_forward on the slab (halo rows' O, LSE exact, kept for
+ * the backward); the backward fills dO's halo rows (R from the left, L+R from the right) and
+ * runs llsa_backward on the slab.  Local rows equal the unsharded call's up to summation order;
+ * margin rows of outputs are scratch; margin rows the exchange does not write must be finite
+ * (zero-initialise once).  The backward must get the forward's Q, K, V, O, LSE slabs.  Dense
+ * inputs (in_broadcast = 0); every shard T >= L + 2R when it has neighbours.  The exchange
+ * precedes the compute (no interior/edge split on the LLSA kernels).  Same transports as SA. */
+int64_t llsa_tshard_margin(int32_t L, int32_t R);
+size_t llsa_tsharded_workspace(const sattn_tshard_desc* td, const sattn_dist* d);
+sattn_status llsa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,
+                                   float* LSE, void* ws, size_t ws_bytes, void* stream);
+sattn_status llsa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
+                                    const void* V, const void* O, const float* LSE, void* dO, void* dQ, void* dK,
+                                    void* dV, void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------- misc ---------------------------------------------------------*/
 const char* sattn_last_error(void);      /* thread-local message of the last failure */
 const char* sattn_version(void);

@@ -149,9 +149,10 @@ struct HaloT {
 };
 
 struct Geo {
-  long long BH;
+  long long BH;        // planes (SA: B*H; LLSA: channels x B*H)
   int T_loc, ld, row_bytes;
   bool left, right;
+  int first;           // row of the first local frame in a plane (SA: the margin M; LLSA: hl)
 };
 
 // message sizes of one exchange (bytes): to / from the left neighbour, to / from the right one
@@ -195,7 +196,7 @@ sattn_status exchange(sattn_dist* d, const Geo& g, const HaloT* t, int nt, char*
   size_t o_sl = 0, o_rl = 0, o_sr = 0, o_rr = 0;
   for (int i = 0; i < nt; ++i) {
     char* b = t[i].base;
-    const long long first = (long long)kMargin * g.row_bytes, last = (long long)(kMargin + g.T_loc) * g.row_bytes;
+    const long long first = (long long)g.first * g.row_bytes, last = (long long)(g.first + g.T_loc) * g.row_bytes;
     if (g.left) {
       // to rank-1: my first need_r rows (its right margin); from rank-1: my left margin
       pack.s[pack.n++] = Seg{b + first, send_l + o_sl, pitch, (long long)t[i].need_r * g.row_bytes,
@@ -321,6 +322,7 @@ sattn_status shard_setup(const sattn_tshard_desc* td, const sattn_dist* d, Shard
   s.g.row_bytes = (int)l.D * 2;
   s.g.left = left;
   s.g.right = right;
+  s.g.first = kMargin;
   s.hl = left ? kMargin : 0;
   s.hr = right ? kMargin : 0;
   s.Ts = s.hl + (int)l.T + s.hr;
@@ -341,10 +343,13 @@ sattn_status shard_setup(const sattn_tshard_desc* td, const sattn_dist* d, Shard
 const bf16* at(const void* p, long long off) { return reinterpret_cast<const bf16*>(p) + off; }
 bf16* at(void* p, long long off) { return reinterpret_cast<bf16*>(p) + off; }
 
-size_t halo_ws(const Shard& s, const HaloT* t, int nt) {
-  const Msg m = msg_sizes(s.g, t, nt);
+size_t halo_ws(const Geo& g, const HaloT* t, int nt) {
+  const Msg m = msg_sizes(g, t, nt);
   return (m.send_l + m.recv_l + m.send_r + m.recv_r + 255) & ~size_t(255);
 }
+size_t halo_ws(const Shard& s, const HaloT* t, int nt) { return halo_ws(s.g, t, nt); }
+int llsa_tshard_margin_of(int L, int R) { return L + 2 * R; }
+int elem_bytes(int dtype) { return dtype == SATTN_BF16 ? 2 : 4; }
 
 void fwd_halos(const Shard& s, const void* Q, const void* K, const void* V, HaloT* t) {
   const int L = s.a.L, R = s.a.R;
@@ -373,6 +378,57 @@ sattn_status split_run(sattn_dist* d, Shard& s, int nk, cudaStream_t st, bool ex
   AttnArgs a = s.a;
   set_edges(a, tl);
   if (a.nkt > 0) return run(a, false);
+  return SATTN_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Time-sharded LLSA (Eq. 14-16).  Output (t, c) reads the frames
+// [t - R - L, t + R] of every channel (its horizon h = t + c: band keys h - R - L .. h - R of
+// channel R, staircase keys (h - c', c')), so the local outputs need L + R frames from the left
+// and R from the right.  The backward's local dQ, dK, dV also receive from the halo outputs
+// (t, c) with t in [t0 - R, t0) and [t1, t1 + L + R) (every output whose window holds a local
+// slot); their P and delta are exact when their own windows lie in the slab, i.e. with L + 2R
+// frames on each side.  So a rank's tensors are the SLAB [C][B][H][hl + T + hr][D] (hl = L + 2R if
+// a left neighbour exists, else 0; hr likewise; local frames at rows [hl, hl + T)), the forward
+// exchanges Q, K, V margins of L + 2R rows (every channel) and runs the ordinary LLSA forward on
+// the slab (its halo rows' O and LSE are exact), the backward exchanges the halo outputs' dO (R
+// rows from the left, L + R from the right) and runs the ordinary LLSA backward on the slab.
+// Local rows are exact (equal to the unsharded call's up to summation order); margin rows of the
+// outputs are scratch.  Dense inputs only (in_broadcast = 0: a stack's layer 1 duplicates first).
+// ------------------------------------------------------------------------------------------
+struct LShard {
+  Geo g;
+  int hl, hr, Ts, C;
+  sattn_desc slab;
+};
+
+sattn_status lshard_setup(const sattn_tshard_desc* td, const sattn_dist* d, LShard& s) {
+  if (!td || !d) return set_error(SATTN_EARG, "NULL tshard desc or dist handle");
+  const sattn_desc& l = td->local;
+  sattn_status r = check_desc(&l);
+  if (r != SATTN_OK) return r;
+  if (l.in_broadcast) return set_error(SATTN_EUNSUPPORTED, "time-sharded LLSA takes dense [C][B][H][T][D] inputs");
+  if ((l.D * elem_bytes(l.dtype)) % 16 != 0) return set_error(SATTN_EUNSUPPORTED, "rows must be 16-byte multiples");
+  if (td->t0 < 0 || td->T_global < td->t0 + l.T) return set_error(SATTN_EARG, "shard [t0, t0 + T) outside [0, T_global)");
+  const bool left = td->t0 > 0, right = td->t0 + l.T < td->T_global;
+  if (left != (d->rank > 0) || right != (d->rank < d->world - 1))
+    return set_error(SATTN_ECONFIG, "shard position does not match the rank (shards must be in rank order)");
+  const int mg = llsa_tshard_margin_of(l.L, l.R);
+  if ((left || right) && l.T < mg)
+    return set_error(SATTN_ECONFIG, "a shard must hold at least L + 2R frames for its neighbours' halos");
+  s.C = l.R + 1;
+  s.hl = left ? mg : 0;
+  s.hr = right ? mg : 0;
+  s.Ts = s.hl + (int)l.T + s.hr;
+  s.g.BH = (long long)s.C * l.B * l.H;
+  s.g.T_loc = (int)l.T;
+  s.g.ld = s.Ts;
+  s.g.row_bytes = (int)(l.D * elem_bytes(l.dtype));
+  s.g.left = left;
+  s.g.right = right;
+  s.g.first = s.hl;
+  s.slab = l;
+  s.slab.T = s.Ts;
   return SATTN_OK;
 }
 
@@ -523,6 +579,58 @@ sattn_status sa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, co
   count_launches(1);
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SATTN_OK : cuda_fail("time-sharded backward launch", e);
+}
+
+int64_t llsa_tshard_margin(int32_t L, int32_t R) { return llsa_tshard_margin_of(L, R); }
+
+size_t llsa_tsharded_workspace(const sattn_tshard_desc* td, const sattn_dist* d) {
+  LShard s;
+  if (lshard_setup(td, d, s) != SATTN_OK) return 0;
+  const int mg = llsa_tshard_margin_of(s.slab.L, s.slab.R);
+  const HaloT f[3] = {{nullptr, mg, mg}, {nullptr, mg, mg}, {nullptr, mg, mg}};
+  const HaloT b[1] = {{nullptr, s.slab.R, s.slab.L + s.slab.R}};
+  const size_t wf = halo_ws(s.g, f, 3);
+  const size_t wb = halo_ws(s.g, b, 1) + ((llsa_backward_workspace(&s.slab) + 255) & ~size_t(255));
+  return wf > wb ? wf : wb;
+}
+
+sattn_status llsa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,
+                                   float* LSE, void* ws, size_t ws_bytes, void* stream) {
+  LShard s;
+  sattn_status r = lshard_setup(td, d, s);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !O || !LSE) return set_error(SATTN_EARG, "NULL pointer");
+  const int mg = llsa_tshard_margin_of(s.slab.L, s.slab.R);
+  const HaloT h[3] = {{(char*)Q, mg, mg}, {(char*)K, mg, mg}, {(char*)V, mg, mg}};
+  const size_t need = halo_ws(s.g, h, 3);
+  if (need && (!ws || ws_bytes < need)) return set_error(SATTN_ECONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((r = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return r;
+  if (d->comm) {
+    const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
+    if (e != cudaSuccess) return cuda_fail("cudaStreamWaitEvent", e);
+  }
+  return llsa_forward(&s.slab, Q, K, V, O, LSE, stream);
+}
+
+sattn_status llsa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
+                                    const void* V, const void* O, const float* LSE, void* dO, void* dQ, void* dK,
+                                    void* dV, void* ws, size_t ws_bytes, void* stream) {
+  LShard s;
+  sattn_status r = lshard_setup(td, d, s);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !O || !LSE || !dO || !dQ || !dK || !dV || !ws) return set_error(SATTN_EARG, "NULL pointer");
+  const HaloT h[1] = {{(char*)dO, s.slab.R, s.slab.L + s.slab.R}};
+  const size_t nh = halo_ws(s.g, h, 1);
+  const size_t nb = llsa_backward_workspace(&s.slab);
+  if (ws_bytes < nh + nb) return set_error(SATTN_ECONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((r = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return r;
+  if (d->comm) {
+    const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
+    if (e != cudaSuccess) return cuda_fail("cudaStreamWaitEvent", e);
+  }
+  return llsa_backward(&s.slab, Q, K, V, O, LSE, dO, dQ, dK, dV, (char*)ws + nh, ws_bytes - nh, stream);
 }
 
 // host-only geometry of a shard (for tests and tooling): slab rows and the tile split

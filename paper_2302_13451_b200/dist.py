@@ -1,4 +1,4 @@
-"""Time-sharded SA over ranks through the C ABI (include/sattn.h "time sharding"): thin binding.
+"""Time-sharded SA and LLSA over ranks through the C ABI (include/sattn.h "time sharding"): thin binding.
 
 The library does the work — halo pack/unpack kernels, the exchange (NCCL point-to-point on a
 library stream, or a caller callback), the interior/edge tile split that overlaps it, and the
@@ -48,6 +48,10 @@ EXPORTS = {
     "sa_forward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_backward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sattn_tshard_geometry": (_I, [_PT, _I, _I, ctypes.POINTER(ctypes.c_int64)]),
+    "llsa_tshard_margin": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
+    "llsa_tsharded_workspace": (_SZ, [_PT, _P]),
+    "llsa_forward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "llsa_backward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
 }
 _bound = False
 
@@ -163,8 +167,8 @@ class Dist:
             traceback.print_exc()
             return 1
 
-    def _workspace(self, d, device):
-        n = int(_lib().sa_tsharded_workspace(ctypes.byref(d), self._h))
+    def _workspace(self, d, device, query="sa_tsharded_workspace"):
+        n = int(getattr(_lib(), query)(ctypes.byref(d), self._h))
         if n == 0:
             raise SattnError(_lib().sattn_last_error().decode() or "invalid time-shard configuration")
         if self._ws is None or self._ws.numel() < n or self._ws.device != device:
@@ -242,4 +246,57 @@ def sa_backward_tsharded(qm, km, vm, lsem, dom, L: int, R: int, t0: int, T_globa
     _check(_lib().sa_backward_tsharded(ctypes.byref(td), d._h, _ptr(qm), _ptr(km), _ptr(vm), _ptr(lsem), _ptr(dom),
                                        _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()),
            "sa_backward_tsharded")
+    return dq, dk, dv
+
+
+# ------------------------------------------------------------------ time-sharded LLSA (slab layout)
+
+def llsa_margin(L: int, R: int) -> int:
+    """Frames of a time-sharded LLSA slab's margin on a side with a neighbour (L + 2R)."""
+    return int(_lib().llsa_tshard_margin(L, R))
+
+
+def llsa_slab_rows(T_loc: int, L: int, R: int, t0: int, T_global: int):
+    """(hl, hr): margin frames before / after this rank's local rows in its LLSA slab."""
+    m = llsa_margin(L, R)
+    return (m if t0 > 0 else 0), (m if t0 + T_loc < T_global else 0)
+
+
+def _ltdesc(x, T_loc, L, R, t0, T_global, scale):
+    C, B, H, Ts, D = x.shape
+    if C != R + 1:
+        raise SattnError(f"LLSA slab has {C} channels, expected R + 1 = {R + 1}")
+    hl, hr = llsa_slab_rows(T_loc, L, R, t0, T_global)
+    if Ts != hl + T_loc + hr:
+        raise SattnError(f"slab frames {Ts} != {hl} + {T_loc} + {hr}")
+    return TShardDesc(make_desc(B, H, T_loc, D, L, R, _dtype_code(x), scale), t0, T_global)
+
+
+def llsa_forward_tsharded(q, k, v, T_loc: int, L: int, R: int, t0: int, T_global: int, d: Dist, scale=None):
+    """Slabs q, k, v [C, B, H, hl + T_loc + hr, D] (local frames [t0, t0 + T_loc) at rows
+    [hl, hl + T_loc)) -> slabs (o, lse); fills the q, k, v margins (kept for the backward)."""
+    td = _ltdesc(q, T_loc, L, R, t0, T_global, scale)
+    for t in (k, v):
+        if t.shape != q.shape or t.dtype != q.dtype:
+            raise SattnError("q, k, v must share shape and dtype")
+    o = torch.zeros_like(q)
+    lse = torch.zeros(q.shape[:-1], dtype=torch.float32, device=q.device)
+    ws = d._workspace(td, q.device, "llsa_tsharded_workspace")
+    _check(_lib().llsa_forward_tsharded(ctypes.byref(td), d._h, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                        _ptr(ws), ws.numel(), _stream()), "llsa_forward_tsharded")
+    return o, lse
+
+
+def llsa_backward_tsharded(q, k, v, o, lse, do, T_loc: int, L: int, R: int, t0: int, T_global: int, d: Dist,
+                           scale=None):
+    """Slabs dq, dk, dv (local rows exact).  q, k, v, o, lse: the forward's slabs; do: this
+    rank's dO slab (local rows set; its halo rows are filled here)."""
+    td = _ltdesc(q, T_loc, L, R, t0, T_global, scale)
+    if do.shape != q.shape or o.shape != q.shape or lse.shape != q.shape[:-1] or lse.dtype != torch.float32:
+        raise SattnError("o, do must be shaped like q and lse [C, B, H, Ts] fp32")
+    dq, dk, dv = torch.zeros_like(q), torch.zeros_like(q), torch.zeros_like(q)
+    ws = d._workspace(td, q.device, "llsa_tsharded_workspace")
+    _check(_lib().llsa_backward_tsharded(ctypes.byref(td), d._h, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse),
+                                         _ptr(do), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()),
+           "llsa_backward_tsharded")
     return dq, dk, dv

@@ -98,3 +98,34 @@ def test_host_swap_gloo(world):
         rl, rr = out[r]
         assert rl == (None if r == 0 else [100 + r - 1] * 5)
         assert rr == (None if r == world - 1 else [10 + r + 1] * (3 + r + 1))
+
+
+def _noop_exchange(*args):
+    return 0
+
+
+def test_llsa_tshard_margin_and_workspace_validation():
+    # the time-sharded LLSA slab: margin L + 2R on a side with a neighbour (the halo outputs'
+    # windows); the workspace query rejects what the calls would reject
+    import ctypes
+    from paper_2302_13451_b200 import dist as sd
+    assert sd.llsa_margin(32, 8) == 48 and sd.llsa_margin(32, 16) == 64 and sd.llsa_margin(3, 1) == 5
+    assert sd.llsa_slab_rows(1000, 32, 8, 0, 3000) == (0, 48)
+    assert sd.llsa_slab_rows(1000, 32, 8, 1000, 3000) == (48, 48)
+    assert sd.llsa_slab_rows(1000, 32, 8, 2000, 3000) == (48, 0)
+    L = sd._lib()
+    cb = sd.EXCHANGE_FN(_noop_exchange)
+    for rank, t0, T_global in ((0, 0, 2000), (1, 1000, 2000)):
+        h = ctypes.c_void_p()
+        assert L.sattn_dist_init_external(rank, 2, cb, None, ctypes.byref(h)) == 0
+        td = sd.tdesc(2, 3, 1000, 64, 32, 8, t0, T_global)
+        n = L.llsa_tsharded_workspace(ctypes.byref(td), h)
+        # at least the forward's messages: 3 tensors x (R+1) channels x B*H x (L+2R) rows x 128 B, sent and received
+        assert n >= 2 * 3 * 9 * 6 * 48 * 128
+        bad = sd.tdesc(2, 3, 40, 64, 32, 8, t0, T_global)        # shard shorter than L + 2R
+        assert L.llsa_tsharded_workspace(ctypes.byref(bad), h) == 0
+        bad = sd.tdesc(2, 3, 1000, 64, 32, 8, 500 if rank == 0 else 0, T_global)   # position vs rank
+        assert L.llsa_tsharded_workspace(ctypes.byref(bad), h) == 0
+        td.local.in_broadcast = 1                                 # dense inputs only
+        assert L.llsa_tsharded_workspace(ctypes.byref(td), h) == 0
+        L.sattn_dist_destroy(h)

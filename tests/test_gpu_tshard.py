@@ -95,6 +95,99 @@ def test_tsharded_c_path_multiprocess(world, T, L, R):
         assert res["oracle_excess"] <= 0, (r, res)
 
 
+def _llsa_worker(rank, world, port, T, L, R, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as tdist
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    import paper_2302_13451_b200 as s
+    from paper_2302_13451_b200 import dist as sd
+    from paper_2302_13451_b200 import tshard
+    import oracle
+    from gates import excess
+    B, H, D, C = 1, 2, 64, R + 1
+    g = torch.Generator(device="cuda").manual_seed(31)
+    q, k, v, do = (torch.randn(C, B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    o, lse = s.llsa_forward(q, k, v, L, R)
+    dq, dk, dv = s.llsa_backward(q, k, v, o, lse, do, L, R)
+    t0, t1 = tshard.shard_bounds(T, world, rank, 1)
+    n = t1 - t0
+    hl, hr = sd.llsa_slab_rows(n, L, R, t0, T)
+    d = sd.Dist()
+    assert d.transport == "host"
+    slab = lambda: torch.zeros(C, B, H, hl + n + hr, D, dtype=torch.bfloat16, device="cuda")  # noqa: E731
+    qs, ks, vs, dos = slab(), slab(), slab(), slab()
+    for m, x in ((qs, q), (ks, k), (vs, v), (dos, do)):
+        m[:, :, :, hl:hl + n].copy_(x[:, :, :, t0:t1])
+    os_, lses = sd.llsa_forward_tsharded(qs, ks, vs, n, L, R, t0, T, d)
+    gs = sd.llsa_backward_tsharded(qs, ks, vs, os_, lses, dos, n, L, R, t0, T, d)
+    loc = lambda m: m[..., hl:hl + n, :] if m.dim() == 5 else m[..., hl:hl + n]  # noqa: E731
+    res = {}
+    # against the unsharded GPU call (same kernels, different item tiling: the bf16 gate)
+    res["vs_unsharded"] = max(
+        excess(loc(a).double().cpu().numpy(), b[..., t0:t1, :].double().cpu().numpy(), "bf16", f"llsa-tshard-{nm}")
+        for nm, a, b in (("O", os_, o), ("dQ", gs[0], dq), ("dK", gs[1], dk), ("dV", gs[2], dv)))
+    res["lse_vs_unsharded"] = float((loc(lses) - lse[..., t0:t1]).abs().max())
+    # against the fp64 oracle on a window around each inner boundary: rows whose dependency cones
+    # (forward [t-R-L, t+R], backward +-(L+2R)) lie inside the window
+    worst = 0.0
+    for c in (t0, t1):
+        if c in (0, T):
+            continue
+        a0, a1 = max(0, c - 200), min(T, c + 200)
+        sl = lambda x: x[:, 0, :, a0:a1].double().cpu().numpy()  # noqa: E731
+        O, _ = oracle.llsa.llsa_forward(sl(q), sl(k), sl(v), L, R)
+        G = oracle.llsa.llsa_backward(sl(q), sl(k), sl(v), sl(do), L, R)
+        lo, hi = max(t0, c - 48), min(t1, c + 48)
+        if lo >= hi:
+            continue
+        r = slice(lo - a0, hi - a0)
+        pick = lambda m: m[:, 0, :, hl + lo - t0:hl + hi - t0].double().cpu().numpy()  # noqa: E731
+        for nm, got, ref in (("O", pick(os_), O[:, :, r]), ("dQ", pick(gs[0]), G[0][:, :, r]),
+                             ("dK", pick(gs[1]), G[1][:, :, r]), ("dV", pick(gs[2]), G[2][:, :, r])):
+            worst = max(worst, excess(got, ref, "bf16", f"llsa-tshard-w{world}-r{rank}-{nm}"))
+    res["oracle_excess"] = worst
+    out[rank] = res
+    d.close()
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,T,L,R", [(2, 900, 32, 8), (3, 700, 3, 1), (2, 800, 32, 16)])
+def test_llsa_tsharded_c_path_multiprocess(world, T, L, R):
+    # time-sharded LLSA through the C ABI with the halo exchange live between real
+    # processes (callback transport over gloo: the processes share the one GPU): local rows against
+    # the unsharded LLSA call and against the fp64 oracle at every shard boundary
+    import torch.multiprocessing as mp
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_llsa_worker, args=(world, _free_port(), T, L, R, out), nprocs=world, join=True)
+    assert sorted(out.keys()) == list(range(world))
+    for r in range(world):
+        res = out[r]
+        assert res["vs_unsharded"] <= 0 and res["lse_vs_unsharded"] <= 1e-3, (r, res)
+        assert res["oracle_excess"] <= 0, (r, res)
+
+
+def test_llsa_tsharded_nccl_world1_equals_unsharded():
+    # world 1 over the NCCL transport: no neighbours, the slab is the whole stream: bitwise equal
+    import paper_2302_13451_b200 as s
+    from paper_2302_13451_b200 import dist as sd
+    C, B, H, T, D, L, R = 9, 1, 2, 600, 64, 32, 8
+    g = torch.Generator(device="cuda").manual_seed(6)
+    q, k, v, do = (torch.randn(C, B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
+    o, lse = s.llsa_forward(q, k, v, L, R)
+    dq, dk, dv = s.llsa_backward(q, k, v, o, lse, do, L, R)
+    d = sd.Dist(transport="nccl")
+    os_, lses = sd.llsa_forward_tsharded(q.clone(), k.clone(), v.clone(), T, L, R, 0, T, d)
+    gs = sd.llsa_backward_tsharded(q, k, v, os_, lses, do.clone(), T, L, R, 0, T, d)
+    assert torch.equal(os_, o) and torch.equal(lses, lse)
+    for a, b in zip(gs, (dq, dk, dv)):
+        assert torch.equal(a, b)
+    d.close()
+
+
 def test_tsharded_nccl_world1_equals_unsharded():
     # the NCCL transport's handle at world 1 (no neighbours, no exchange): the slab is the whole
     # stream and the result must be the unsharded call's, bitwise
