@@ -517,8 +517,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dsfull = dpfull + 2;      // [2] (128)
   uint64_t* dqfull = dsfull + 2;      // [2]
   uint64_t* tfree = dqfull + 2;       // [2] (128)
-  // PST: the stage's K region has its own barriers, so that band / dO / V (dead once dP is issued
-  // and the warpgroup has read its band rows) are released before the dQ MMA retires K
+  // the stage's K region has its own release barrier, so that Q or the band / dO / V (dead once dP
+  // is issued and, PST, the warpgroup has read its band rows) are released before the dQ MMA
+  // retires K; PST: K also lands on its own barrier (dP does not need it)
   uint64_t* fullK = tfree + 2;        // [NS]
   uint64_t* emptyK = fullK + NS;      // [NS]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyK + NS);
@@ -575,6 +576,8 @@ __global__ void __launch_bounds__(320, 1)
           tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &fullK[st], 0, t0 - a.L - ksh, bh);
           continue;
         } else {
+        // Q, dO, V are free once dP is issued (empty); K stays until dQ (emptyK).  S needs K too,
+        // so everything lands on `full`, but the Q / dO / V loads no longer wait for the dQ MMA
         tc::mbar_expect_tx(&full[st], 2 * C::QB + 2 * C::KB);
         if (nch > 1) {   // LLSA: [C][BH][T][64] maps
           tc::tma_load_4d(b0, &tmQ, &full[st], 0, t0, bh, a.bcast ? 0 : c);
@@ -583,9 +586,10 @@ __global__ void __launch_bounds__(320, 1)
           tc::tma_load_3d(b0, &tmQ, &full[st], 0, t0, bh);
           tc::tma_load_3d(b0 + C::QB, &tmdO, &full[st], 0, t0, bh);
         }
-        }
-        tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - ksh, bh);
         tc::tma_load_3d(b0 + 2 * C::QB + C::KB, &tmV, &full[st], 0, t0 - a.L - ksh, bh);
+        if (k >= NS) tc::mbar_wait(&emptyK[st], ((k - NS) / NS) & 1);
+        tc::tma_load_3d(b0 + 2 * C::QB, &tmK, &full[st], 0, t0 - a.L - ksh, bh);
+        }
       }
     }
   } else if (warp == 1) {
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(320, 1)
               tc::mma_bf16_ts(x + NK, x + NK / 2 + 8 * j, tc::desc_mnmajor_sw128(kk + 2048 * j), idQ, true);
           }
           tc::mma_commit(&dqfull[b]);
-          tc::mma_commit(PST ? &emptyK[st] : &empty[st]);
+          tc::mma_commit(&emptyK[st]);
           ++ndq;
           continue;
         }
@@ -631,7 +635,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(v + 32 * j), idS,
                          j > 0);
           tc::mma_commit(&dpfull[b]);
-          if (PST) tc::mma_commit(&empty[st]);   // band / dO / V: free once dP has read them
+          tc::mma_commit(&empty[st]);   // Q (or the band) / dO / V: free once S and dP have read them
           ++ndp;
           continue;
         }
@@ -878,7 +882,7 @@ __global__ void __launch_bounds__(320, 1)
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
-    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], PST ? 1 + 128 : 1); }
+    for (int i = 0; i < NS; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1 + 128); }
     for (int i = 0; i < NSB; ++i) { tc::mbar_init(&fullB[i], 1); tc::mbar_init(&emptyB[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
@@ -925,10 +929,11 @@ __global__ void __launch_bounds__(320, 1)
           tc::mbar_expect_tx(&fullB[sb], 2 * C::QB);
           tc::tma_load_3d(bb + OFF_Q, &tmQ, &fullB[sb], 0, u0 - a.R, bh);
           tc::tma_load_3d(bb + OFF_DO, &tmdO, &fullB[sb], 0, u0 - a.R, bh);
-        } else {
+        } else {   // K, V (and the LSE / delta rows) free after dP + dS (empty); Q, dO after dV / dK (emptyB)
           tc::mbar_expect_tx(&full[st], 2 * C::KB + 2 * C::QB);
           tc::tma_load_3d(b0, &tmK, &full[st], 0, u0, bh);
           tc::tma_load_3d(b0 + OFF_V, &tmV, &full[st], 0, u0, bh);
+          if (k >= NS) tc::mbar_wait(&emptyB[st], ((k - NS) / NS) & 1);
           tc::tma_load_3d(b0 + OFF_Q, &tmQ, &full[st], 0, u0 - a.R, bh);
           tc::tma_load_3d(b0 + OFF_DO, &tmdO, &full[st], 0, u0 - a.R, bh);
         }
@@ -978,7 +983,7 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < NQ / 16; ++j)
             tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, j > 0);
           tc::mma_commit(&kvfull[b]);
-          if (!PST) tc::mma_commit(&empty[st]);   // PST: ring B is released after the dV / dK stores
+          if (!PST) tc::mma_commit(&emptyB[st]);   // Q, dO (PST: ring B is released after the dV / dK stores)
           ++nkv;
           continue;
         }
@@ -993,7 +998,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
                          j > 0);
           tc::mma_commit(&dpfull[b]);
-          if (PST) tc::mma_commit(&empty[st]);   // V: free once dP has read it
+          tc::mma_commit(&empty[st]);   // K (S^T), V: free once S and dP have read them
           ++ndp;
           continue;
         }
@@ -1105,6 +1110,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
       }
+      tc::mbar_arrive(&empty[st]);   // this warpgroup's reads of the LSE / delta rows are done
       tmem_write_row<CW, NQ>(x, q4, p);                 // P^T  -> packed columns [0, NQ/2)
       tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);      // dS^T -> packed columns [NQ/2, NQ)
       tc::tmem_st_wait();
