@@ -1639,7 +1639,9 @@ template <int CW> struct LkvCfg {
   static constexpr int NQP = (NQ + 3 + 31) / 32 * 32;
   static constexpr int KVSTAGE = 2 * KB;
   static constexpr int QSTAGE = (2 * QB + 2 * NQP * 4 + 1023) / 1024 * 1024;
-  static constexpr int SMEM = 1024 + 2 * KVSTAGE + 2 * QSTAGE + 4 * KB + 512;
+  static constexpr int NQS = 3;      // sub-item ring depth (dV / dK are staged in the tile's dead K / V)
+  static constexpr int SMEM = 1024 + 2 * KVSTAGE + NQS * QSTAGE + 512;
+  static_assert(SMEM <= 232448, "LLSA kv pass shared memory");
 };
 
 template <int CW>
@@ -1654,15 +1656,15 @@ __global__ void __launch_bounds__(320, 1)
   static_assert(NQ + 64 <= 256, "TMEM layout needs NQ <= 192");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* kv0 = smem;                                   // [K | V] x 2
-  uint8_t* qs0 = smem + 2 * Cf::KVSTAGE;                 // [Q_c | dO_c | lse2 | delta] x 2
-  uint8_t* obuf0 = qs0 + 2 * Cf::QSTAGE;                 // per warpgroup [dV | dK]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(obuf0 + 4 * Cf::KB);
+  constexpr int NQS = Cf::NQS;
+  uint8_t* kv0 = smem;                                   // [K | V] x 2 (then the tile's [dV | dK] staging)
+  uint8_t* qs0 = smem + 2 * Cf::KVSTAGE;                 // [Q_c | dO_c | lse2 | delta] x NQS
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qs0 + NQS * Cf::QSTAGE);
   uint64_t* kvfull_ld = bars;         // [2] K/V of a tile landed
-  uint64_t* kvempty = kvfull_ld + 2;  // [2] K/V stage free
-  uint64_t* qfull = kvempty + 2;      // [2]
-  uint64_t* qempty = qfull + 2;       // [2]
-  uint64_t* sfull = qempty + 2;       // [2]
+  uint64_t* kvempty = kvfull_ld + 2;  // [2] K/V stage free (after the tile's dV / dK stores read it)
+  uint64_t* qfull = kvempty + 2;      // [NQS]
+  uint64_t* qempty = qfull + NQS;     // [NQS]
+  uint64_t* sfull = qempty + NQS;     // [2]
   uint64_t* xfree = sfull + 2;        // [2] (128)
   uint64_t* dpfull = xfree + 2;       // [2]
   uint64_t* pdsfull = dpfull + 2;     // [2] (128)
@@ -1680,9 +1682,9 @@ __global__ void __launch_bounds__(320, 1)
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
     tc::tma_prefetch_desc(&tmdO); tc::tma_prefetch_desc(&tmdK); tc::tma_prefetch_desc(&tmdV);
+    for (int i = 0; i < NQS; ++i) { tc::mbar_init(&qfull[i], 1); tc::mbar_init(&qempty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&kvfull_ld[i], 1); tc::mbar_init(&kvempty[i], 1);
-      tc::mbar_init(&qfull[i], 1); tc::mbar_init(&qempty[i], 1);
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&xfree[i], 128); tc::mbar_init(&dpfull[i], 1);
       tc::mbar_init(&pdsfull[i], 128); tc::mbar_init(&kvfull[i], 1); tc::mbar_init(&kvfree[i], 128);
     }
@@ -1710,8 +1712,8 @@ __global__ void __launch_bounds__(320, 1)
         tc::tma_load_3d(kvb, &tmK, &kvfull_ld[ks], 0, u0, bh);
         tc::tma_load_3d(kvb + Cf::KB, &tmV, &kvfull_ld[ks], 0, u0, bh);
         for (int c = 0; c < C; ++c, ++k) {
-          const int qs = k & 1;
-          if (k >= 2) tc::mbar_wait(&qempty[qs], ((k - 2) >> 1) & 1);
+          const int qs = k % NQS;
+          if (k >= NQS) tc::mbar_wait(&qempty[qs], ((k - NQS) / NQS) & 1);
           uint8_t* qb = qs0 + qs * Cf::QSTAGE;
           const int n0 = u0 + (R - c);                    // query frame of column 0
           const int na = n0 & ~3;
@@ -1733,14 +1735,14 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&pdsfull[nkv & 1]), (nkv >> 1) & 1,
                                           tc::smem_u32(&kvfull_ld[kts & 1]), (kts >> 1) & 1,
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
-                                          tc::smem_u32(&qfull[ns & 1]), (ns >> 1) & 1);
+                                          tc::smem_u32(&qfull[ns % NQS]), (ns / NQS) & 1);
         if (nkv < ndp && (m & 1)) {
           const int kt = nkv / C, c = nkv % C;
           if (c == 0 && kt >= 1 && !tc::mbar_test(tc::smem_u32(&kvfree[(kt - 1) & 1]), ((kt - 1) >> 1) & 1)) {
             // accumulators still being drained by the previous tile's epilogue
           } else {
             tc::tc_fence_after();
-            const int b = nkv & 1, qs = nkv & 1;
+            const int b = nkv & 1, qs = nkv % NQS;
             const uint32_t x = tbase + b * 256;
             const uint32_t q = tc::smem_u32(qs0 + qs * Cf::QSTAGE), dO = q + Cf::QB;
 #pragma unroll
@@ -1750,10 +1752,7 @@ __global__ void __launch_bounds__(320, 1)
             for (int j = 0; j < NQ / 16; ++j)
               tc::mma_bf16_ts(DK, x + NQ / 2 + 8 * j, tc::desc_mnmajor_sw128(q + 2048 * j), idG, (c > 0) || (j > 0));
             tc::mma_commit(&qempty[qs]);
-            if (c == C - 1) {
-              tc::mma_commit(&kvfull[kt & 1]);
-              tc::mma_commit(&kvempty[kt & 1]);
-            }
+            if (c == C - 1) tc::mma_commit(&kvfull[kt & 1]);   // K / V dead: the epilogue stages dV / dK there
             ++nkv;
             continue;
           }
@@ -1762,7 +1761,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::tc_fence_after();
           const int b = ndp & 1, kt = ndp / C;
           const uint32_t v = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE) + Cf::KB;
-          const uint32_t dO = tc::smem_u32(qs0 + (ndp & 1) * Cf::QSTAGE) + Cf::QB;
+          const uint32_t dO = tc::smem_u32(qs0 + (ndp % NQS) * Cf::QSTAGE) + Cf::QB;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(v + 32 * j), tc::desc_kmajor_sw128(dO + 32 * j), idS,
@@ -1777,7 +1776,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::tc_fence_after();
             const int b = ns & 1;
             const uint32_t kk = tc::smem_u32(kv0 + (kt & 1) * Cf::KVSTAGE);
-            const uint32_t q = tc::smem_u32(qs0 + (ns & 1) * Cf::QSTAGE);
+            const uint32_t q = tc::smem_u32(qs0 + (ns % NQS) * Cf::QSTAGE);
 #pragma unroll
             for (int j = 0; j < kD / 16; ++j)
               tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(kk + 32 * j), tc::desc_kmajor_sw128(q + 32 * j), idS,
@@ -1795,17 +1794,16 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t lanes = uint32_t(32 * q4) << 16;
     const bool leader = q4 == 2 && lane == 0;
     const int W = L + 1;
-    uint8_t* ostage = obuf0 + wg * 2 * Cf::KB;  // [dV | dK]
     for (int k = wg; k < nsub; k += 2) {
       const int kt = k / C, c = k % C;
       const int g = blockIdx.x + kt * gridDim.x;
       const int bh = g / ntq, u0 = (g % ntq) * kM;
-      const int b = k & 1, use = k >> 1, qs = k & 1;
+      const int b = k & 1, use = k >> 1, qs = k % NQS;
       const int n0 = u0 + (R - c);
       const int sh = n0 - (n0 & ~3);
       const float* sL2 = reinterpret_cast<const float*>(qs0 + qs * Cf::QSTAGE + 2 * Cf::QB) + sh;
       const float* sDel = sL2 + Cf::NQP;
-      tc::mbar_wait(&qfull[qs], use & 1);
+      tc::mbar_wait(&qfull[qs], (k / NQS) & 1);
       const uint32_t x = tbase + lanes + b * 256;
       const int c0 = 32 * q4;
       tc::mbar_wait(&sfull[b], use & 1);
@@ -1842,8 +1840,7 @@ __global__ void __launch_bounds__(320, 1)
         tc::mbar_wait(&kvfull[kt & 1], (kt >> 1) & 1);
         __syncwarp();
         tc::tc_fence_after();
-        if (leader) tc::bulk_wait_read0();
-        tc::named_bar(1 + wg, 128);
+        uint8_t* ostage = kv0 + (kt & 1) * Cf::KVSTAGE;   // [dV | dK] over the tile's dead [K | V]
         tmem_row64_to_smem_sw128(DV + lanes, 1.f, ostage, r);
         tmem_row64_to_smem_sw128(DK + lanes, a.scale, ostage + Cf::KB, r);
         tc::tc_fence_before();
@@ -1854,6 +1851,8 @@ __global__ void __launch_bounds__(320, 1)
           tc::tma_store_3d(&tmdV, ostage, 0, u0, bh);
           tc::tma_store_3d(&tmdK, ostage + Cf::KB, 0, u0, bh);
           tc::bulk_commit();
+          tc::bulk_wait_read0();                 // the stores have read the staging: K / V may reload
+          tc::mbar_arrive(&kvempty[kt & 1]);
         }
       }
     }
