@@ -15,9 +15,10 @@ for dt in (torch.bfloat16, torch.float32):
         dy = torch.randn(y.shape, device="cuda", generator=g).to(dt)
         s.stack_backward(x0, saved, dy, L, R, NLy, mode)
     for cls in (s.LLSAStream, s.SAStream):
-        st = cls(B, H, D, L, R, NLy, dtype=dt)
-        for t in range(40):
-            st.step(torch.randn(B, H, D, device="cuda", generator=g).to(dt))
-        st.flush()
+        for (Ls, Rs) in ((L, R), (32, 16), (3, 1)):   # (32, 16): two query m-tiles on the mma.sync step
+            st = cls(B, H, D, Ls, Rs, NLy, dtype=dt)
+            for t in range(40):
+                st.step(torch.randn(B, H, D, device="cuda", generator=g).to(dt))
+            st.flush()
 torch.cuda.synchronize()
 print("done")
