@@ -917,9 +917,11 @@ template <int NB, int RM> struct LFCfg {
   static constexpr int KBB = NB * 128;
   static constexpr int SB = 112 * 128;
   static constexpr int STAGE = QB + 2 * KBB + 2 * SB;      // Q | Kb | Vb | Ks | Vs
-  static constexpr int XB = 2 * 128 * 128;                 // PS per warpgroup
+  static constexpr int XB = 2 * 128 * 128;                 // PS (shared by the warpgroups, see below)
   static constexpr int SCR = 128 * RM * 4;                 // stair scores per warpgroup
-  static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
+  // three stages where they fit (the warpgroups otherwise wait on the TMA loads)
+  static constexpr int NSTG = 1024 + 3 * STAGE + XB + 2 * SCR + 128 + 256 <= 232448 ? 3 : 2;
+  static constexpr int SMEM = 1024 + NSTG * STAGE + XB + 2 * SCR + 128 + 256;
   static_assert(NB + 64 <= 256 && SMEM <= 232448, "TMEM / shared memory");
 };
 
@@ -933,13 +935,14 @@ __global__ void __launch_bounds__(320, 1)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;
-  uint8_t* xps0 = smem + 2 * Cf::STAGE;
-  uint8_t* scr0 = xps0 + 2 * Cf::XB;
+  constexpr int NSTG = Cf::NSTG;
+  uint8_t* xps0 = smem + NSTG * Cf::STAGE;   // P_stair tile, one for both warpgroups
+  uint8_t* scr0 = xps0 + Cf::XB;
   uint8_t* zrow = scr0 + 2 * Cf::SCR;
   uint64_t* bars = reinterpret_cast<uint64_t*>(zrow + 128);
-  uint64_t* full = bars;          // [2]
-  uint64_t* empty = full + 2;     // [2] (released by the epilogue leader)
-  uint64_t* sfull = empty + 2;    // [2]
+  uint64_t* full = bars;          // [NSTG]
+  uint64_t* empty = full + NSTG;  // [NSTG] (released by the epilogue leader)
+  uint64_t* sfull = empty + NSTG; // [2]
   uint64_t* pfull = sfull + 2;    // [2] (128)
   uint64_t* ofull = pfull + 2;    // [2]
   uint64_t* tfree = ofull + 2;    // [2] (128)
@@ -952,13 +955,13 @@ __global__ void __launch_bounds__(320, 1)
   const int nme = blockIdx.x < nitems ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int qbytes = C * HZ * 128, sbytes = R * HZ * 128;
 
-  for (int o = tid * 16; o < 2 * Cf::STAGE + 2 * Cf::XB + 2 * Cf::SCR + 128; o += 320 * 16)
+  for (int o = tid * 16; o < NSTG * Cf::STAGE + Cf::XB + 2 * Cf::SCR + 128; o += 320 * 16)
     *reinterpret_cast<uint4*>(smem + o) = make_uint4(0u, 0u, 0u, 0u);
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmKb); tc::tma_prefetch_desc(&tmVb);
     tc::tma_prefetch_desc(&tmKs); tc::tma_prefetch_desc(&tmVs); tc::tma_prefetch_desc(&tmO);
+    for (int i = 0; i < NSTG; ++i) { tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      tc::mbar_init(&full[i], 1); tc::mbar_init(&empty[i], 1);
       tc::mbar_init(&sfull[i], 1); tc::mbar_init(&pfull[i], 128);
       tc::mbar_init(&ofull[i], 1); tc::mbar_init(&tfree[i], 128);
     }
@@ -988,9 +991,9 @@ __global__ void __launch_bounds__(320, 1)
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / nit, h0 = (g % nit) * HZ;
-        const int s = k & 1;
-        prefetch(k + 2);
-        if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
+        const int s = k % NSTG;
+        prefetch(k + NSTG);
+        if (k >= NSTG) tc::mbar_wait(&empty[s], ((k - NSTG) / NSTG) & 1);
         uint8_t* sb = stage0 + s * Cf::STAGE;
         tc::mbar_expect_tx(&full[s], qbytes + 2 * Cf::KBB + 2 * sbytes);
         tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);
@@ -1008,16 +1011,16 @@ __global__ void __launch_bounds__(320, 1)
       int ns = 0, no = 0;
       while (no < nme) {
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1,
-                                          tc::smem_u32(&full[ns & 1]), (ns >> 1) & 1,
+                                          tc::smem_u32(&full[ns % NSTG]), (ns / NSTG) & 1,
                                           tc::smem_u32(&tfree[ns & 1]), ((ns + 2) >> 1) & 1,
                                           tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1);
         if (no < ns && (m & 1)) {   // O of item no
           tc::tc_fence_after();
           const int b = no & 1;
-          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t sb = tc::smem_u32(stage0 + (no % NSTG) * Cf::STAGE);
           const uint32_t vb = sb + Cf::QB + Cf::KBB, vs = sb + Cf::QB + 2 * Cf::KBB + Cf::SB;
           const uint32_t x = tbase + b * 256;
-          const uint32_t ps = tc::smem_u32(xps0 + b * Cf::XB);
+          const uint32_t ps = tc::smem_u32(xps0);
 #pragma unroll
           for (int j = 0; j < NB / 16; ++j)
             tc::mma_bf16_ts(x + NB, x + 8 * j, tc::desc_mnmajor_sw128(vb + 2048 * j), idO, j > 0);
@@ -1031,7 +1034,7 @@ __global__ void __launch_bounds__(320, 1)
         if (ns < nme && ns < no + 2 && (m & 2) && (ns < 2 || (m & 4))) {   // S_band of item ns
           tc::tc_fence_after();
           const int b = ns & 1;
-          const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
+          const uint32_t sb = tc::smem_u32(stage0 + (ns % NSTG) * Cf::STAGE);
           const uint32_t q = sb, kb = sb + Cf::QB;
 #pragma unroll
           for (int j = 0; j < kD / 16; ++j)
@@ -1051,7 +1054,7 @@ __global__ void __launch_bounds__(320, 1)
     const int c = r / HZ, i = r - c * HZ;
     const bool in_item = c < C;
     const int wq = warp & 3;
-    const uint32_t psa = tc::smem_u32(xps0 + wg * Cf::XB), sca = tc::smem_u32(scr0 + wg * Cf::SCR);
+    const uint32_t psa = tc::smem_u32(xps0), sca = tc::smem_u32(scr0 + wg * Cf::SCR);
     const uint32_t za = tc::smem_u32(zrow);
     for (int k = wg; k < nme; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
@@ -1059,9 +1062,10 @@ __global__ void __launch_bounds__(320, 1)
       const int b = wg, use = k >> 1;
       const int h = h0 + i, t = h - c;
       const bool row_ok = in_item && t >= 0 && t < T;
-      uint8_t* sbp = stage0 + b * Cf::STAGE;
+      const int st = k % NSTG;
+      uint8_t* sbp = stage0 + st * Cf::STAGE;
       const uint32_t sb = tc::smem_u32(sbp);
-      tc::mbar_wait(&full[b], use & 1);
+      tc::mbar_wait(&full[st], (k / NSTG) & 1);
       // ---- staircase scores S[c][c'] = q_(h-c, c) . k_(h-c', c') on mma.sync: per horizon ceil(C/16)
       //      x RM/8 blocks of 16 x 8 (two horizons per iteration), through the scratch [128][RM]
       {
@@ -1157,7 +1161,9 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < NB / 8; ++j)
         tc::tmem_st4(x + 4 * j, pack_bf16(s[8 * j], s[8 * j + 1]), pack_bf16(s[8 * j + 2], s[8 * j + 3]),
                      pack_bf16(s[8 * j + 4], s[8 * j + 5]), pack_bf16(s[8 * j + 6], s[8 * j + 7]));
-      // P_stair -> this warpgroup's PS (its previous item's PV MMA completed before that epilogue)
+      // P_stair -> PS, shared by the warpgroups: item k - 1's PV MMA (the other warpgroup's) must
+      // have read it (every item writes the same positions; the rest stays zero)
+      if (k > 0) tc::mbar_wait(&ofull[(k - 1) & 1], ((k - 1) >> 1) & 1);
       if (in_item) {
 #pragma unroll
         for (int cp = 0; cp < RM; ++cp)
@@ -1189,7 +1195,7 @@ __global__ void __launch_bounds__(320, 1)
           tc::bulk_commit();
           tc::bulk_wait_read0();
         }
-        tc::mbar_arrive(&empty[b]);
+        tc::mbar_arrive(&empty[st]);
       }
     }
   }
