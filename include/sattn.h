@@ -99,14 +99,17 @@ sattn_status sa_backward(const sattn_desc* desc, const void* Q, const void* K, c
  *   multiple of 8 (16-byte rows); 0 if desc is invalid.
  * sa_forward_p: as sa_forward, and also writes P [B][H][T][ld] (desc->dtype),
  *   P[t][j] = a_{t, t-L+j} (Eq. 5) for j < W, exactly 0 where t-L+j is
- *   outside [0, T-1] (G2) and for j >= W.  Tensor cores for bf16, D = 64,
- *   W <= 64 (forward) / W <= 49 (backward); CUDA cores otherwise
- *   (desc->impl = SATTN_IMPL_TC outside those limits -> SATTN_EUNSUPPORTED).
+ *   outside [0, T-1] (G2) and for j >= W.  Forward on tensor cores for bf16,
+ *   D = 64, W <= 64; CUDA cores otherwise (desc->impl = SATTN_IMPL_TC outside
+ *   that limit -> SATTN_EUNSUPPORTED).
  * sa_backward_p: gradients of <dO, O> with a_t read from P instead of
  *   recomputed (Eq. 7-13); P must come from sa_forward_p on the same inputs.
+ *   Tensor cores for bf16, D = 64: one pass for W <= 49, 48-column sub-bands of
+ *   P (gradients summed in fp32) for 49 < W <= 4096; CUDA cores otherwise.
  *   ws >= sa_backward_p_workspace(desc) bytes (delta_t, fp32: sum_j P_tj dP_tj
- *   on tensor cores, dO_t . O_t on CUDA cores; O is read only by the latter).
- *   Deterministic (no atomics).                                               */
+ *   in the one-pass tensor-core kernels, dO_t . O_t for sub-bands and on CUDA
+ *   cores, where O is read; sub-bands also keep fp32 dQ, dK, dV accumulators in
+ *   ws).  Deterministic (no atomics).                                         */
 int64_t sa_p_ld(const sattn_desc* desc);
 sattn_status sa_forward_p(const sattn_desc* desc, const void* Q, const void* K, const void* V,
                           void* O, float* LSE, void* P, void* stream);

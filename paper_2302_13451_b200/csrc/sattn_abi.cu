@@ -403,8 +403,19 @@ sattn_status sa_forward_p(const sattn_desc* d, const void* Q, const void* K, con
   return ffma_forward_p(d, a, (cudaStream_t)stream);
 }
 
+// the stored-band backward of a band too wide for one tensor-core pass (W > 49) runs as sub-bands
+bool p_bwd_wide(const sattn_desc* d) {
+  const int W = d->L + d->R + 1;
+  return d->impl != SATTN_IMPL_FFMA && d->dtype == SATTN_BF16 && d->D == 64 &&
+         !tc_p_supported(d->dtype, (int)d->D, d->L, d->R, true) && W > 49 && W <= 4096;
+}
+
 size_t sa_backward_p_workspace(const sattn_desc* d) {
-  return validate(d) == SATTN_OK ? (size_t)d->B * d->H * ((d->T + 3) & ~3LL) * sizeof(float) : 0;
+  if (validate(d) != SATTN_OK) return 0;
+  const size_t n = (size_t)d->B * d->H * ((d->T + 3) & ~3LL) * sizeof(float);
+  if (!p_bwd_wide(d)) return n;
+  const size_t w = tc_wide_bwd_ws(d->B * d->H, d->T);   // delta rows + fp32 dQ, dK, dV accumulators
+  return w > n ? w : n;
 }
 
 sattn_status sa_backward_p(const sattn_desc* d, const void* Q, const void* K, const void* V, const void* O,
@@ -419,11 +430,20 @@ sattn_status sa_backward_p(const sattn_desc* d, const void* Q, const void* K, co
   if (ws_bytes < sa_backward_p_workspace(d))
     return fail(SATTN_ECONFIG, "workspace %zu < required %zu bytes", ws_bytes, sa_backward_p_workspace(d));
   const bool tc = d->impl != SATTN_IMPL_FFMA && tc_p_supported(d->dtype, (int)d->D, d->L, d->R, true);
-  if (d->impl == SATTN_IMPL_TC && !tc)
-    return fail(SATTN_EUNSUPPORTED, "tensor-core stored-band backward needs bf16, D=64, L+R+1 <= 49");
+  const bool wide = p_bwd_wide(d);
+  if (d->impl == SATTN_IMPL_TC && !tc && !wide)
+    return fail(SATTN_EUNSUPPORTED, "tensor-core stored-band backward needs bf16, D=64, L+R+1 <= 4096");
   AttnArgs a = make_args(d, false);
   a.Q = Q; a.K = K; a.V = V; a.O = O; a.dO = dO; a.P = const_cast<void*>(P); a.ldp = (int)p_ld(d);
   a.dQ = dQ; a.dK = dK; a.dV = dV; a.delta = static_cast<float*>(ws);
+  if (wide) {
+    r = tc_backward_p_wide(a, (cudaStream_t)stream);
+    if (r != SATTN_OK) return fail(r, "tc_backward_p_wide: %s", tc_last_error());
+    g_launches.fetch_add(1 + 2 * tc_wide_p_parts(d->L, d->R) + 3, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SATTN_ECUDA, "tc_backward_p_wide launch: %s", cudaGetErrorString(e));
+    return SATTN_OK;
+  }
   if (tc) {
     r = tc_backward_p(a, (cudaStream_t)stream);
     if (r != SATTN_OK) return fail(r, "tc_backward_p: %s", tc_last_error());

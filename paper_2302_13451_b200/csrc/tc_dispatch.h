@@ -23,6 +23,10 @@ sattn_status tc_backward_wide(const AttnArgs& a, cudaStream_t st);
 int tc_key_box_rows(int L, int R);   // rows of the K / V box a query tile loads (NK)
 size_t tc_backward_ws_bytes();
 bool tc_p_supported(int dtype, int D, int L, int R, bool backward);   // stored-band mode (NEXT-4)
+// stored-band backward for W > 49: 48-column sub-bands of a_t on the tensor-core kernels (workspace
+// tc_wide_bwd_ws; needs O for delta = dO . O)
+sattn_status tc_backward_p_wide(const AttnArgs& a, cudaStream_t st);
+int tc_wide_p_parts(int L, int R);
 sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st);   // SA tensor-core backward: CTA hand-off rows (fused sweep)
 const char* tc_last_error();

@@ -1124,6 +1124,8 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       tc::tc_fence_after();
       if constexpr (ACC) {   // sub-band of a wide band: add into the fp32 dK / dV rows
+        // PST: ring B (Q, dO) is dead once dV / dK are done and nothing is staged there
+        if (PST && leader) tc::mbar_arrive(&emptyB[k % NSB]);
         float dvr[64], dkr[64];
         tmem_ld64(DV + lanes, dvr);
         tmem_ld64(DK + lanes, dkr);
@@ -1899,9 +1901,12 @@ bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows)
 
 // stored band P [BH][T][ldp] bf16 as (ldp, T, BH); box (ldp, rows, 1), no swizzle (row-major
 // [rows][ldp] in shared memory); rows outside [0, T) load as zeros and are clipped on store.
-bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows) {
+// the stored band [BH][T][row] bf16 (row = ldp, or a wider row of which ldp columns from `base` are
+// mapped: a sub-band of a wide band); box (ldp, rows, 1), no swizzle
+bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows, int row = 0) {
+  const int pitch = row > 0 ? row : ldp;
   cuuint64_t dims[3] = {(cuuint64_t)ldp, (cuuint64_t)T, (cuuint64_t)BH};
-  cuuint64_t strides[2] = {(cuuint64_t)ldp * 2, (cuuint64_t)T * ldp * 2};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)T * pitch * 2};
   cuuint32_t box[3] = {(cuuint32_t)ldp, (cuuint32_t)rows, 1};
   CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (r != CUDA_SUCCESS) {
@@ -2309,6 +2314,76 @@ sattn_status tc_backward_wide(const AttnArgs& a, cudaStream_t st) {
       case 72: r = bwd_wide_sub<72>(aj, st, wa); break;
       case 80: r = bwd_wide_sub<80>(aj, st, wa); break;
       default: g_tc_err = "wide sub-band"; return SATTN_EUNSUPPORTED;
+    }
+    if (r != SATTN_OK) return r;
+  }
+  const long long n8 = rows * 64 / 8;
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dq, reinterpret_cast<bf16*>(a.dQ), n8);
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dk, reinterpret_cast<bf16*>(a.dK), n8);
+  f32_to_bf16_kernel<<<4 * num_sms(), 256, 0, st>>>(wa.dv, reinterpret_cast<bf16*>(a.dV), n8);
+  return SATTN_OK;
+}
+
+// stored-band mode, wide bands (W > 49): the stored row a_t [0, W) is cut into 48-column sub-bands
+// (16-byte aligned column offsets; the last one ends at W, where the row's padding is zero), each
+// an SA band of its own with (L_j, R_j) as above whose probabilities are those columns of a_t.
+// The gradient is the sum of the sub-bands' gradients with the global delta = dO . O (G28): the
+// stored-band K1 / K2 ACC instances accumulate into fp32, then one kernel rounds.
+constexpr int kWideSubP = 48;
+
+template <int CW>
+sattn_status bwd_p_wide_sub(const AttnArgs& a, int row, cudaStream_t st, const WideAcc& wa) {
+  using K2 = DkvCfg<CW>;
+  constexpr int NK = nk_of(CW);
+  const int Tp = (a.T + 3) & ~3;
+  CUtensorMap mp128, mk, mv, mdo, mqN, mpN, mv128, mdoN, mdel;
+  if (!make_map_p(&mp128, a.P, a.T, a.BH, a.ldp, kM, row) || !make_map(&mk, a.K, a.T, a.BH, NK) ||
+      !make_map(&mv, a.V, a.T, a.BH, NK) || !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
+      !make_map(&mqN, a.Q, a.T, a.BH, K2::NQ) || !make_map_p(&mpN, a.P, a.T, a.BH, a.ldp, K2::NQ, row) ||
+      !make_map(&mv128, a.V, a.T, a.BH, kM) || !make_map(&mdoN, a.dO, a.T, a.BH, K2::NQ) ||
+      !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, K2::NQP))
+    return SATTN_ECUDA;
+  TcArgs t = tc_args(a);
+  t.acc_dq = wa.dq; t.acc_dk = wa.dk; t.acc_dv = wa.dv; t.acc_first = wa.first;
+  const int ntiles = (a.T + kM - 1) / kM * a.BH;
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  set_smem(sa_bwd_dq_tc<CW, true, true>, DqCfg<CW>::SMEM);
+  launch_pdl(sa_bwd_dq_tc<CW, true, true>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mp128, mk, mv,
+             mdo, mp128, t);
+  set_smem(sa_bwd_dkdv_tc<CW, true, true>, K2::SMEM_P);
+  launch_pdl(sa_bwd_dkdv_tc<CW, true, true>, dim3(grid), dim3(K2::THREADS), K2::SMEM_P, st, mqN, mpN, mv128, mdoN,
+             mqN, mqN, mdel, mdel, t);
+  return SATTN_OK;
+}
+
+int tc_wide_p_parts(int L, int R) { return (L + R + 1 + kWideSubP - 1) / kWideSubP; }
+
+sattn_status tc_backward_p_wide(const AttnArgs& a, cudaStream_t st) {
+  const int W = a.L + a.R + 1, S = tc_wide_p_parts(a.L, a.R);
+  const long long rows = (long long)a.BH * a.T;
+  const int Tp = (a.T + 3) & ~3;
+  WideAcc wa{};
+  wa.dq = a.delta + 2LL * a.BH * Tp;
+  wa.dk = wa.dq + rows * 64;
+  wa.dv = wa.dk + rows * 64;
+  wide_delta_kernel<<<4 * num_sms(), 256, 0, st>>>(reinterpret_cast<const bf16*>(a.dO), reinterpret_cast<const bf16*>(a.O),
+                                                   a.delta, a.T, Tp, (long long)a.BH * Tp);
+  for (int j = 0; j < S; ++j) {
+    const int o = j * kWideSubP, w = W - o < kWideSubP ? W - o : kWideSubP;
+    AttnArgs aj = a;
+    aj.L = a.L - o;
+    aj.R = o + w - 1 - a.L;
+    aj.P = reinterpret_cast<bf16*>(a.P) + o;
+    aj.ldp = (w + 7) & ~7;
+    wa.first = j == 0;
+    sattn_status r;
+    switch (cw_of(w)) {
+      case 32: r = bwd_p_wide_sub<32>(aj, a.ldp, st, wa); break;
+      case 48: r = bwd_p_wide_sub<48>(aj, a.ldp, st, wa); break;
+      case 64: r = bwd_p_wide_sub<64>(aj, a.ldp, st, wa); break;
+      case 72: r = bwd_p_wide_sub<72>(aj, a.ldp, st, wa); break;
+      case 80: r = bwd_p_wide_sub<80>(aj, a.ldp, st, wa); break;
+      default: g_tc_err = "wide stored-band sub-band"; return SATTN_EUNSUPPORTED;
     }
     if (r != SATTN_OK) return r;
   }

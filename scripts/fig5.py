@@ -6,7 +6,7 @@ For each point: peak device memory of one SA forward + backward through the C AB
 tensor-core kernels at every W: W <= 65 in one launch, wider bands as log-sum-exp-merged sub-bands
 of width <= 49) per training vector (frame),
 and its time, for both SA modes -- LSE + recompute (sa_forward / sa_backward) and the paper's own
-stored band a_t (sa_forward_p / sa_backward_p; tensor cores for W <= 49) -- next to masked
+stored band a_t (sa_forward_p / sa_backward_p; one tensor-core pass for W <= 49, 48-column sub-bands beyond) -- next to masked
 acausal attention (MAA) as PyTorch computes it (dense T x T scores,
 boolean band mask, softmax, autograd), which is what the paper compares against.  Writes
 profiles/r1/fig5.json and prints a markdown table.  Inputs are synthetic (iid N(0,1))."""
@@ -73,7 +73,8 @@ def run(H, B=8):
         m_maa, t_maa = measure(maa)
         frames = B * T
         rows.append({"H": H, "W": W, "L": L, "R": R, "kernels": "tcgen05" if W <= 65 else f"tcgen05 x {-(-W // 49)} sub-bands",
-                     "band_kernels": "tcgen05" if W <= 49 else ("tcgen05 fwd + ffma bwd" if W <= 64 else "ffma"),
+                     "band_kernels": "tcgen05" if W <= 49 else (f"tcgen05 fwd + tcgen05 x {-(-W // 48)} sub-band bwd" if W <= 64
+                                                              else f"ffma fwd + tcgen05 x {-(-W // 48)} sub-band bwd"),
                      "sa_bytes_per_frame": m_sa / frames, "maa_bytes_per_frame": m_maa / frames,
                      "sa_band_bytes_per_frame": m_sb / frames,
                      "sa_ms": t_sa, "sa_band_ms": t_sb, "maa_ms": t_maa})

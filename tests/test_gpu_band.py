@@ -18,6 +18,8 @@ CASES = [
     ((2, 2, 1750, 64), 32, 8, "bf16"), ((1, 2, 300, 64), 32, 16, "bf16"), ((1, 3, 777, 64), 32, 32, "bf16"),
     ((1, 2, 130, 16), 7, 3, "bf16"), ((1, 2, 129, 64), 0, 0, "bf16"), ((3, 2, 300, 64), 24, 0, "bf16"),
     ((1, 3, 777, 64), 16, 8, "bf16"), ((2, 1, 1000, 64), 40, 23, "bf16"), ((1, 1, 5, 64), 2, 2, "bf16"),
+    # wide bands: the backward as 48-column sub-bands of a_t on tensor cores (W = 57, 351, 490)
+    ((1, 2, 300, 64), 32, 24, "bf16"), ((1, 2, 600, 64), 200, 150, "bf16"), ((1, 1, 1000, 64), 245, 244, "bf16"),
 ]
 
 
@@ -28,7 +30,8 @@ def _ld(L, R):
 @pytest.mark.parametrize("impl", ["auto", "ffma"])
 @pytest.mark.parametrize("shape,L,R,dt", CASES)
 def test_sa_stored_band(shape, L, R, dt, impl):
-    # auto: tensor cores for bf16 D=64 (forward W <= 64, backward W <= 49), CUDA cores otherwise
+    # auto: tensor cores for bf16 D=64 (forward W <= 64; backward W <= 49 in one pass, wider bands
+    # as 48-column sub-bands), CUDA cores otherwise
     s = sattn()
     if impl == "ffma" and dt == "f32":
         pytest.skip("fp32 runs on the CUDA-core kernels under auto already")
@@ -72,9 +75,10 @@ def test_sa_stored_band_errors():
         s.sa_forward_p(q.float(), q.float(), q.float(), 3, 1, impl="tc")
     with pytest.raises(s.SattnError):
         s.sa_forward_p(q, q, q, 40, 40, impl="tc")        # W = 81 > 64
-    o, lse, p = s.sa_forward_p(q, q, q, 32, 24, impl="tc")
+    q32 = torch.zeros(1, 1, 16, 32, device="cuda", dtype=torch.bfloat16)
+    o, lse, p = s.sa_forward_p(q32, q32, q32, 3, 1)
     with pytest.raises(s.SattnError):
-        s.sa_backward_p(q, q, q, o, p, q, 32, 24, impl="tc")   # W = 57 > 49
+        s.sa_backward_p(q32, q32, q32, o, p, q32, 3, 1, impl="tc")   # D = 32: no tensor-core path
     with pytest.raises(s.SattnError):
         s.sa_forward_p(q.cpu(), q.cpu(), q.cpu(), 3, 1)
 
