@@ -19,8 +19,9 @@ B=8 batch, no data-path collective ("weak"); value = frames of all ranks / max-o
 time.  Sub-objects: "llsa" = M2, the LLSA step with the B*H = 96 (b, h) units split over the
 ranks (strong scaling); "large" = M3, wav2vec2-large (B=64, H=16, 24 layers) batch-sharded
 (strong); "hour" = M4, one hour-long stream time-sharded through the library's NCCL halo
-exchange (sa_forward_tsharded / sa_backward_tsharded, strong), with "hour.llsa" the same stream
-through the LLSA time-sharded calls (llsa_forward_tsharded / llsa_backward_tsharded).
+exchange (stored-band mode: sa_forward_p_tsharded / sa_backward_p_tsharded, strong; "hour.lse_mode" the
+LSE-mode calls), with "hour.llsa" the same stream through the LLSA time-sharded calls
+(llsa_forward_tsharded / llsa_backward_tsharded).
 
 --impl reference runs the CPU oracle (oracle/, numpy fp64) on a bounded sample of
 the same workload (the task's reference arm for this paper-only reference).
@@ -380,9 +381,16 @@ def run_gpu(args):
     if not args.no_hour:
         torch.cuda.empty_cache()
         try:
-            hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
+            hour = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm, band=True)
         except Exception as e:   # the headline line must not depend on this sub-measurement
             hour = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
+        try:
+            hour_lse = run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm, band=False)
+        except Exception as e:
+            hour_lse = {"error": f"{type(e).__name__}: {e}"[:300]}
+        if isinstance(hour, dict):
+            hour["lse_mode"] = hour_lse
         torch.cuda.empty_cache()
         try:
             hour_llsa = run_hour_llsa(args, sattn, dev, rnd, barrier, world, rank, stream, hbm)
@@ -688,12 +696,13 @@ def run_mode(args, sattn, dev, rnd, barrier, world, stream, hbm, mode):
             "workload": f"12 layers x ({kf} + {kb}), untied per-layer inputs, bf16"}
 
 
-def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
+def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm, band=True):
     """M4 (BASELINE configs[4]): one hour-long stream (B=1, H=12, T=180,000 frames = 1 h at 50 Hz),
-    12 layers x (SA fwd + SA bwd), bf16, time-sharded over the ranks through the library
-    (sa_forward_tsharded / sa_backward_tsharded on margined shards: rank r owns frames [t0, t1),
-    128-aligned; each call exchanges the halo rows with its neighbours over NCCL on a library
-    stream while the interior tiles run).  At N = 1 the same calls run with no neighbours.
+    12 layers x (SA fwd + SA bwd), bf16, time-sharded over the ranks through the library on margined
+    shards (rank r owns frames [t0, t1), 128-aligned; each call exchanges the halo rows with its
+    neighbours over NCCL on a library stream while the interior tiles run).  band=True: the stored-band
+    mode (sa_forward_p_tsharded / sa_backward_p_tsharded, as the headline); False: LSE + recompute
+    (sa_forward_tsharded / sa_backward_tsharded).  At N = 1 the same calls run with no neighbours.
     Strong scaling: value = T frames / max-over-ranks step time."""
     import ctypes
     import torch
@@ -710,23 +719,29 @@ def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
     if nws == 0:
         raise RuntimeError(L_.sattn_last_error().decode())
     ws = torch.empty(nws, device=dev, dtype=torch.uint8)
+    ld = (L + R + 1 + 7) // 8 * 8
     Qm, Km, Vm, dOm = ([sd.margined(Bh, H, n, D, device=dev) for _ in range(n_layers)] for _ in range(4))
     for bufs in (Qm, Km, Vm, dOm):
         for m in bufs:
             sd.local(m, n).copy_(rnd(Bh, H, n, D))
     Om = [sd.margined(Bh, H, n, D, device=dev) for _ in range(n_layers)]
     LSEm = [sd.margined(Bh, H, n, None, dtype=torch.float32, device=dev) for _ in range(n_layers)]
+    Pm = [sd.margined(Bh, H, n, ld, device=dev) for _ in range(n_layers)] if band else None
     dQm, dKm, dVm = (sd.margined(Bh, H, n, D, device=dev) for _ in range(3))
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
 
     def step():
         sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         for l in range(n_layers):
-            st = L_.sa_forward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(Om[l]), P(LSEm[l]), P(ws), nws, sp)
+            st = (L_.sa_forward_p_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(Om[l]), P(LSEm[l]), P(Pm[l]),
+                                           P(ws), nws, sp) if band else
+                  L_.sa_forward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(Om[l]), P(LSEm[l]), P(ws), nws, sp))
             assert st == 0, L_.sattn_last_error()
         for l in reversed(range(n_layers)):
-            st = L_.sa_backward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(LSEm[l]), P(dOm[l]), P(dQm),
-                                         P(dKm), P(dVm), P(ws), nws, sp)
+            st = (L_.sa_backward_p_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(Pm[l]), P(dOm[l]), P(dQm),
+                                            P(dKm), P(dVm), P(ws), nws, sp) if band else
+                  L_.sa_backward_tsharded(tdp, d._h, P(Qm[l]), P(Km[l]), P(Vm[l]), P(LSEm[l]), P(dOm[l]), P(dQm),
+                                          P(dKm), P(dVm), P(ws), nws, sp))
             assert st == 0, L_.sattn_last_error()
 
     step()
@@ -755,13 +770,20 @@ def run_hour(args, sattn, dev, rnd, barrier, world, rank, stream, hbm):
     ms_loc = a0.elapsed_time(a1) / k
     ms = _max_ms(ms_loc, world, dev)
     d.close()
+    graphed = graph is not None
+    del graph
     units = Bh * H * n
+    W = L + R + 1
+    fb, bb = (FWD_BYTES + 2 * W, 896 + 2 * W) if band else (FWD_BYTES, BWD_BYTES)
+    calls = ("sa_forward_p_tsharded / sa_backward_p_tsharded (stored band)" if band else
+             "sa_forward_tsharded / sa_backward_tsharded (LSE + recompute)")
     return {"value": round(Bh * Th / (ms / 1e3), 1), "unit": UNIT, "ms_per_step": round(ms, 3), "steps": k,
-            "scaling": "strong", "hbm_frac": round((FWD_BYTES + BWD_BYTES) * units * n_layers / (ms_loc / 1e3) / 1e9 / hbm, 4),
+            "scaling": "strong", "mode": "band" if band else "lse",
+            "hbm_frac": round((fb + bb) * units * n_layers / (ms_loc / 1e3) / 1e9 / hbm, 4),
             "workload": f"M4: hour-long stream B=1, H={H}, T={Th}, (L,R)=({L},{R}), {n_layers} layers x (SA fwd + bwd) "
-                        f"through sa_forward_tsharded / sa_backward_tsharded, time-sharded x{world} "
+                        f"through {calls}, time-sharded x{world} "
                         f"({'NCCL halo exchange overlapped with interior tiles' if world > 1 else 'no neighbours'}), "
-                        f"{'CUDA graph' if graph is not None else 'eager'}",
+                        f"{'CUDA graph' if graphed else 'eager'}",
             "frames_per_rank": n, "halo_exchange": "nccl" if world > 1 else None}
 
 

@@ -241,6 +241,15 @@ sattn_status sa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, voi
 sattn_status sa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
                                   const void* V, const float* LSE, void* dO, void* dQ, void* dK, void* dV,
                                   void* ws, size_t ws_bytes, void* stream);
+/* The stored-band mode (sa_forward_p / sa_backward_p) on the same margined shards, with P margined
+ * too: [B][H][M + T + M][sa_p_ld(desc)].  The forward's exchange and overlap are as above and it
+ * writes the band rows of the whole slab; the backward exchanges dO only (the halo queries' delta =
+ * rowsum(P o dP) is formed from the margins).  Tensor cores, L + R + 1 <= 49.  Same workspace query. */
+sattn_status sa_forward_p_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,
+                                   float* LSE, void* P, void* ws, size_t ws_bytes, void* stream);
+sattn_status sa_backward_p_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
+                                    const void* V, const void* P, void* dO, void* dQ, void* dK, void* dV, void* ws,
+                                    size_t ws_bytes, void* stream);
 /* host-only: out6 = {hl, hr, slab frames, query tiles, first interior tile, first right-edge tile} */
 sattn_status sattn_tshard_geometry(const sattn_tshard_desc* td, int rank, int world, int64_t* out6);
 

@@ -26,6 +26,8 @@ bool tc_p_supported(int dtype, int D, int L, int R, bool backward);   // stored-
 // stored-band backward for W > 49: 48-column sub-bands of a_t on the tensor-core kernels (workspace
 // tc_wide_bwd_ws; needs O for delta = dO . O)
 sattn_status tc_backward_p_wide(const AttnArgs& a, cudaStream_t st);
+// the stored-band backward in phases (bit 0: K1 over the launch's query tiles, bit 1: K2), for time shards
+sattn_status tc_backward_p_phase(const AttnArgs& a, cudaStream_t st, int phase);
 int tc_wide_p_parts(int L, int R);
 sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st);
 sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st);   // SA tensor-core backward: CTA hand-off rows (fused sweep)

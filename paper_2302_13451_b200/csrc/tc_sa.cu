@@ -1903,10 +1903,11 @@ bool make_map4(CUtensorMap* m, const void* base, int T, int BH, int C, int rows)
 // [rows][ldp] in shared memory); rows outside [0, T) load as zeros and are clipped on store.
 // the stored band [BH][T][row] bf16 (row = ldp, or a wider row of which ldp columns from `base` are
 // mapped: a sub-band of a wide band); box (ldp, rows, 1), no swizzle
-bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows, int row = 0) {
-  const int pitch = row > 0 ? row : ldp;
+bool make_map_p(CUtensorMap* m, const void* base, int T, int BH, int ldp, int rows, int row = 0, int ld = 0) {
+  const int pitch = row > 0 ? row : ldp;   // elements per stored row
+  const int frames = ld > 0 ? ld : T;      // rows per head (a time shard's margined length)
   cuuint64_t dims[3] = {(cuuint64_t)ldp, (cuuint64_t)T, (cuuint64_t)BH};
-  cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)T * pitch * 2};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)frames * pitch * 2};
   cuuint32_t box[3] = {(cuuint32_t)ldp, (cuuint32_t)rows, 1};
   CUresult r = tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
   if (r != CUDA_SUCCESS) {
@@ -2004,7 +2005,7 @@ sattn_status fwd_launch(const AttnArgs& a, cudaStream_t st, const WideAcc* wa = 
   if (!make_map(&mq, a.Q, a.T, a.BH, kM, a.ld) || !make_map(&mk, a.K, a.T, a.BH, C::NK, a.ld) ||
       !make_map(&mv, a.V, a.T, a.BH, C::NK, a.ld) || !make_map(&mo, a.Out, a.T, a.BH, kM, a.ld))
     return SATTN_ECUDA;
-  if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM)) return SATTN_ECUDA;
+  if (PST && !make_map_p(&mp, a.P, a.T, a.BH, a.ldp, kM, 0, a.ld)) return SATTN_ECUDA;
   set_smem(sa_fwd_tc<CW, PST, ACC>, C::SMEM);
   const int ntiles = ta.nkt * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
@@ -2456,42 +2457,51 @@ sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st) {
   return SATTN_EUNSUPPORTED;
 }
 
+// phase as bwd_launch: bit 0 = K1 over the launch's query tiles, bit 1 = K2 over every key tile
 template <int CW>
-sattn_status bwd_p_launch(const AttnArgs& a, cudaStream_t st) {
+sattn_status bwd_p_launch(const AttnArgs& a, cudaStream_t st, int phase = 3) {
   using K2 = DkvCfg<CW>;
   static_assert(K2::SMEM_P <= 232448, "stored-band K2 stage");
   constexpr int NK = nk_of(CW);
   const int Tp = (a.T + 3) & ~3;
+  const int ld = a.ld;
   CUtensorMap mp128, mk, mv, mdo, mdq, mqN, mpN, mv128, mdoN, mdk, mdv, mdel;
-  if (!make_map_p(&mp128, a.P, a.T, a.BH, a.ldp, kM) || !make_map(&mk, a.K, a.T, a.BH, NK) ||
-      !make_map(&mv, a.V, a.T, a.BH, NK) || !make_map(&mdo, a.dO, a.T, a.BH, kM) ||
-      !make_map(&mdq, a.dQ, a.T, a.BH, kM) || !make_map(&mqN, a.Q, a.T, a.BH, K2::NQ) ||
-      !make_map_p(&mpN, a.P, a.T, a.BH, a.ldp, K2::NQ) || !make_map(&mv128, a.V, a.T, a.BH, kM) ||
-      !make_map(&mdoN, a.dO, a.T, a.BH, K2::NQ) || !make_map(&mdk, a.dK, a.T, a.BH, kM) ||
-      !make_map(&mdv, a.dV, a.T, a.BH, kM) || !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, K2::NQP))
+  if (!make_map_p(&mp128, a.P, a.T, a.BH, a.ldp, kM, 0, ld) || !make_map(&mk, a.K, a.T, a.BH, NK, ld) ||
+      !make_map(&mv, a.V, a.T, a.BH, NK, ld) || !make_map(&mdo, a.dO, a.T, a.BH, kM, ld) ||
+      !make_map(&mdq, a.dQ, a.T, a.BH, kM, ld) || !make_map(&mqN, a.Q, a.T, a.BH, K2::NQ, ld) ||
+      !make_map_p(&mpN, a.P, a.T, a.BH, a.ldp, K2::NQ, 0, ld) || !make_map(&mv128, a.V, a.T, a.BH, kM, ld) ||
+      !make_map(&mdoN, a.dO, a.T, a.BH, K2::NQ, ld) || !make_map(&mdk, a.dK, a.T, a.BH, kM, ld) ||
+      !make_map(&mdv, a.dV, a.T, a.BH, kM, ld) || !make_map_f32_rows(&mdel, a.delta, a.T, Tp, a.BH, K2::NQP))
     return SATTN_ECUDA;
+  if (phase & 1) {
+    const TcArgs t1 = tc_args(a);
+    const int nt1 = t1.nkt * a.BH;
+    set_smem(sa_bwd_dq_tc<CW, true>, DqCfg<CW>::SMEM);
+    launch_pdl(sa_bwd_dq_tc<CW, true>, dim3(nt1 < num_sms() ? nt1 : num_sms()), dim3(DqCfg<CW>::THREADS),
+               DqCfg<CW>::SMEM, st, mp128, mk, mv, mdo, mdq, t1);
+  }
+  if (!(phase & 2)) return SATTN_OK;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
-  set_smem(sa_bwd_dq_tc<CW, true>, DqCfg<CW>::SMEM);
-  launch_pdl(sa_bwd_dq_tc<CW, true>, dim3(grid), dim3(DqCfg<CW>::THREADS), DqCfg<CW>::SMEM, st, mp128, mk, mv, mdo,
-             mdq, tc_args(a));
   set_smem(sa_bwd_dkdv_tc<CW, true>, K2::SMEM_P);
   launch_pdl(sa_bwd_dkdv_tc<CW, true>, dim3(grid), dim3(K2::THREADS), K2::SMEM_P, st, mqN, mpN, mv128, mdoN, mdk,
              mdv, mdel, mdel, tc_args(a));
   return SATTN_OK;
 }
 
-sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st) {
+sattn_status tc_backward_p_phase(const AttnArgs& a, cudaStream_t st, int phase) {
   switch (cw_of(a.L + a.R + 1)) {
-    case 32: return bwd_p_launch<32>(a, st);
-    case 48: return bwd_p_launch<48>(a, st);
-    case 64: return bwd_p_launch<64>(a, st);
-    case 72: return bwd_p_launch<72>(a, st);
-    case 80: return bwd_p_launch<80>(a, st);
+    case 32: return bwd_p_launch<32>(a, st, phase);
+    case 48: return bwd_p_launch<48>(a, st, phase);
+    case 64: return bwd_p_launch<64>(a, st, phase);
+    case 72: return bwd_p_launch<72>(a, st, phase);
+    case 80: return bwd_p_launch<80>(a, st, phase);
   }
   g_tc_err = "band too wide for the tensor-core stored-band backward";
   return SATTN_EUNSUPPORTED;
 }
+
+sattn_status tc_backward_p(const AttnArgs& a, cudaStream_t st) { return tc_backward_p_phase(a, st, 3); }
 size_t tc_backward_ws_bytes() { return 0; }
 
 bool tc_llsa_bwd_supported(int dtype, int D, int L, int R) {

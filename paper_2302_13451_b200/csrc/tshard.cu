@@ -633,6 +633,83 @@ sattn_status llsa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, 
   return llsa_backward(&s.slab, Q, K, V, O, LSE, dO, dQ, dK, dV, (char*)ws + nh, ws_bytes - nh, stream);
 }
 
+// ------------------------------------------------------------------------------------------
+// The stored-band mode (the paper's a_t) on the same margined shards: the forward exchanges
+// K, V, Q as above and writes the band rows of the whole slab (the halo rows' a_t are exact for the
+// same reason their LSE is); the backward exchanges dO only, K1 forms the halo queries' delta =
+// rowsum(P o dP) from the margins (G26), K2 reads the band window.  P is margined like the other
+// tensors: [B][H][M + T + M][sa_p_ld(desc)].
+// ------------------------------------------------------------------------------------------
+sattn_status sa_forward_p_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,
+                                   float* LSE, void* P, void* ws, size_t ws_bytes, void* stream) {
+  Shard s;
+  sattn_status r = shard_setup(td, d, s);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !O || !LSE || !P) return set_error(SATTN_EARG, "NULL pointer");
+  if (!tc_p_supported(td->local.dtype, (int)td->local.D, td->local.L, td->local.R, true))
+    return set_error(SATTN_EUNSUPPORTED, "time-sharded stored-band SA needs L + R + 1 <= 49");
+  HaloT h[3];
+  fwd_halos(s, Q, K, V, h);
+  const size_t need = halo_ws(s, h, 3);
+  if (need && (!ws || ws_bytes < need)) return set_error(SATTN_ECONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool ext = d->comm == nullptr;
+  if (!ext && (r = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return r;
+  const int ldp = (s.a.L + s.a.R + 1 + 7) & ~7;
+  s.a.Q = at(Q, s.off); s.a.K = at(K, s.off); s.a.V = at(V, s.off);
+  s.a.Out = at(O, s.off);
+  s.a.LSEout = LSE + (kMargin - s.hl);
+  s.a.P = at(P, (long long)(kMargin - s.hl) * ldp);
+  s.a.ldp = ldp;
+  const int nk = tc_key_box_rows(s.a.L, s.a.R);
+  return split_run(d, s, nk, st, true, [&](const AttnArgs& a, bool interior) -> sattn_status {
+    sattn_status rr;
+    if (!interior && ext && (rr = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return rr;
+    if ((rr = tc_forward_p(a, st)) != SATTN_OK) return set_error(rr, tc_last_error());
+    count_launches(1);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SATTN_OK : cuda_fail("time-sharded stored-band forward launch", e);
+  });
+}
+
+sattn_status sa_backward_p_tsharded(const sattn_tshard_desc* td, sattn_dist* d, const void* Q, const void* K,
+                                    const void* V, const void* P, void* dO, void* dQ, void* dK, void* dV, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  Shard s;
+  sattn_status r = shard_setup(td, d, s);
+  if (r != SATTN_OK) return r;
+  if (!Q || !K || !V || !P || !dO || !dQ || !dK || !dV || !ws) return set_error(SATTN_EARG, "NULL pointer");
+  if (!tc_p_supported(td->local.dtype, (int)td->local.D, td->local.L, td->local.R, true))
+    return set_error(SATTN_EUNSUPPORTED, "time-sharded stored-band SA needs L + R + 1 <= 49");
+  HaloT h[1];
+  bwd_halos(s, dO, h);
+  const size_t nh = halo_ws(s, h, 1), nrows = bwd_rows_ws(s);
+  if (ws_bytes < nh + nrows) return set_error(SATTN_ECONFIG, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool ext = d->comm == nullptr;
+  if (!ext && (r = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return r;
+  const int ldp = (s.a.L + s.a.R + 1 + 7) & ~7;
+  s.a.Q = at(Q, s.off); s.a.K = at(K, s.off); s.a.V = at(V, s.off);
+  s.a.dO = at(dO, s.off);
+  s.a.P = const_cast<bf16*>(at(P, (long long)(kMargin - s.hl) * ldp));
+  s.a.ldp = ldp;
+  s.a.dQ = at(dQ, s.off); s.a.dK = at(dK, s.off); s.a.dV = at(dV, s.off);
+  s.a.delta = reinterpret_cast<float*>((char*)ws + nh);
+  const int nk = tc_key_box_rows(s.a.L, s.a.R);
+  r = split_run(d, s, nk, st, true, [&](const AttnArgs& a, bool interior) -> sattn_status {
+    sattn_status rr;
+    if (!interior && ext && (rr = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return rr;
+    if ((rr = tc_backward_p_phase(a, st, 1)) != SATTN_OK) return set_error(rr, tc_last_error());
+    count_launches(1);
+    return SATTN_OK;
+  });
+  if (r != SATTN_OK) return r;
+  if ((r = tc_backward_p_phase(s.a, st, 2)) != SATTN_OK) return set_error(r, tc_last_error());
+  count_launches(1);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SATTN_OK : cuda_fail("time-sharded stored-band backward launch", e);
+}
+
 // host-only geometry of a shard (for tests and tooling): slab rows and the tile split
 sattn_status sattn_tshard_geometry(const sattn_tshard_desc* td, int rank, int world, int64_t* out6) {
   if (!out6) return set_error(SATTN_EARG, "out is NULL");

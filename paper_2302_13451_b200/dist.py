@@ -48,6 +48,8 @@ EXPORTS = {
     "sa_forward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sa_backward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "sattn_tshard_geometry": (_I, [_PT, _I, _I, ctypes.POINTER(ctypes.c_int64)]),
+    "sa_forward_p_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
+    "sa_backward_p_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
     "llsa_tshard_margin": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32]),
     "llsa_tsharded_workspace": (_SZ, [_PT, _P]),
     "llsa_forward_tsharded": (_I, [_PT, _P, _P, _P, _P, _P, _P, _P, _SZ, _P]),
@@ -248,6 +250,37 @@ def sa_backward_tsharded(qm, km, vm, lsem, dom, L: int, R: int, t0: int, T_globa
            "sa_backward_tsharded")
     return dq, dk, dv
 
+
+def sa_forward_p_tsharded(qm, km, vm, L: int, R: int, t0: int, T_global: int, d: Dist, scale=None):
+    """The stored-band forward on margined shards -> margined (o, lse, p); p [B, H, M + T_loc + M, ld]
+    (ld = W rounded to 8), its local rows = the unsharded sa_forward_p's band rows."""
+    td = _tdesc_from(qm, L, R, t0, T_global, scale)
+    for t in (km, vm):
+        if t.shape != qm.shape or t.dtype != qm.dtype:
+            raise SattnError("q, k, v must share shape and dtype")
+    ld = (L + R + 1 + 7) // 8 * 8
+    om = torch.zeros_like(qm)
+    lsem = torch.zeros(qm.shape[:-1], dtype=torch.float32, device=qm.device)
+    pm = torch.zeros(qm.shape[:-1] + (ld,), dtype=qm.dtype, device=qm.device)
+    ws = d._workspace(td, qm.device)
+    _check(_lib().sa_forward_p_tsharded(ctypes.byref(td), d._h, _ptr(qm), _ptr(km), _ptr(vm), _ptr(om), _ptr(lsem),
+                                        _ptr(pm), _ptr(ws), ws.numel(), _stream()), "sa_forward_p_tsharded")
+    return om, lsem, pm
+
+
+def sa_backward_p_tsharded(qm, km, vm, pm, dom, L: int, R: int, t0: int, T_global: int, d: Dist, scale=None):
+    """Margined dq, dk, dv from the stored band (local rows = the unsharded sa_backward_p's).  q, k, v,
+    p: the forward's margined buffers; dom: margined dO (its margins are filled here)."""
+    td = _tdesc_from(qm, L, R, t0, T_global, scale)
+    ld = (L + R + 1 + 7) // 8 * 8
+    if dom.shape != qm.shape or pm.shape != qm.shape[:-1] + (ld,) or pm.dtype != qm.dtype:
+        raise SattnError("dO must be shaped like q and p [B, H, M + T_loc + M, ld] in q's dtype")
+    dq, dk, dv = torch.zeros_like(qm), torch.zeros_like(qm), torch.zeros_like(qm)
+    ws = d._workspace(td, qm.device)
+    _check(_lib().sa_backward_p_tsharded(ctypes.byref(td), d._h, _ptr(qm), _ptr(km), _ptr(vm), _ptr(pm), _ptr(dom),
+                                         _ptr(dq), _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()),
+           "sa_backward_p_tsharded")
+    return dq, dk, dv
 
 # ------------------------------------------------------------------ time-sharded LLSA (slab layout)
 

@@ -56,6 +56,19 @@ def _worker(rank, world, port, T, L, R, out):
     res["bitwise_fwd"] = bool(torch.equal(sd.local(om, n), o[:, :, t0:t1]) and
                               torch.equal(sd.local(lsem, n), lse[:, :, t0:t1]))
     res["bitwise_bwd"] = all(bool(torch.equal(sd.local(a, n), b[:, :, t0:t1])) for a, b in zip(gm, (dq, dk, dv)))
+    # the stored-band mode on the same shards (W <= 49): bitwise equal to the unsharded calls too
+    if L + R + 1 <= 49:
+        o_p, lse_p, p_p = s.sa_forward_p(q, k, v, L, R)
+        g_p = s.sa_backward_p(q, k, v, o_p, p_p, do, L, R)
+        dom2 = sd.margined(B, H, n, D)
+        sd.local(dom2, n).copy_(do[:, :, t0:t1])
+        om2, lsem2, pm2 = sd.sa_forward_p_tsharded(qm, km, vm, L, R, t0, T, d)
+        gm2 = sd.sa_backward_p_tsharded(qm, km, vm, pm2, dom2, L, R, t0, T, d)
+        res["bitwise_band"] = bool(torch.equal(sd.local(om2, n), o_p[:, :, t0:t1]) and
+                                   torch.equal(sd.local(pm2, n), p_p[:, :, t0:t1]) and
+                                   all(torch.equal(sd.local(a, n), b[:, :, t0:t1]) for a, b in zip(gm2, g_p)))
+    else:
+        res["bitwise_band"] = True
     # oracle on a slab around each boundary of this shard: rows whose whole dependency cone
     # (forward +-(L+R), backward +-2(L+R)) lies in the slab
     worst = 0.0
@@ -91,7 +104,7 @@ def test_tsharded_c_path_multiprocess(world, T, L, R):
     assert sorted(out.keys()) == list(range(world))
     for r in range(world):
         res = out[r]
-        assert res["bitwise_fwd"] and res["bitwise_bwd"], (r, res)
+        assert res["bitwise_fwd"] and res["bitwise_bwd"] and res["bitwise_band"], (r, res)
         assert res["oracle_excess"] <= 0, (r, res)
 
 
