@@ -894,7 +894,7 @@ def run_encoder(args, dev):
     return out
 
 
-def run_stream(sattn, dev, n_steps=2000, warm=200):
+def run_stream(sattn, dev, n_steps=10000, warm=1000):
     """Incremental LLSA (infer_llsa) and SA (infer_sa) inference: per-frame step latency, 12 layers,
     H=12, D=64, (L,R)=(32,8), bf16, one kernel launch per frame for all layers.
     device = CUDA-event time around one eager step (includes the Python binding's launch overhead, the
@@ -902,11 +902,12 @@ def run_stream(sattn, dev, n_steps=2000, warm=200):
     kernel alone (64 consecutive steps in one CUDA graph, replayed)."""
     import torch
     res = {}
-    for kind, nb in (("llsa", 1), ("llsa", 64), ("sa", 1), ("sa", 64)):
+    for kind, nb, dt in (("llsa", 1, torch.bfloat16), ("llsa", 64, torch.bfloat16), ("sa", 1, torch.bfloat16),
+                         ("sa", 64, torch.bfloat16), ("llsa", 1, torch.float32), ("sa", 1, torch.float32)):
         cls = sattn.LLSAStream if kind == "llsa" else sattn.SAStream
-        st = cls(nb, H, D, L, R, NL, dtype=torch.bfloat16, device=dev)
-        xs = torch.randn(warm + n_steps, nb, H, D, device=dev).to(torch.bfloat16)
-        y = torch.empty(nb, H, D, device=dev, dtype=torch.bfloat16)
+        st = cls(nb, H, D, L, R, NL, dtype=dt, device=dev)
+        xs = torch.randn(warm + n_steps, nb, H, D, device=dev).to(dt)
+        y = torch.empty(nb, H, D, device=dev, dtype=dt)
         for i in range(warm):
             st.step_into(xs[i], y)
         torch.cuda.synchronize()
@@ -944,15 +945,17 @@ def run_stream(sattn, dev, n_steps=2000, warm=200):
             del g
         except Exception as ex:  # report, do not hide: the host-timed numbers above stand
             kern_us = f"unavailable: {type(ex).__name__}: {ex}"[:200]
-        res[f"B{nb}" if kind == "llsa" else f"sa_B{nb}"] = {"device_p50_us": round(float(np.percentile(dev_us, 50)), 2),
+        key = (f"B{nb}" if kind == "llsa" else f"sa_B{nb}") + ("" if dt == torch.bfloat16 else "_f32")
+        res[key] = {"device_p50_us": round(float(np.percentile(dev_us, 50)), 2),
                          "device_p99_us": round(float(np.percentile(dev_us, 99)), 2),
                          "host_p50_us": round(float(np.percentile(host_us, 50)), 2),
                          "host_p99_us": round(float(np.percentile(host_us, 99)), 2),
                          "kernel_us_graph": kern_us,
-                         "streams": nb, "steps": n_steps}
+                         "streams": nb, "steps": n_steps, "dtype": "bf16" if dt == torch.bfloat16 else "f32"}
         del st
-    res["config"] = (f"{NL} layers, H={H}, D={D}, (L,R)=({L},{R}), bf16, one launch per frame; B1/B64 = infer_llsa "
-                     f"(latency R = {R} frames), sa_B1/sa_B64 = infer_sa (latency {NL}R = {NL * R} frames)")
+    res["config"] = (f"{NL} layers, H={H}, D={D}, (L,R)=({L},{R}), bf16 (mma.sync step; *_f32: fp32 CUDA-core step), "
+                     f"one launch per frame, {n_steps} steps after {warm} warm-up; B1/B64 = infer_llsa (latency R = {R} "
+                     f"frames), sa_B1/sa_B64 = infer_sa (latency {NL}R = {NL * R} frames)")
     return res
 
 
