@@ -1179,8 +1179,9 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ------------------------------------------------------------------------------------------
-// backward K2, block-ring variant (SATTN_K2=ring): the key-major kernel above with its query window
-// staged as 128-row blocks.  A CTA sweeps a contiguous range of key tiles, so consecutive
+// backward K2, block-ring variant (the LSE-mode K2 for 49 < W <= 65, whose NQ = 192 window does not
+// fit two stages of the kernel above): the key-major kernel with its query window staged as 128-row
+// blocks.  A CTA sweeps a contiguous range of key tiles, so consecutive
 // tiles' windows [u0 - R, u0 - R + NQ) share a block: each tile loads one new Q block and one
 // dO block (not the NQ-row windows), and a 3-slot block ring holds the current tile's two
 // blocks plus the next one in flight.  K and V get their own 2-slot rings (released after S
