@@ -504,16 +504,32 @@ __global__ void __launch_bounds__(32 * kMmaWarps) stream_mma_kernel(StreamMmaArg
   auto frame_of = [&](int l, int i) -> long long {   // frame of window row i of layer l
     return SA ? h - (long long)(l + 1) * R - L + i : h - R - L + i;
   };
+  // this thread's 16-byte chunks of a layer's ring rows (n_ring * 8 <= 504): window row, chunk, and
+  // the row's frame / ring slot at layer 0 (LLSA: every layer; SA: they move back R per layer)
+  constexpr int kMaxChunks = 4;
+  int ch_off[kMaxChunks], ch_slot[kMaxChunks];
+  long long ch_u[kMaxChunks];
+#pragma unroll
+  for (int j = 0; j < kMaxChunks; ++j) {
+    const int idx = tid + j * 32 * kMmaWarps, r = idx >> 3;
+    ch_off[j] = idx < n_ring * 8 ? r * kMmaRowB + 16 * (idx & 7) : -1;
+    ch_u[j] = frame_of(0, r);
+    ch_slot[j] = NRG > 0 ? slot_of(ch_u[j]) * 64 + 8 * (idx & 7) : 0;   // element offset in the ring
+  }
   // one cp.async group per layer and thread (empty past the last layer: the count stays uniform)
   auto issue_layer = [&](int l) {
     if (l < a.n_layers) {
       const bf16* rg = a.ring + ((long long)l * a.BH + bh) * NRG * 64;
       const uint32_t b = buf_u32(l);
-      for (int idx = tid; idx < n_ring * 8; idx += 32 * kMmaWarps) {
-        const int r = idx >> 3, k = idx & 7;
-        const long long u = frame_of(l, r);
+      const int shift = SA ? (int)(((long long)l * R) % NRG) * 64 : 0;   // SA: frames move back l R
+#pragma unroll
+      for (int j = 0; j < kMaxChunks; ++j) {
+        if (ch_off[j] < 0) continue;
+        const long long u = ch_u[j] - (SA ? (long long)l * R : 0);
         const bool ok = u >= 0 && u <= last;
-        cp_async16(b + r * kMmaRowB + 16 * k, rg + (long long)(ok ? slot_of(u) : 0) * 64 + 8 * k, ok);
+        int e = ch_slot[j] - shift;
+        if (e < 0) e += NRG * 64;
+        cp_async16(b + ch_off[j], rg + (ok ? e : 0), ok);
       }
     }
     cp_async_commit();
