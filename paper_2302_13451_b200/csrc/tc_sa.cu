@@ -268,6 +268,16 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // L2 prefetch of the first tiles' boxes while the previous kernel drains (PDL): safe whether or
+  // not that kernel writes them (L2 is coherent; only the shared-memory loads must wait)
+  if (tid == 0)
+    for (int k = 0; k < ntile_me && k < NQK; ++k) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
+      tc::tma_prefetch_3d(&tmQ, 0, t0, bh);
+      tc::tma_prefetch_3d(&tmK, 0, t0 - a.L, bh);
+      tc::tma_prefetch_3d(&tmV, 0, t0 - a.L, bh);
+    }
   // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
   tc::pdl_wait();
   tc::pdl_launch_dependents();
@@ -552,6 +562,16 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // L2 prefetch of the first tiles' boxes while the previous kernel drains (PDL; see the forward)
+  if (tid == 0 && nch == 1)
+    for (int k = 0; k < ntile_me && k < NS; ++k) {
+      const int g = blockIdx.x + k * gridDim.x;
+      const int bh = g / ntq, t0 = tile_t0(g % ntq, a);
+      tc::tma_prefetch_3d(&tmQ, 0, t0, bh);
+      tc::tma_prefetch_3d(&tmdO, 0, t0, bh);
+      tc::tma_prefetch_3d(&tmK, 0, t0 - a.L - a.kshift, bh);
+      tc::tma_prefetch_3d(&tmV, 0, t0 - a.L - a.kshift, bh);
+    }
   // everything above overlapped the previous kernel's tail (PDL); its outputs are visible after this
   tc::pdl_wait();
   tc::pdl_launch_dependents();
