@@ -504,6 +504,20 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // L2 prefetch of the first items' boxes while the previous kernel drains (PDL; coherent L2)
+  auto prefetch_l2 = [&](int k) {
+    if (k >= nme) return;
+    const int g = blockIdx.x + k * gridDim.x;
+    const int bh = g / nit, h0 = (g % nit) * HZ;
+    tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
+    tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
+    tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+  };
+  if (tid == 0)
+    for (int k = 0; k < 2; ++k) prefetch_l2(k);
   tc::pdl_wait();
   tc::pdl_launch_dependents();
 
@@ -973,6 +987,19 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  // L2 prefetch of the first items' boxes while the previous kernel drains (PDL; coherent L2)
+  auto prefetch_l2 = [&](int k) {
+    if (k >= nme) return;
+    const int g = blockIdx.x + k * gridDim.x;
+    const int bh = g / nit, h0 = (g % nit) * HZ;
+    tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
+    tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
+    tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+  };
+  if (tid == 0)
+    for (int k = 0; k < 2; ++k) prefetch_l2(k);
   tc::pdl_wait();
   tc::pdl_launch_dependents();
 
