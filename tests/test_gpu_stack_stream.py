@@ -252,6 +252,21 @@ def _run_stream(st, tx, T):
 
 @pytest.mark.parametrize("mode", ["llsa", "sa"])
 @pytest.mark.parametrize("L,R", [(3, 1), (32, 16), (0, 4), (16, 0), (47, 16), (5, 7)])
+def test_stream_bands_f32(mode, L, R):
+    # the fp32 CUDA-core step (warp per query row) across band shapes: 3 layers against the oracle's own
+    # recurrence at the per-call fp32 gate x max(1, max|ref|) (G24)
+    s = sattn()
+    B, H, T, D, n = 1, 2, 120, 32, 3
+    x = synth.round_to(synth.normal(12, "X", (B, H, T, D)), "f32")
+    tx = dev(x, torch.float32)
+    cls = s.LLSAStream if mode == "llsa" else s.SAStream
+    ys = _run_stream(cls(B, H, D, L, R, n, dtype=torch.float32), tx, T)
+    Y_or, _ = (oracle.stream.stream_all if mode == "llsa" else oracle.stream.sa_stream_all)(x, L, R, n)
+    assert np.abs(host(ys) - Y_or).max() <= 1e-5 * max(1.0, float(np.abs(Y_or).max()))
+
+
+@pytest.mark.parametrize("mode", ["llsa", "sa"])
+@pytest.mark.parametrize("L,R", [(3, 1), (32, 16), (0, 4), (16, 0), (47, 16), (5, 7)])
 def test_stream_bands_bf16(mode, L, R):
     # the per-frame step across band shapes (the bf16 D=64 step runs on mma.sync for windows of
     # up to 64 rows, 2 query m-tiles for LLSA R >= 16; the CUDA-core step otherwise): 2 layers
