@@ -58,6 +58,9 @@ struct AttnArgs {
   // (see TcArgs in tc_sa.cu)
   int ld;
   int nkt, kt0, kt_split, kt_jump;
+  // packed tiles (tensor-core SA, tc_sa.cu flat_view): T is the flattened BH*T frame axis, BH = 1,
+  // and Th the frames of one head (every row attends inside its own head); 0 = T
+  int Th;
 };
 
 template <int D> struct Smem {

@@ -75,6 +75,9 @@ struct TcArgs {
   // query tiles of this launch per head: kt = kt0 + i + (i >= kt_split ? kt_jump : 0), i < nkt
   // (all tiles: kt0 = 0, nkt = ceil(T/128); a time shard launches interior and edge tiles apart)
   int nkt, kt0, kt_split, kt_jump;
+  int Th;                                        // frames per head: row t attends only inside its head
+                                                 // [t - t % Th, + Th) (= T, or the head length when a
+                                                 // launch packs tiles over the flattened BH*T axis)
   // wide bands (W > 65) as sub-bands of the narrow kernels, accumulated in fp32 (ACC instances):
   // forward (o, m, l) rows merged by log-sum-exp; K1 dQ / K2 dK, dV rows summed; K1 reads the
   // global delta = dO . O from ws_del instead of forming it over its sub-band (G28)
@@ -375,8 +378,9 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(pa + 32 * q4 + 8 * j, s + 8 * j);
       tc::tmem_ld_wait();
       const int key0 = t0 - a.L + 32 * q4;
+      const int hs = t - t % a.Th;              // this row's head: frames [hs, hs + Th)
       float m, l;
-      band_softmax<CW>(s, max(lane, -key0), min(lane + W, T - key0), a.scale_log2, m, l);
+      band_softmax<CW>(s, max(lane, hs - key0), min(lane + W, hs + a.Th - key0), a.scale_log2, m, l);
       tmem_write_row<CW, NK>(pa, q4, s);      // P (bf16) over the consumed S columns
       tc::tmem_st_wait();
       tc::tc_fence_before();
@@ -733,7 +737,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::tmem_ld_wait();
       const int key0 = t0 - a.L - ksh + 32 * q4;
       {
-        const int lo = max(lane, -key0), hi = min(lane + W, T - key0);
+        const int hs = t - t % a.Th;
+        const int lo = max(lane, hs - key0), hi = min(lane + W, hs + a.Th - key0);
 #pragma unroll
         for (int i = 0; i < CW; ++i)
           p[i] = (i >= lo && i < hi) ? tc::ex2(fmaf(p[i], a.scale_log2, -lse2)) : 0.f;
@@ -1111,9 +1116,14 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
+      {   // queries of key u = u0 + r inside its head [hs, hs + Th): column i <-> query u0 - R + c0 + i
+        const int u = u0 + r, q0 = u0 - a.R + c0;
+        const int hs = u - u % a.Th;
+        const int lo = max(lane, hs - q0), hi = min(lane + W, hs + a.Th - q0);
 #pragma unroll
-      for (int i = 0; i < CW; ++i)
-        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+        for (int i = 0; i < CW; ++i)
+          p[i] = (i >= lo && i < hi) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      }
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
       if (tr) trace_at(a.trace, 3, k);
@@ -1992,6 +2002,7 @@ TcArgs tc_args(const AttnArgs& a) {
   t.ws_l2 = a.delta + (long long)a.BH * t.Tp;
   t.ldp = a.ldp;
   t.ld = a.ld > 0 ? a.ld : a.T;
+  t.Th = a.Th > 0 ? a.Th : a.T;
   const int ntq = (a.T + kM - 1) / kM;
   if (a.nkt > 0) {
     t.nkt = a.nkt; t.kt0 = a.kt0; t.kt_split = a.kt_split; t.kt_jump = a.kt_jump;
@@ -1999,6 +2010,25 @@ TcArgs tc_args(const AttnArgs& a) {
     t.nkt = ntq; t.kt0 = 0; t.kt_split = ntq; t.kt_jump = 0;
   }
   return t;
+}
+
+// Packed tiles.  A full launch over contiguous [BH][T] heads runs on the flattened BH*T frame axis
+// as one sequence (BH = 1) whose rows each attend only inside their own head (TcArgs::Th): 128-row
+// tiles then straddle head boundaries, and the launch has ceil(BH*T / 128) tiles instead of
+// BH * ceil(T / 128).  Base shape (BH = 96, T = 1750): 1313 tiles = 8.87 rounds of 148 SMs instead
+// of 1344 = 9.08, i.e. 9 tiles on the busiest CTA instead of 10.  Keys of a neighbouring head in a
+// tile's box are masked like frames outside [0, T) were (the stored band holds zeros for them).
+// Not for time-shard launches (a row stride or a tile subset) or when packing saves no tile.
+AttnArgs flat_view(const AttnArgs& a) {
+  const long long tot = (long long)a.BH * a.T;
+  if (a.BH <= 1 || a.nkt > 0 || (a.ld > 0 && a.ld != a.T) || a.Th > 0 || tot > (1LL << 30)) return a;
+  if ((tot + kM - 1) / kM >= (long long)a.BH * ((a.T + kM - 1) / kM)) return a;
+  AttnArgs f = a;
+  f.T = (int)tot;
+  f.BH = 1;
+  f.ld = 0;
+  f.Th = a.T;
+  return f;
 }
 
 int num_sms() {
@@ -2425,7 +2455,8 @@ bool tc_supported(int dtype, int D, int L, int R, bool llsa, bool backward) {
   return W + 31 <= 96;
 }
 
-sattn_status tc_forward(const AttnArgs& a, cudaStream_t st) {
+sattn_status tc_forward(const AttnArgs& a0, cudaStream_t st) {
+  const AttnArgs a = flat_view(a0);
   switch (cw_of(a.L + a.R + 1)) {
     case 32: return fwd_launch<32>(a, st);
     case 48: return fwd_launch<48>(a, st);
@@ -2440,8 +2471,12 @@ sattn_status tc_forward(const AttnArgs& a, cudaStream_t st) {
 
 sattn_status tc_backward(const AttnArgs& a, cudaStream_t st) { return tc_backward_phase(a, st, 3); }
 
-sattn_status tc_backward_phase(const AttnArgs& a, cudaStream_t st, int phase) {
-  switch (cw_of(a.L + a.R + 1)) {
+sattn_status tc_backward_phase(const AttnArgs& a0, cudaStream_t st, int phase) {
+  // packed tiles only when one call runs both kernels (K1's delta rows are K2's input layout) and
+  // the band takes the two-stage K2 (the block-ring K2 for CW = 96 keeps the per-head tiling)
+  const int cw = cw_of(a0.L + a0.R + 1);
+  const AttnArgs a = phase == 3 && cw > 0 && cw <= 80 ? flat_view(a0) : a0;
+  switch (cw) {
     case 32: return bwd_launch<32>(a, st, phase);
     case 48: return bwd_launch<48>(a, st, phase);
     case 64: return bwd_launch<64>(a, st, phase);
@@ -2465,7 +2500,8 @@ bool tc_p_supported(int dtype, int D, int L, int R, bool backward) {
   return backward ? cw_of(W) > 0 && cw_of(W) <= 80 : W <= 64;
 }
 
-sattn_status tc_forward_p(const AttnArgs& a, cudaStream_t st) {
+sattn_status tc_forward_p(const AttnArgs& a0, cudaStream_t st) {
+  const AttnArgs a = flat_view(a0);
   switch (cw_of(a.L + a.R + 1)) {
     case 32: return fwd_launch<32, true>(a, st);
     case 48: return fwd_launch<48, true>(a, st);
@@ -2510,7 +2546,8 @@ sattn_status bwd_p_launch(const AttnArgs& a, cudaStream_t st, int phase = 3) {
   return SATTN_OK;
 }
 
-sattn_status tc_backward_p_phase(const AttnArgs& a, cudaStream_t st, int phase) {
+sattn_status tc_backward_p_phase(const AttnArgs& a0, cudaStream_t st, int phase) {
+  const AttnArgs a = phase == 3 ? flat_view(a0) : a0;   // packed tiles: as tc_backward_phase
   switch (cw_of(a.L + a.R + 1)) {
     case 32: return bwd_p_launch<32>(a, st, phase);
     case 48: return bwd_p_launch<48>(a, st, phase);

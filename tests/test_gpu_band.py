@@ -20,6 +20,9 @@ CASES = [
     ((1, 3, 777, 64), 16, 8, "bf16"), ((2, 1, 1000, 64), 40, 23, "bf16"), ((1, 1, 5, 64), 2, 2, "bf16"),
     # wide bands: the backward as 48-column sub-bands of a_t on tensor cores (W = 57, 351, 490)
     ((1, 2, 300, 64), 32, 24, "bf16"), ((1, 2, 600, 64), 200, 150, "bf16"), ((1, 1, 1000, 64), 245, 244, "bf16"),
+    # packed tiles over the flattened B*H*T axis (heads shorter than a tile; windows cut by head
+    # boundaries inside a tile)
+    ((2, 3, 50, 64), 32, 8, "bf16"), ((4, 4, 20, 64), 32, 8, "bf16"), ((3, 5, 100, 64), 8, 8, "bf16"),
 ]
 
 

@@ -69,7 +69,10 @@ def test_sa_fp32(shape, L, R, impl):
 SA_BF16 = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 32, 8), ((2, 2, 1750, 64), 32, 16),
            ((1, 2, 600, 64), 32, 32), ((1, 2, 300, 64), 200, 150), ((1, 3, 777, 64), 32, 8), ((1, 1, 50, 16), 5, 2),
            # wide bands on tensor cores (sub-bands merged by log-sum-exp): Fig. 5's top end W = 490, asymmetric
-           ((1, 2, 1000, 64), 245, 244), ((2, 3, 600, 64), 100, 30), ((1, 2, 257, 64), 0, 90)]
+           ((1, 2, 1000, 64), 245, 244), ((2, 3, 600, 64), 100, 30), ((1, 2, 257, 64), 0, 90),
+           # packed tiles over the flattened B*H*T axis: heads shorter than a tile, windows cut by
+           # head boundaries inside one 128-row tile (2-7 heads per tile)
+           ((2, 3, 50, 64), 32, 8), ((4, 4, 20, 64), 32, 8), ((3, 5, 100, 64), 3, 1), ((2, 2, 300, 64), 40, 24)]
 
 
 @pytest.mark.parametrize("shape,L,R", SA_BF16)
