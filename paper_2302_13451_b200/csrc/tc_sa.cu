@@ -903,6 +903,8 @@ __global__ void __launch_bounds__(320, 1)
   const int ntq = (T + kM - 1) / kM;
   const int ntiles = ntq * a.BH;
   const int ntile_me = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // K2 walks the tiles in the reverse of K1's order: its first rounds re-read the V / dO / band
+  // (or LSE-mode K / V / Q / dO) rows K1 streamed in its last rounds, still resident in L2
 
   if (tid == 0) {
     tc::tma_prefetch_desc(&tmQ); tc::tma_prefetch_desc(&tmK); tc::tma_prefetch_desc(&tmV);
@@ -937,7 +939,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       int nd = 0;   // PST: next tile whose delta rows are to be loaded
       for (int k = 0; k < ntile_me; ++k) {
-        const int g = blockIdx.x + k * gridDim.x;
+        const int g = ntiles - 1 - (blockIdx.x + k * gridDim.x);   // reversed order (below)
         const int bh = g / ntq, u0 = (g % ntq) * kM;
         const int st = k % NS;
         uint8_t* b0 = stage0 + st * STG;
@@ -970,7 +972,7 @@ __global__ void __launch_bounds__(320, 1)
         if (k + 1 >= NS || k + 1 == ntile_me) {
           if (nd == 0) tc::pdl_wait();   // K1 complete: its rows are visible
           for (; nd <= k; ++nd) {
-            const int gd = blockIdx.x + nd * gridDim.x;
+            const int gd = ntiles - 1 - (blockIdx.x + nd * gridDim.x);   // reversed order (below)
             const int sd = nd % NS, nad = ((gd % ntq) * kM - a.R) & ~3;
             uint8_t* bd = stage0 + sd * STG;
             tc::mbar_expect_tx(&dfull[sd], (PST ? 1 : 2) * C::NQP * 4);
@@ -1050,7 +1052,7 @@ __global__ void __launch_bounds__(320, 1)
     const bool leader = q4 == 2 && lane == 0;
     uint8_t* ostage = obuf0 + wg * 2 * C::KB;  // [dV | dK] (not PST)
     for (int k = wg; k < ntile_me; k += 2) {
-      const int g = blockIdx.x + k * gridDim.x;
+      const int g = ntiles - 1 - (blockIdx.x + k * gridDim.x);   // reversed order (below)
       const int bh = g / ntq, u0 = (g % ntq) * kM;
       const int b = wg, use = k >> 1, st = k % NS;
       const int sh = (u0 - a.R) - ((u0 - a.R) & ~3);   // column 0 sits `sh` floats into the aligned box
