@@ -1083,7 +1083,7 @@ __global__ void __launch_bounds__(320, 1)
         if (tr) trace_at(a.trace, 4, k);
         __syncwarp();
         tc::tc_fence_after();
-        float ds[CW];
+        float ds[CW];   // (per-chunk waits: one batched wait measured 41.1 -> 41.3 us, more spills)
 #pragma unroll
         for (int j = 0; j < CW / 8; ++j) {
           float dp[8];
@@ -1133,15 +1133,12 @@ __global__ void __launch_bounds__(320, 1)
       if (tr) trace_at(a.trace, 4, k);
       __syncwarp();
       tc::tc_fence_after();
-      float ds[CW];
+      float ds[CW];   // dP^T strip, all loads in flight before one wait, then dS^T in place
 #pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, ds + 8 * j);
+      tc::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
-      }
+      for (int i = 0; i < CW; ++i) ds[i] = p[i] * (ds[i] - sDel[c0 + i]);
       tc::mbar_arrive(&empty[st]);   // this warpgroup's reads of the LSE / delta rows are done
       tmem_write_row<CW, NQ>(x, q4, p);                 // P^T  -> packed columns [0, NQ/2)
       tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);      // dS^T -> packed columns [NQ/2, NQ)
@@ -1588,15 +1585,12 @@ __global__ void __launch_bounds__(320, 1)
       if (tr) trace_at(a.trace, 4, k);
       __syncwarp();
       tc::tc_fence_after();
-      float ds[CW];
+      float ds[CW];   // dP^T strip, all loads in flight before one wait, then dS^T in place
 #pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, ds + 8 * j);
+      tc::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
-      }
+      for (int i = 0; i < CW; ++i) ds[i] = p[i] * (ds[i] - sDel[c0 + i]);
       tc::mbar_arrive(&rempty[s]);                     // LSE / delta window consumed
       tmem_write_row<CW, NQ>(x, q4, p);
       tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);
@@ -1856,15 +1850,12 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_wait(&dpfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
-      float ds[CW];
+      float ds[CW];   // dP^T strip, all loads in flight before one wait, then dS^T in place
 #pragma unroll
-      for (int j = 0; j < CW / 8; ++j) {
-        float dp[8];
-        tc::tmem_ld8(x + c0 + 8 * j, dp);
-        tc::tmem_ld_wait();
+      for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, ds + 8 * j);
+      tc::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) ds[8 * j + e] = p[8 * j + e] * (dp[e] - sDel[c0 + 8 * j + e]);
-      }
+      for (int i = 0; i < CW; ++i) ds[i] = p[i] * (ds[i] - sDel[c0 + i]);
       tmem_write_row<CW, NQ>(x, q4, p);
       tmem_write_row<CW, NQ>(x + NQ / 2, q4, ds);
       tc::tmem_st_wait();
