@@ -44,5 +44,6 @@ sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st);
 int tc_llsa_backward_launches(const AttnArgs& a);
 bool tc_llsa_bwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
 bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
-sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, cudaStream_t st);
+// ws_flat: delta / LSE rows as [C][BH*T rounded to 4] (the packed-tile kv pass) instead of [C][BH][Tp]
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st);
 }  // namespace sattn

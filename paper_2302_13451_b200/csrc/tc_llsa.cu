@@ -399,7 +399,8 @@ struct LlsaBwdArgs {
   float scale, scale_log2;
   const float* LSE;              // [C][BH][T]
   bf16 *dQ, *dK, *dV;            // [C][BH][T][64]
-  float *ws_del, *ws_l2;         // [C][BH][Tp]
+  float *ws_del, *ws_l2;         // [C][BH][Tp], or [C][Tp] over the flattened BH*T axis (ws_flat)
+  int ws_flat;                   // rows for the packed-tile kv pass: index c Tp + bh T + t, Tp = BH*T rounded to 4
   long long* trace;              // debug: per-item phase clock64 stamps of CTA 0 ([16][64]), or null
 };
 
@@ -850,10 +851,13 @@ __global__ void __launch_bounds__(320, 1)
 
       // workspace rows for the key-major band pass (padded rows [T, Tp) zero)
       if (row_ok) {
-        a.ws_del[crow * a.Tp + t] = delta;
-        a.ws_l2[crow * a.Tp + t] = lse2;
-        if (t == T - 1)
-          for (int tt = T; tt < a.Tp; ++tt) { a.ws_del[crow * a.Tp + tt] = 0.f; a.ws_l2[crow * a.Tp + tt] = 0.f; }
+        // per-head rows, or one row per channel over the flattened BH*T axis (padding after the last head)
+        const long long w0 = a.ws_flat ? (long long)c * a.Tp + (long long)bh * T : crow * a.Tp;
+        const int wend = a.ws_flat ? a.Tp - (a.BH - 1) * T : a.Tp;   // padded end, relative to w0
+        a.ws_del[w0 + t] = delta;
+        a.ws_l2[w0 + t] = lse2;
+        if (t == T - 1 && (!a.ws_flat || bh == a.BH - 1))
+          for (int tt = T; tt < wend; ++tt) { a.ws_del[w0 + tt] = 0.f; a.ws_l2[w0 + tt] = 0.f; }
       }
       LTR(7);
       // ---- epilogue: dQ row (t, c); staircase key rows m = r: (u, c'), u = h0 + i' - c'
@@ -1327,7 +1331,7 @@ int fused_hz(int L, int R) {
 }
 
 template <int NB, int RM>
-sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, cudaStream_t st) {
+sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st) {
   using Cf = LBCfg<NB, RM>;
   const int R = a.R, C = R + 1;
   CUtensorMap mq, mdo, mkb, mvb, mks, mvs, mdq, mdk, mdv;
@@ -1345,6 +1349,10 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   la.LSE = a.LSE;
   la.dQ = reinterpret_cast<bf16*>(a.dQ); la.dK = reinterpret_cast<bf16*>(a.dK); la.dV = reinterpret_cast<bf16*>(a.dV);
   la.ws_del = ws_del; la.ws_l2 = ws_l2;
+  if (ws_flat) {   // the kv pass runs packed tiles over the flattened BH*T axis (tc_sa.cu)
+    la.ws_flat = 1;
+    la.Tp = (int)((((long long)a.BH * a.T) + 3) & ~3LL);
+  }
   la.trace = g_llsa_trace;
   const int items = (a.T + R + HZ - 1) / HZ * a.BH;
   const int grid = items < num_sms() ? items : num_sms();
@@ -1457,15 +1465,15 @@ bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, l
   return hz >= 4 && BH * T - 1 >= T + R;
 }
 
-sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, cudaStream_t st) {
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st) {
   const int HZ = fused_hz(a.L, a.R);
   const int nb = (HZ + a.L + 15) / 16 * 16;
   const bool r16 = a.R > 8;
   switch (nb) {
     case 16:
-    case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, st);
-    case 48: return r16 ? bwd_fused_launch<48, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<48, 8>(a, HZ, ws_del, ws_l2, st);
-    case 64: return r16 ? bwd_fused_launch<64, 16>(a, HZ, ws_del, ws_l2, st) : bwd_fused_launch<64, 8>(a, HZ, ws_del, ws_l2, st);
+    case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
+    case 48: return r16 ? bwd_fused_launch<48, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<48, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
+    case 64: return r16 ? bwd_fused_launch<64, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<64, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
   }
   g_err = "band too wide for the fused LLSA backward";
   return SATTN_EUNSUPPORTED;

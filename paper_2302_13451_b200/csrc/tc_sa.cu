@@ -1842,9 +1842,14 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int j = 0; j < CW / 8; ++j) tc::tmem_ld8(x + c0 + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
+      {   // queries of key u = u0 + r inside its head [hs, hs + Th): column i <-> query n0 + c0 + i
+        const int u = u0 + r, qc = n0 + c0;
+        const int hs = u - u % a.Th;
+        const int lo = max(lane, hs - qc), hi = min(lane + W, hs + a.Th - qc);
 #pragma unroll
-      for (int i = 0; i < CW; ++i)
-        p[i] = (i >= lane && i < lane + W) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+        for (int i = 0; i < CW; ++i)
+          p[i] = (i >= lo && i < hi) ? tc::ex2(fmaf(p[i], a.scale_log2, -sL2[c0 + i])) : 0.f;
+      }
       tc::tc_fence_before();
       tc::mbar_arrive(&xfree[b]);
       tc::mbar_wait(&dpfull[b], use & 1);
@@ -2184,12 +2189,20 @@ void wide_split(int W, int j, int S, int& o, int& w) {
 // LLSA key-major band pass: dK, dV of channel R's keys accumulated over the C query channels
 // (delta and LSE log2e rows from the workspace)
 template <int CW>
-sattn_status llsa_bwd_kv_launch(const AttnArgs& a, const bf16* Q, const bf16* dO, const bf16* Kr, const bf16* Vr,
-                                bf16* dK, bf16* dV, float* ws_del, float* ws_l2, cudaStream_t st) {
+sattn_status llsa_bwd_kv_launch(const AttnArgs& a0, const bf16* Q, const bf16* dO, const bf16* Kr, const bf16* Vr,
+                                bf16* dK, bf16* dV, float* ws_del, float* ws_l2, bool flat, cudaStream_t st) {
   using LC = LkvCfg<CW>;
-  const int R = a.R, C = R + 1;
-  const bool bc = a.in_cs == 0;
-  const long long plane = (long long)a.BH * a.T * kD;
+  const int R = a0.R, C = R + 1;
+  const bool bc = a0.in_cs == 0;
+  const long long plane = (long long)a0.BH * a0.T * kD;
+  // packed tiles (flat: the delta / LSE rows are [C][BH*T rounded to 4], written so by the fused
+  // pass): key tiles over the flattened BH*T axis, every query masked to its key's head (Th)
+  AttnArgs a = a0;
+  if (flat) {
+    a.T = a0.BH * a0.T;
+    a.BH = 1;
+    a.Th = a0.T;
+  }
   const int Tp = (a.T + 3) & ~3;
   const int ntiles = (a.T + kM - 1) / kM * a.BH;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
@@ -2234,12 +2247,16 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   if (tc_llsa_bwd_fused_supported(SATTN_BF16, kD, a.L, R, a.BH, a.T, !bc)) {
     // fused horizon-major pass (tc_llsa.cu): dQ, staircase dK / dV, delta / LSE rows; then the
     // key-major band pass below for channel R's dK / dV
-    sattn_status r = tc_llsa_bwd_fused(a, ws_del, ws_l2, st);
+    // packed kv tiles when they save a round's worth of tiles (base shape: 1313 instead of 1344)
+    const long long tot = (long long)a.BH * a.T;
+    const bool flat = a.BH > 1 && tot <= (1LL << 30) &&
+                      (tot + kM - 1) / kM < (long long)a.BH * ((a.T + kM - 1) / kM);
+    sattn_status r = tc_llsa_bwd_fused(a, ws_del, ws_l2, flat ? 1 : 0, st);
     if (r != SATTN_OK) {
       g_tc_err = tc_llsa_last_error();
       return r;
     }
-    return llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, st);
+    return llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, flat, st);
   }
   StairArgs sa{};
   sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
@@ -2281,7 +2298,7 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
   }
   // (2) key-major band pass: dK, dV of channel R accumulated over the C query channels
   {
-    const sattn_status r = llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, st);
+    const sattn_status r = llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, false, st);
     if (r != SATTN_OK) return r;
   }
   // (3) staircase keys and the staircase part of dQ (mma.sync)

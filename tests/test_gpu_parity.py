@@ -120,6 +120,8 @@ LLSA_CASES = [
     # item-form forward / fused backward (dense inputs, 1 <= R <= 16): small R, L = 0, R = 16 with L = 48
     ("bf16", (2, 2, 300, 64), 32, 1), ("bf16", (1, 3, 257, 64), 8, 2), ("bf16", (2, 1, 150, 64), 0, 3),
     ("bf16", (1, 2, 400, 64), 48, 16), ("bf16", (2, 2, 513, 64), 20, 12),
+    # packed kv tiles over the flattened B*H*T axis: heads shorter than a key tile
+    ("bf16", (2, 3, 60, 64), 32, 8), ("bf16", (3, 2, 20, 64), 16, 4),
 ]
 
 
