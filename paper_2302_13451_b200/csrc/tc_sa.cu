@@ -1732,7 +1732,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       int k = 0;
       for (int kt = 0; kt < ntile_me; ++kt) {
-        const int g = blockIdx.x + kt * gridDim.x;
+        const int g = ntiles - 1 - (blockIdx.x + kt * gridDim.x);   // reverse of the fused pass order (L2)
         const int bh = g / ntq, u0 = (g % ntq) * kM;
         const int ks = kt & 1;
         if (kt >= 2) tc::mbar_wait(&kvempty[ks], ((kt - 2) >> 1) & 1);
@@ -1825,7 +1825,7 @@ __global__ void __launch_bounds__(320, 1)
     const int W = L + 1;
     for (int k = wg; k < nsub; k += 2) {
       const int kt = k / C, c = k % C;
-      const int g = blockIdx.x + kt * gridDim.x;
+      const int g = ntiles - 1 - (blockIdx.x + kt * gridDim.x);
       const int bh = g / ntq, u0 = (g % ntq) * kM;
       const int b = k & 1, use = k >> 1, qs = k % NQS;
       const int n0 = u0 + (R - c);
