@@ -4,10 +4,11 @@
    multi-process group: 2 and 3 processes share the one leased GPU (NCCL refuses two ranks on one
    device, so the halo moves through the library's callback transport, host-staged over gloo;
    pack / unpack kernels, the interior / edge tile split and the kernels are the production
-   path).  Every rank's local rows must be BITWISE equal to the unsharded call (shards 128-frame
-   aligned) and match the fp64 oracle on slabs straddling each shard boundary.
+   path).  Every rank's local rows must be BITWISE equal to the unsharded call on per-head tiles
+   (one head per call; shards 128-frame aligned) and match the fp64 oracle on slabs straddling each shard boundary.
 2. NCCL transport initialisation (world 1: a communicator of one rank, no neighbours).
-3. Virtual ranks on one device: the CUDA path on hand-cut halo slabs == unsharded (bitwise).
+3. Virtual ranks on one device: the CUDA path on hand-cut halo slabs == unsharded (bitwise, one
+   head per call on both sides: see _per_head).
 """
 import os
 import socket
@@ -27,6 +28,17 @@ def _free_port():
     return p
 
 
+def _per_head(fn, *xs):
+    """fn on each (batch, head) plane separately, outputs concatenated back to [B][H]: every call
+    has one head, so the SA kernels tile each head from frame 0 in 128-frame tiles, as a time shard
+    does; a multi-head call packs its tiles over the flattened B*H*T axis and rounds in another
+    order (equal to the gate, not bitwise)"""
+    B, H = xs[0].shape[:2]
+    outs = [[fn(*(x[b:b + 1, h:h + 1].clone() for x in xs)) for h in range(H)] for b in range(B)]
+    return tuple(torch.cat([torch.cat([o_[i] for o_ in row], dim=1) for row in outs], dim=0)
+                 for i in range(len(outs[0][0])))
+
+
 def _worker(rank, world, port, T, L, R, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -41,8 +53,11 @@ def _worker(rank, world, port, T, L, R, out):
     B, H, D = 1, 3, 64
     g = torch.Generator(device="cuda").manual_seed(21)
     q, k, v, do = (torch.randn(B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
-    o, lse = s.sa_forward(q, k, v, L, R)
-    dq, dk, dv = s.sa_backward(q, k, v, o, lse, do, L, R)
+    # unsharded reference one head per call (_per_head)
+    per_head = _per_head
+    o, lse = per_head(lambda q_, k_, v_: s.sa_forward(q_, k_, v_, L, R), q, k, v)
+    dq, dk, dv = per_head(lambda q_, k_, v_, o_, l_, d_: s.sa_backward(q_, k_, v_, o_, l_, d_, L, R),
+                          q, k, v, o, lse, do)
     t0, t1 = tshard.shard_bounds(T, world, rank, 128)
     n = t1 - t0
     d = sd.Dist()
@@ -58,8 +73,9 @@ def _worker(rank, world, port, T, L, R, out):
     res["bitwise_bwd"] = all(bool(torch.equal(sd.local(a, n), b[:, :, t0:t1])) for a, b in zip(gm, (dq, dk, dv)))
     # the stored-band mode on the same shards (W <= 49): bitwise equal to the unsharded calls too
     if L + R + 1 <= 49:
-        o_p, lse_p, p_p = s.sa_forward_p(q, k, v, L, R)
-        g_p = s.sa_backward_p(q, k, v, o_p, p_p, do, L, R)
+        o_p, lse_p, p_p = per_head(lambda q_, k_, v_: s.sa_forward_p(q_, k_, v_, L, R), q, k, v)
+        g_p = per_head(lambda q_, k_, v_, o_, p_, d_: s.sa_backward_p(q_, k_, v_, o_, p_, d_, L, R),
+                       q, k, v, o_p, p_p, do)
         dom2 = sd.margined(B, H, n, D)
         sd.local(dom2, n).copy_(do[:, :, t0:t1])
         om2, lsem2, pm2 = sd.sa_forward_p_tsharded(qm, km, vm, L, R, t0, T, d)
@@ -209,8 +225,9 @@ def test_tsharded_nccl_world1_equals_unsharded():
     B, H, T, D, L, R = 2, 3, 777, 64, 32, 8
     g = torch.Generator(device="cuda").manual_seed(5)
     q, k, v, do = (torch.randn(B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
-    o, lse = s.sa_forward(q, k, v, L, R)
-    dq, dk, dv = s.sa_backward(q, k, v, o, lse, do, L, R)
+    o, lse = _per_head(lambda q_, k_, v_: s.sa_forward(q_, k_, v_, L, R), q, k, v)
+    dq, dk, dv = _per_head(lambda q_, k_, v_, o_, l_, d_: s.sa_backward(q_, k_, v_, o_, l_, d_, L, R),
+                           q, k, v, o, lse, do)
     d = sd.Dist(transport="nccl")
     qm, km, vm, dom = (sd.margined(B, H, T, D) for _ in range(4))
     for m, x in ((qm, q), (km, k), (vm, v), (dom, do)):
@@ -235,21 +252,23 @@ def test_virtual_rank_slabs_bitwise_equal_unsharded(world, L, R):
     B, H, T, D = 1, 3, 3000, 64
     g = torch.Generator(device="cuda").manual_seed(11)
     q, k, v, do = (torch.randn(B, H, T, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(4))
-    o, lse = s.sa_forward(q, k, v, L, R)
-    dq, dk, dv = s.sa_backward(q, k, v, o, lse, do, L, R)
+    fwd = lambda q_, k_, v_: s.sa_forward(q_, k_, v_, L, R)  # noqa: E731
+    bwd = lambda q_, k_, v_, o_, l_, d_: s.sa_backward(q_, k_, v_, o_, l_, d_, L, R)  # noqa: E731
+    o, lse = _per_head(fwd, q, k, v)
+    dq, dk, dv = _per_head(bwd, q, k, v, o, lse, do)
     for r in range(world):
         t0, t1 = tshard.shard_bounds(T, world, r, 128)
         hl, hr = _round_up(L, 128), _round_up(R, 128)
         a0, a1 = max(0, t0 - hl), min(T, t1 + hr)
         sl = lambda x: x[:, :, a0:a1].contiguous()  # noqa: E731
-        o_r, lse_r = s.sa_forward(sl(q), sl(k), sl(v), L, R)
+        o_r, lse_r = _per_head(fwd, sl(q), sl(k), sl(v))
         n = t1 - t0
         assert torch.equal(o_r[:, :, t0 - a0:t0 - a0 + n], o[:, :, t0:t1])
         assert torch.equal(lse_r[:, :, t0 - a0:t0 - a0 + n], lse[:, :, t0:t1])
         h = _round_up(L + R, 128)
         b0, b1 = max(0, t0 - h), min(T, t1 + h)
         sb = lambda x: x[:, :, b0:b1].contiguous()  # noqa: E731
-        gq, gk, gv = s.sa_backward(sb(q), sb(k), sb(v), sb(o), sb(lse), sb(do), L, R)
+        gq, gk, gv = _per_head(bwd, sb(q), sb(k), sb(v), sb(o), sb(lse), sb(do))
         for got, ref in ((gq, dq), (gk, dk), (gv, dv)):
             assert torch.equal(got[:, :, t0 - b0:t0 - b0 + n], ref[:, :, t0:t1])
 
