@@ -23,6 +23,7 @@ CASES = [
     # packed tiles over the flattened B*H*T axis (heads shorter than a tile; windows cut by head
     # boundaries inside a tile)
     ((2, 3, 50, 64), 32, 8, "bf16"), ((4, 4, 20, 64), 32, 8, "bf16"), ((3, 5, 100, 64), 8, 8, "bf16"),
+    ((5, 40, 1, 64), 32, 8, "bf16"), ((3, 7, 127, 64), 32, 8, "bf16"),
 ]
 
 

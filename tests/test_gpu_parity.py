@@ -72,7 +72,8 @@ SA_BF16 = [((1, 2, 129, 64), 0, 0), ((1, 2, 129, 64), 3, 1), ((2, 2, 1750, 64), 
            ((1, 2, 1000, 64), 245, 244), ((2, 3, 600, 64), 100, 30), ((1, 2, 257, 64), 0, 90),
            # packed tiles over the flattened B*H*T axis: heads shorter than a tile, windows cut by
            # head boundaries inside one 128-row tile (2-7 heads per tile)
-           ((2, 3, 50, 64), 32, 8), ((4, 4, 20, 64), 32, 8), ((3, 5, 100, 64), 3, 1), ((2, 2, 300, 64), 40, 24)]
+           ((2, 3, 50, 64), 32, 8), ((4, 4, 20, 64), 32, 8), ((3, 5, 100, 64), 3, 1), ((2, 2, 300, 64), 40, 24),
+           ((5, 40, 1, 64), 32, 8), ((3, 7, 127, 64), 32, 8)]
 
 
 @pytest.mark.parametrize("shape,L,R", SA_BF16)
