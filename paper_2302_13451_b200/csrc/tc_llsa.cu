@@ -475,7 +475,9 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* done = dsfull + 2;     // [2]
   uint64_t* tfree = done + 2;      // [2] (128)
   uint64_t* xsfree = tfree + 2;    // [1] DS / PS read by the item's MMAs
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(xsfree + 1);
+  uint64_t* emptyA = xsfree + 1;   // [2] the stage's dO / Kb / Vb read by the item's MMAs (not used
+                                   //     as epilogue staging: reloaded before the stores finish)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(emptyA + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, L = a.L, R = a.R, C = a.C, HZ = a.HZ;
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_init(&dsfull[i], 128); tc::mbar_init(&done[i], 1); tc::mbar_init(&tfree[i], 128);
     }
     tc::mbar_init(xsfree, 1);
+    tc::mbar_init(&emptyA[0], 1); tc::mbar_init(&emptyA[1], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, 512);
@@ -542,13 +545,16 @@ __global__ void __launch_bounds__(320, 1)
         const int bh = g / nit, h0 = (g % nit) * HZ;
         const int s = k & 1;
         prefetch(k + 2);
-        if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
+        // dO / Kb / Vb as soon as the previous item on this stage has finished its MMAs; Q / Ks / Vs
+        // (the epilogue's staging tiles) once its TMA stores have read them
+        if (k >= 2) tc::mbar_wait(&emptyA[s], ((k - 2) >> 1) & 1);
         uint8_t* sb = stage0 + s * Cf::STAGE;
         tc::mbar_expect_tx(&full[s], 2 * qbytes + 2 * Cf::KBB + 2 * sbytes);
-        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);                         // rows (h0+i-c, c)
         tc::tma_load_4d(sb + Cf::QB, &tmdO, &full[s], 0, h0, 0, bh);
         tc::tma_load_4d(sb + 2 * Cf::QB, &tmKb, &full[s], 0, h0 - R - L, bh, R);   // band keys (u, R)
         tc::tma_load_4d(sb + 2 * Cf::QB + Cf::KBB, &tmVb, &full[s], 0, h0 - R - L, bh, R);
+        if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
+        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);                         // rows (h0+i-c, c)
         tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, h0, 0, bh);   // (h0+i-c', c')
         tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, h0, 0, bh);
       }
@@ -586,7 +592,8 @@ __global__ void __launch_bounds__(320, 1)
                          tc::desc_mnmajor_sw128(dO + 2048 * j), idK, j > 0);
           }
           tc::mma_commit(&done[b]);
-          tc::mma_commit(xsfree);   // the stage itself is released by the epilogue's TMA stores
+          tc::mma_commit(xsfree);
+          tc::mma_commit(&emptyA[b]);   // dO / Kb / Vb; Q / Ks / Vs are released by the epilogue's stores
           ++ng;
           continue;
         }
