@@ -210,7 +210,9 @@ void sa_stream_destroy(sattn_stream* s);
  * (zero-initialise the buffers once).  The backward must get the same Q, K, V buffers (with
  * the margins the forward filled) and the forward's LSE.  Outputs: local rows of O / LSE /
  * dQ / dK / dV (margin rows of the outputs are scratch).  With t0 a multiple of 128 the local
- * rows are bitwise equal to the unsharded call's.  Tensor-core path only: bf16, D = 64,
+ * rows are bitwise equal to the unsharded call's on one (b, h) plane per call (a call over
+ * several planes packs its 128-row tiles over the flattened B*H*T axis, summing in another
+ * order: equal to the parity gate, not bitwise).  Tensor-core path only: bf16, D = 64,
  * L + R + 1 <= 65, L + R <= M; every shard T >= L + R when it has neighbours.
  * The exchange overlaps the tiles whose operands are all local; no host synchronisation.
  * Transport: NCCL (sattn_dist_init: one communicator per process, send/recv to rank +- 1
