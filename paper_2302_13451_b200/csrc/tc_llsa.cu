@@ -1048,11 +1048,14 @@ __global__ void __launch_bounds__(320, 1)
       const int nks = (R * HZ + 15) / 16;
       int ns = 0, no = 0;
       while (no < nme) {
+        // O(no) overwrites the O columns of item no - 2: it waits for that item's epilogue (tfree);
+        // S(ns) only needs its stage and PV(ns - 2) issued ahead of it (in-order execution), so it
+        // runs while the warpgroup is still in the epilogue of item ns - 2
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1,
                                           tc::smem_u32(&full[ns % NSTG]), (ns / NSTG) & 1,
-                                          tc::smem_u32(&tfree[ns & 1]), ((ns + 2) >> 1) & 1,
+                                          tc::smem_u32(&tfree[no & 1]), ((no + 2) >> 1) & 1,
                                           tc::smem_u32(&pfull[no & 1]), (no >> 1) & 1);
-        if (no < ns && (m & 1)) {   // O of item no
+        if (no < ns && (m & 1) && (no < 2 || (m & 4))) {   // O of item no
           tc::tc_fence_after();
           const int b = no & 1;
           const uint32_t sb = tc::smem_u32(stage0 + (no % NSTG) * Cf::STAGE);
@@ -1069,7 +1072,7 @@ __global__ void __launch_bounds__(320, 1)
           ++no;
           continue;
         }
-        if (ns < nme && ns < no + 2 && (m & 2) && (ns < 2 || (m & 4))) {   // S_band of item ns
+        if (ns < nme && ns < no + 2 && (m & 2)) {   // S_band of item ns
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t sb = tc::smem_u32(stage0 + (ns % NSTG) * Cf::STAGE);
