@@ -567,11 +567,13 @@ __global__ void __launch_bounds__(320, 1)
       const int nks = (R * HZ + 15) / 16;                    // 16-key steps over the stair keys
       int ns = 0, ndp = 0, ng = 0;
       while (ng < nme) {
+        // dQ / dK / dV (ng) overwrite the accumulators of item ng - 2: they wait for its epilogue
+        // (tfree); S / dP (ns) only use columns [0, NB) and run during that epilogue
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&dsfull[ng & 1]), (ng >> 1) & 1,
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
                                           tc::smem_u32(&full[ns & 1]), (ns >> 1) & 1,
-                                          tc::smem_u32(&tfree[ns & 1]), ((ns + 2) >> 1) & 1);
-        if (ng < ndp && (m & 1)) {   // dQ, dK_stair, dV_stair of item ng
+                                          tc::smem_u32(&tfree[ng & 1]), ((ng + 2) >> 1) & 1);
+        if (ng < ndp && (m & 1) && (ng < 2 || (m & 8))) {   // dQ, dK_stair, dV_stair of item ng
           tc::tc_fence_after();
           const int b = ng & 1;
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(320, 1)
           ++ndp;
           continue;
         }
-        if (ns < nme && ns < ng + 2 && (m & 4) && (ns < 2 || (m & 8))) {   // S_band of item ns
+        if (ns < nme && ns < ng + 2 && (m & 4)) {   // S_band of item ns
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
