@@ -267,8 +267,10 @@ sattn_status sattn_tshard_geometry(const sattn_tshard_desc* td, int rank, int wo
  * runs llsa_backward on the slab.  Local rows equal the unsharded call's up to summation order;
  * margin rows of outputs are scratch; margin rows the exchange does not write must be finite
  * (zero-initialise once).  The backward must get the forward's Q, K, V, O, LSE slabs.  Dense
- * inputs (in_broadcast = 0); every shard T >= L + 2R when it has neighbours.  The exchange
- * precedes the compute (no interior/edge split on the LLSA kernels).  Same transports as SA. */
+ * inputs (in_broadcast = 0); every shard T >= L + 2R when it has neighbours.  On the dense
+ * tensor-core path (bf16, D = 64, the item-form kernels) the exchange overlaps the items whose
+ * rows are all local (forward: rows [h0-R-L, h0+HZ); backward fused pass: dO rows [h0-R, h0+HZ));
+ * the edge items, then the kv pass, follow the halo.  Same transports as SA. */
 int64_t llsa_tshard_margin(int32_t L, int32_t R);
 size_t llsa_tsharded_workspace(const sattn_tshard_desc* td, const sattn_dist* d);
 sattn_status llsa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, void* Q, void* K, void* V, void* O,

@@ -45,5 +45,13 @@ int tc_llsa_backward_launches(const AttnArgs& a);
 bool tc_llsa_bwd_any_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
 bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, long long T, bool dense);
 // ws_flat: delta / LSE rows as [C][BH*T rounded to 4] (the packed-tile kv pass) instead of [C][BH][Tp]
-sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st);
+// sub4 (or null = all items): it0, nit_l, it_split, it_jump — the items of this launch per (b, h)
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st,
+                               const int* sub4 = nullptr);
+// time-shard phases of the dense LLSA path: HZ of the item form (0: not available), the item-form
+// forward over an item subset, the backward in phases (bit 0: the fused pass over the item subset
+// sub4, bit 1: the key-major kv pass); tc_llsa_backward = phases 3 over all items
+int tc_llsa_item_hz(const AttnArgs& a);
+sattn_status tc_llsa_forward_items(const AttnArgs& a, const int* sub4, cudaStream_t st);
+sattn_status tc_llsa_backward_phase(const AttnArgs& a, cudaStream_t st, int phase, const int* sub4);
 }  // namespace sattn

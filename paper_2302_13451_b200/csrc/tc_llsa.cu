@@ -394,8 +394,23 @@ __global__ void __launch_bounds__(320, 1)
 // entries at columns c' HZ + i (fixed per row), every other entry stays zero from the start.
 // Warp roles as in the forward: TMA producer, MMA issuer, two warpgroups alternating items.
 // ------------------------------------------------------------------------------------------
+// items of a launch per (b, h): item j = it0 + i + (i >= it_split ? it_jump : 0), i < nit_l (all
+// items: it0 = 0, nit_l = ceil((T + R) / HZ), it_split = nit_l, it_jump = 0; a time shard launches
+// its interior items during the halo exchange and the edge items after it)
+struct ItemSub {
+  int it0, nit_l, it_split, it_jump;
+};
+__host__ __device__ __forceinline__ int item_j(int i, const ItemSub& u) {
+  return u.it0 + i + (i >= u.it_split ? u.it_jump : 0);
+}
+ItemSub all_items(const AttnArgs& a, int HZ) {
+  const int n = (a.T + a.R + HZ - 1) / HZ;   // horizons 0 .. T-1+R per (b, h)
+  return ItemSub{0, n, n, 0};
+}
+
 struct LlsaBwdArgs {
   int T, L, R, C, BH, HZ, Tp;
+  ItemSub sub;
   float scale, scale_log2;
   const float* LSE;              // [C][BH][T]
   bf16 *dQ, *dK, *dV;            // [C][BH][T][64]
@@ -481,7 +496,7 @@ __global__ void __launch_bounds__(320, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, L = a.L, R = a.R, C = a.C, HZ = a.HZ;
-  const int nit = (T + R + HZ - 1) / HZ;                     // horizons 0 .. T-1+R per (b, h)
+  const int nit = a.sub.nit_l;                               // items of this launch per (b, h)
   const int nitems = nit * a.BH;
   const int nme = blockIdx.x < nitems ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int qbytes = C * HZ * 128, sbytes = R * HZ * 128;
@@ -512,7 +527,7 @@ __global__ void __launch_bounds__(320, 1)
   auto prefetch_l2 = [&](int k) {
     if (k >= nme) return;
     const int g = blockIdx.x + k * gridDim.x;
-    const int bh = g / nit, h0 = (g % nit) * HZ;
+    const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
     tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
     tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
     tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
@@ -532,7 +547,7 @@ __global__ void __launch_bounds__(320, 1)
       auto prefetch = [&](int k) {
         if (k >= nme) return;
         const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
         tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
         tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
         tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
@@ -542,7 +557,7 @@ __global__ void __launch_bounds__(320, 1)
       };
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
         const int s = k & 1;
         prefetch(k + 2);
         // dO / Kb / Vb as soon as the previous item on this stage has finished its MMAs; Q / Ks / Vs
@@ -639,7 +654,7 @@ __global__ void __launch_bounds__(320, 1)
     auto lse_of = [&](int k) -> float {
       if (k >= nme || !in_item) return 0.f;
       const int g = blockIdx.x + k * gridDim.x;
-      const int bh = g / nit, t = (g % nit) * HZ + i - c;
+      const int bh = g / nit, t = item_j(g % nit, a.sub) * HZ + i - c;
       return (t >= 0 && t < T) ? a.LSE[((long long)c * a.BH + bh) * T + t] : 0.f;
     };
     float lse_next = lse_of(wg);
@@ -647,7 +662,7 @@ __global__ void __launch_bounds__(320, 1)
     const int wq = warp & 3;                                  // warp within the warpgroup
     for (int k = wg; k < nme; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
-      const int bh = g / nit, h0 = (g % nit) * HZ;
+      const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
       const int b = wg, use = k >> 1;
       const int h = h0 + i, t = h - c;
       const bool row_ok = in_item && t >= 0 && t < T;
@@ -934,6 +949,7 @@ __global__ void __launch_bounds__(320, 1)
 // ------------------------------------------------------------------------------------------
 struct LlsaFwdArgs {
   int T, L, R, C, BH, HZ;
+  ItemSub sub;
   float scale, scale_log2;
   float* LSE;                    // [C][BH][T]
   bf16* O;                       // [C][BH][T][64]
@@ -977,7 +993,7 @@ __global__ void __launch_bounds__(320, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T = a.T, L = a.L, R = a.R, C = a.C, HZ = a.HZ;
-  const int nit = (T + R + HZ - 1) / HZ;
+  const int nit = a.sub.nit_l;                               // items of this launch per (b, h)
   const int nitems = nit * a.BH;
   const int nme = blockIdx.x < nitems ? (nitems - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const int qbytes = C * HZ * 128, sbytes = R * HZ * 128;
@@ -1004,7 +1020,7 @@ __global__ void __launch_bounds__(320, 1)
   auto prefetch_l2 = [&](int k) {
     if (k >= nme) return;
     const int g = blockIdx.x + k * gridDim.x;
-    const int bh = g / nit, h0 = (g % nit) * HZ;
+    const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
     tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
     tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
     tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
@@ -1021,7 +1037,7 @@ __global__ void __launch_bounds__(320, 1)
       auto prefetch = [&](int k) {
         if (k >= nme) return;
         const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
         tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
         tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
         tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
@@ -1030,7 +1046,7 @@ __global__ void __launch_bounds__(320, 1)
       };
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
-        const int bh = g / nit, h0 = (g % nit) * HZ;
+        const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
         const int s = k % NSTG;
         prefetch(k + NSTG);
         if (k >= NSTG) tc::mbar_wait(&empty[s], ((k - NSTG) / NSTG) & 1);
@@ -1101,7 +1117,7 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t za = tc::smem_u32(zrow);
     for (int k = wg; k < nme; k += 2) {
       const int g = blockIdx.x + k * gridDim.x;
-      const int bh = g / nit, h0 = (g % nit) * HZ;
+      const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
       const int b = wg, use = k >> 1;
       const int h = h0 + i, t = h - c;
       const bool row_ok = in_item && t >= 0 && t < T;
@@ -1343,7 +1359,8 @@ int fused_hz(int L, int R) {
 }
 
 template <int NB, int RM>
-sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st) {
+sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st,
+                               const ItemSub* sub) {
   using Cf = LBCfg<NB, RM>;
   const int R = a.R, C = R + 1;
   CUtensorMap mq, mdo, mkb, mvb, mks, mvs, mdq, mdk, mdv;
@@ -1366,7 +1383,9 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
     la.Tp = (int)((((long long)a.BH * a.T) + 3) & ~3LL);
   }
   la.trace = g_llsa_trace;
-  const int items = (a.T + R + HZ - 1) / HZ * a.BH;
+  la.sub = sub ? *sub : all_items(a, HZ);
+  const int items = la.sub.nit_l * a.BH;
+  if (items == 0) return SATTN_OK;
   const int grid = items < num_sms() ? items : num_sms();
   set_smem(llsa_bwd_fused_tc<NB, RM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
@@ -1391,7 +1410,7 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
 }  // namespace
 
 template <int NB, int RM>
-sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
+sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st, const ItemSub* sub = nullptr) {
   using Cf = LFCfg<NB, RM>;
   const int R = a.R, C = R + 1;
   CUtensorMap mq, mkb, mvb, mks, mvs, mo;
@@ -1406,7 +1425,9 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st) {
   la.scale = a.scale; la.scale_log2 = a.scale_log2;
   la.LSE = a.LSEout;
   la.O = reinterpret_cast<bf16*>(a.Out);
-  const int items = (a.T + R + HZ - 1) / HZ * a.BH;
+  la.sub = sub ? *sub : all_items(a, HZ);
+  const int items = la.sub.nit_l * a.BH;
+  if (items == 0) return SATTN_OK;
   const int grid = items < num_sms() ? items : num_sms();
   set_smem(llsa_fwd_item_tc<NB, RM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
@@ -1439,6 +1460,31 @@ bool tc_llsa_supported(int dtype, int D, int L, int R) {
   // (NB + 32 R packed / 2 <= 192 columns) and the 8 staged stair tiles need R <= 8; the band
   // MMA's N = 16-rounded 32 + L is instantiated for 48 and 64 (1 <= L <= 32)
   return dtype == SATTN_BF16 && D == 64 && R >= 4 && R <= kRmax && L >= 1 && L + 32 <= 64;
+}
+
+// item-form forward over an item subset (sub4 = it0, nit_l, it_split, it_jump per (b, h)); 0 when
+// the item form does not apply
+int tc_llsa_item_hz(const AttnArgs& a) {
+  return fwd_item_ok(a) && tc_llsa_bwd_fused_supported(SATTN_BF16, 64, a.L, a.R, a.BH, a.T, true) ? fused_hz(a.L, a.R)
+                                                                                                  : 0;
+}
+
+sattn_status tc_llsa_forward_items(const AttnArgs& a, const int* sub4, cudaStream_t st) {
+  const int hz = fused_hz(a.L, a.R);
+  if (!fwd_item_ok(a)) {
+    g_err = "the item-form LLSA forward does not apply";
+    return SATTN_EUNSUPPORTED;
+  }
+  const ItemSub su{sub4[0], sub4[1], sub4[2], sub4[3]};
+  const bool r16 = a.R > 8;
+  switch ((hz + a.L + 15) / 16 * 16) {
+    case 16:
+    case 32: return r16 ? fwd_item_launch<32, 16>(a, hz, st, &su) : fwd_item_launch<32, 8>(a, hz, st, &su);
+    case 48: return r16 ? fwd_item_launch<48, 16>(a, hz, st, &su) : fwd_item_launch<48, 8>(a, hz, st, &su);
+    case 64: return r16 ? fwd_item_launch<64, 16>(a, hz, st, &su) : fwd_item_launch<64, 8>(a, hz, st, &su);
+  }
+  g_err = "band too wide for the item-form LLSA forward";
+  return SATTN_EUNSUPPORTED;
 }
 
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
@@ -1477,15 +1523,19 @@ bool tc_llsa_bwd_fused_supported(int dtype, int D, int L, int R, long long BH, l
   return hz >= 4 && BH * T - 1 >= T + R;
 }
 
-sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st) {
+sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st,
+                                 const int* sub4) {
+  ItemSub su{};
+  const ItemSub* sub = nullptr;
+  if (sub4) { su = ItemSub{sub4[0], sub4[1], sub4[2], sub4[3]}; sub = &su; }
   const int HZ = fused_hz(a.L, a.R);
   const int nb = (HZ + a.L + 15) / 16 * 16;
   const bool r16 = a.R > 8;
   switch (nb) {
     case 16:
-    case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
-    case 48: return r16 ? bwd_fused_launch<48, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<48, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
-    case 64: return r16 ? bwd_fused_launch<64, 16>(a, HZ, ws_del, ws_l2, ws_flat, st) : bwd_fused_launch<64, 8>(a, HZ, ws_del, ws_l2, ws_flat, st);
+    case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, ws_flat, st, sub) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
+    case 48: return r16 ? bwd_fused_launch<48, 16>(a, HZ, ws_del, ws_l2, ws_flat, st, sub) : bwd_fused_launch<48, 8>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
+    case 64: return r16 ? bwd_fused_launch<64, 16>(a, HZ, ws_del, ws_l2, ws_flat, st, sub) : bwd_fused_launch<64, 8>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
   }
   g_err = "band too wide for the fused LLSA backward";
   return SATTN_EUNSUPPORTED;

@@ -2223,7 +2223,7 @@ sattn_status llsa_bwd_kv_launch(const AttnArgs& a0, const bf16* Q, const bf16* d
 // LLSA backward: band (channel-R keys) on the tensor-core kernels; the rest either in the fused
 // horizon-major pass (dense inputs) or, for a broadcast layer-1 input, staircase on mma.sync.
 template <int CW>
-sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
+sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st, int phase = 3, const int* sub4 = nullptr) {
   constexpr int NK = nk_of(CW);
   using LC = LkvCfg<CW>;
   const int R = a.R, C = R + 1;
@@ -2251,12 +2251,14 @@ sattn_status llsa_bwd_launch(const AttnArgs& a, cudaStream_t st) {
     const long long tot = (long long)a.BH * a.T;
     const bool flat = a.BH > 1 && tot <= (1LL << 30) &&
                       (tot + kM - 1) / kM < (long long)a.BH * ((a.T + kM - 1) / kM);
-    sattn_status r = tc_llsa_bwd_fused(a, ws_del, ws_l2, flat ? 1 : 0, st);
-    if (r != SATTN_OK) {
-      g_tc_err = tc_llsa_last_error();
-      return r;
+    if (phase & 1) {
+      sattn_status r = tc_llsa_bwd_fused(a, ws_del, ws_l2, flat ? 1 : 0, st, sub4);
+      if (r != SATTN_OK) {
+        g_tc_err = tc_llsa_last_error();
+        return r;
+      }
     }
-    return llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, flat, st);
+    return phase & 2 ? llsa_bwd_kv_launch<CW>(a, Q, dO, Kr, Vr, dK, dV, ws_del, ws_l2, flat, st) : SATTN_OK;
   }
   StairArgs sa{};
   sa.Q = Q; sa.K = K; sa.V = V; sa.dO = dO;
@@ -2582,13 +2584,20 @@ bool tc_llsa_bwd_any_supported(int dtype, int D, int L, int R, long long BH, lon
          (L + 1 + 31 <= 80 && tc_llsa_bwd_fused_supported(dtype, D, L, R, BH, T, dense));
 }
 
-sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) {
+sattn_status tc_llsa_backward(const AttnArgs& a, cudaStream_t st) { return tc_llsa_backward_phase(a, st, 3, nullptr); }
+
+sattn_status tc_llsa_backward_phase(const AttnArgs& a, cudaStream_t st, int phase, const int* sub4) {
+  if ((phase != 3 || sub4) &&
+      !tc_llsa_bwd_fused_supported(SATTN_BF16, kD, a.L, a.R, a.BH, a.T, a.in_cs != 0)) {
+    g_tc_err = "LLSA backward phases need the fused horizon-major pass (dense inputs)";
+    return SATTN_EUNSUPPORTED;
+  }
   switch (cw_of(a.L + 1)) {
-    case 32: return llsa_bwd_launch<32>(a, st);
-    case 48: return llsa_bwd_launch<48>(a, st);
-    case 64: return llsa_bwd_launch<64>(a, st);
-    case 72: return llsa_bwd_launch<72>(a, st);
-    case 80: return llsa_bwd_launch<80>(a, st);
+    case 32: return llsa_bwd_launch<32>(a, st, phase, sub4);
+    case 48: return llsa_bwd_launch<48>(a, st, phase, sub4);
+    case 64: return llsa_bwd_launch<64>(a, st, phase, sub4);
+    case 72: return llsa_bwd_launch<72>(a, st, phase, sub4);
+    case 80: return llsa_bwd_launch<80>(a, st, phase, sub4);
   }
   g_tc_err = "band too wide for the LLSA tensor-core backward";
   return SATTN_EUNSUPPORTED;

@@ -432,6 +432,47 @@ sattn_status lshard_setup(const sattn_tshard_desc* td, const sattn_dist* d, LSha
   return SATTN_OK;
 }
 
+// Interior / edge item split of the dense item-form LLSA kernels on a slab (per (b, h), item j =
+// horizons [j HZ, j HZ + HZ)): an item reads rows [j HZ - lo, j HZ + HZ - 1] (forward: lo = R + L,
+// Q / K / V; backward fused pass: lo = R, the halo-exchanged dO), so it is interior when those rows
+// are local or beyond a missing neighbour.  sub = {it0, nit_l, it_split, it_jump} (tc_dispatch.h).
+struct ItemSplit {
+  int interior[4], edges[4];
+};
+ItemSplit item_split(const LShard& s, int hz, int lo) {
+  const int R = s.slab.R, nit = (s.Ts + R + hz - 1) / hz;
+  int ja = s.hl == 0 ? 0 : (s.hl + lo + hz - 1) / hz;
+  int jb = nit;
+  if (s.hr > 0) {
+    const int lim = s.hl + s.g.T_loc - hz;   // j hz + hz - 1 <= hl + T_loc - 1
+    jb = lim < 0 ? 0 : lim / hz + 1;
+  }
+  if (ja > nit) ja = nit;
+  if (jb > nit) jb = nit;
+  if (jb < ja) jb = ja;
+  ItemSplit r;
+  const int in[4] = {ja, jb - ja, jb - ja, 0}, ed[4] = {0, ja + (nit - jb), ja, jb - ja};
+  for (int i = 0; i < 4; ++i) { r.interior[i] = in[i]; r.edges[i] = ed[i]; }
+  return r;
+}
+
+// slab args of the dense tensor-core LLSA path ([C][B][H][Ts][D] planes), or false when it does not
+// apply (then the caller runs the exchange and the ordinary call)
+bool lshard_args(const LShard& s, AttnArgs& a, int& hz) {
+  const sattn_desc& l = s.slab;
+  if (l.dtype != SATTN_BF16 || l.D != 64 || l.impl == SATTN_IMPL_FFMA || (!s.g.left && !s.g.right)) return false;
+  a = AttnArgs{};
+  a.T = s.Ts;
+  a.L = l.L;
+  a.R = l.R;
+  a.BH = (int)(l.B * l.H);
+  a.scale = desc_scale(&l);
+  a.scale_log2 = a.scale * kLog2e;
+  a.in_cs = a.out_cs = (long long)a.BH * s.Ts * 64;
+  hz = tc_llsa_item_hz(a);
+  return hz > 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -605,6 +646,31 @@ sattn_status llsa_forward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, v
   const size_t need = halo_ws(s.g, h, 3);
   if (need && (!ws || ws_bytes < need)) return set_error(SATTN_ECONFIG, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  AttnArgs a;
+  int hz = 0;
+  if (lshard_args(s, a, hz)) {
+    // the interior items overlap the exchange (NCCL: it runs on the dist stream; a caller transport
+    // runs synchronously on `st` after the interior launch), the edge items follow the halo
+    a.Q = Q; a.K = K; a.V = V; a.Out = O; a.LSEout = LSE;
+    const ItemSplit sp = item_split(s, hz, s.slab.R + s.slab.L);
+    const bool ext = d->comm == nullptr;
+    if (!ext && (r = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return r;
+    if (sp.interior[1] > 0) {
+      if ((r = tc_llsa_forward_items(a, sp.interior, st)) != SATTN_OK) return set_error(r, tc_llsa_last_error());
+      count_launches(1);
+    }
+    if (ext && (r = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return r;
+    if (!ext) {
+      const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
+      if (e != cudaSuccess) return cuda_fail("cudaStreamWaitEvent", e);
+    }
+    if (sp.edges[1] > 0) {
+      if ((r = tc_llsa_forward_items(a, sp.edges, st)) != SATTN_OK) return set_error(r, tc_llsa_last_error());
+      count_launches(1);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SATTN_OK : cuda_fail("time-sharded LLSA forward launch", e);
+  }
   if ((r = exchange(d, s.g, h, 3, (char*)ws, st)) != SATTN_OK) return r;
   if (d->comm) {
     const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
@@ -625,6 +691,34 @@ sattn_status llsa_backward_tsharded(const sattn_tshard_desc* td, sattn_dist* d, 
   const size_t nb = llsa_backward_workspace(&s.slab);
   if (ws_bytes < nh + nb) return set_error(SATTN_ECONFIG, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
+  AttnArgs a;
+  int hz = 0;
+  if (lshard_args(s, a, hz)) {
+    // the fused pass's interior items overlap the dO exchange; its edge items and the kv pass follow
+    a.Q = Q; a.K = K; a.V = V; a.O = O; a.LSE = LSE; a.dO = dO;
+    a.dQ = dQ; a.dK = dK; a.dV = dV;
+    a.delta = reinterpret_cast<float*>((char*)ws + nh);
+    const ItemSplit sp = item_split(s, hz, s.slab.R);
+    const bool ext = d->comm == nullptr;
+    if (!ext && (r = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return r;
+    if (sp.interior[1] > 0) {
+      if ((r = tc_llsa_backward_phase(a, st, 1, sp.interior)) != SATTN_OK) return set_error(r, tc_last_error());
+      count_launches(1);
+    }
+    if (ext && (r = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return r;
+    if (!ext) {
+      const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
+      if (e != cudaSuccess) return cuda_fail("cudaStreamWaitEvent", e);
+    }
+    if (sp.edges[1] > 0) {
+      if ((r = tc_llsa_backward_phase(a, st, 1, sp.edges)) != SATTN_OK) return set_error(r, tc_last_error());
+      count_launches(1);
+    }
+    if ((r = tc_llsa_backward_phase(a, st, 2, nullptr)) != SATTN_OK) return set_error(r, tc_last_error());
+    count_launches(1);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SATTN_OK : cuda_fail("time-sharded LLSA backward launch", e);
+  }
   if ((r = exchange(d, s.g, h, 1, (char*)ws, st)) != SATTN_OK) return r;
   if (d->comm) {
     const cudaError_t e = cudaStreamWaitEvent(st, d->ev_halo, 0);
