@@ -419,7 +419,7 @@ struct LlsaBwdArgs {
   long long* trace;              // debug: per-item phase clock64 stamps of CTA 0 ([16][64]), or null
 };
 
-template <int NB, int RM> struct LBCfg {
+template <int NB, int RM, bool HM = false> struct LBCfg {
   static constexpr int QB = 128 * 128;             // Q / dO item tiles
   static constexpr int KBB = NB * 128;             // band K / V tiles
   static constexpr int SB = 112 * 128;             // stair K / V tiles (rows c' HZ + i, R HZ <= 112)
@@ -427,10 +427,10 @@ template <int NB, int RM> struct LBCfg {
   static constexpr int XB = 2 * 128 * 128;         // DS / PS
   // staircase scores / dP on mma.sync (16 x 8 blocks per horizon) through a per-warpgroup fp32
   // scratch [128][RM] (S, then dP), when it fits; otherwise packed-FFMA2 dot products
-  static constexpr bool SMMA = 1024 + 2 * STAGE + 2 * XB + 2 * 128 * RM * 4 + 128 + 256 <= 232448;
+  static constexpr bool SMMA = !HM && 1024 + 2 * STAGE + 2 * XB + 2 * 128 * RM * 4 + 128 + 256 <= 232448;
   // both products in one pass through a [2][128][RM] scratch when that fits too (R <= 8)
   static constexpr bool SFUSE = SMMA && 1024 + 2 * STAGE + 2 * XB + 2 * 2 * 128 * RM * 4 + 128 + 256 <= 232448;
-  static constexpr int SCR = SMMA ? (SFUSE ? 2 : 1) * 128 * RM * 4 : 0;   // per warpgroup
+  static constexpr int SCR = SMMA ? (SFUSE ? 2 : 1) * 128 * RM * 4 : 0;   // per warpgroup (none for HM)
   static constexpr int SMEM = 1024 + 2 * STAGE + 2 * XB + 2 * SCR + 128 + 256;
   static_assert(NB + 192 <= 256, "TMEM columns per item");
   static_assert(SMEM <= 232448, "shared memory");
@@ -465,14 +465,19 @@ __device__ __forceinline__ void store_row64(bf16* dst, const float* v, float sc)
                        pack_bf16(v[8 * ch + 4] * sc, v[8 * ch + 5] * sc), pack_bf16(v[8 * ch + 6] * sc, v[8 * ch + 7] * sc));
 }
 
-template <int NB, int RM>
+template <int NB, int RM, bool HM>
 __global__ void __launch_bounds__(320, 1)
     llsa_bwd_fused_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmdO,
                       const __grid_constant__ CUtensorMap tmKb, const __grid_constant__ CUtensorMap tmVb,
                       const __grid_constant__ CUtensorMap tmKs, const __grid_constant__ CUtensorMap tmVs,
                       const __grid_constant__ CUtensorMap tmdQ, const __grid_constant__ CUtensorMap tmdK,
                       const __grid_constant__ CUtensorMap tmdV, LlsaBwdArgs a) {
-  using Cf = LBCfg<NB, RM>;
+  // HM (horizon-major, R == RM): item rows r = i C + c and staircase keys m = i' RM + c' (the TMA
+  // boxes are ordered so), the staircase S / dP as dense tcgen05 products Q Ks^T / dO Vs^T into
+  // TMEM [NB, NB + HZ RM) (a row's R entries are the RM contiguous columns of its horizon), instead
+  // of per-horizon mma.sync blocks through a shared-memory scratch (the legacy mma.sync rate bound
+  // that phase)
+  using Cf = LBCfg<NB, RM, HM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;                                    // [Q | dO | Kb | Vb | Ks | Vs] x 2
@@ -528,12 +533,12 @@ __global__ void __launch_bounds__(320, 1)
     if (k >= nme) return;
     const int g = blockIdx.x + k * gridDim.x;
     const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
-    tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
-    tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmQ, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+    tc::tma_prefetch_4d(&tmdO, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
     tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
     tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
-    tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
-    tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmKs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+    tc::tma_prefetch_4d(&tmVs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
   };
   if (tid == 0)
     for (int k = 0; k < 2; ++k) prefetch_l2(k);
@@ -548,12 +553,12 @@ __global__ void __launch_bounds__(320, 1)
         if (k >= nme) return;
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
-        tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
-        tc::tma_prefetch_4d(&tmdO, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmQ, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+        tc::tma_prefetch_4d(&tmdO, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
         tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
         tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
-        tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
-        tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmKs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+        tc::tma_prefetch_4d(&tmVs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
       };
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
@@ -565,13 +570,13 @@ __global__ void __launch_bounds__(320, 1)
         if (k >= 2) tc::mbar_wait(&emptyA[s], ((k - 2) >> 1) & 1);
         uint8_t* sb = stage0 + s * Cf::STAGE;
         tc::mbar_expect_tx(&full[s], 2 * qbytes + 2 * Cf::KBB + 2 * sbytes);
-        tc::tma_load_4d(sb + Cf::QB, &tmdO, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb + Cf::QB, &tmdO, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);
         tc::tma_load_4d(sb + 2 * Cf::QB, &tmKb, &full[s], 0, h0 - R - L, bh, R);   // band keys (u, R)
         tc::tma_load_4d(sb + 2 * Cf::QB + Cf::KBB, &tmVb, &full[s], 0, h0 - R - L, bh, R);
         if (k >= 2) tc::mbar_wait(&empty[s], ((k - 2) >> 1) & 1);
-        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);                         // rows (h0+i-c, c)
-        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, h0, 0, bh);   // (h0+i-c', c')
-        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb, &tmQ, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);                         // rows (h0+i-c, c)
+        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);   // (h0+i-c', c')
+        tc::tma_load_4d(sb + 2 * Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);
       }
     }
   } else if (warp == 1) {
@@ -580,6 +585,10 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idQ = tc::idesc_bf16(128, kD, 0, 1);
       constexpr uint32_t idK = tc::idesc_bf16(128, kD, 1, 1);
       const int nks = (R * HZ + 15) / 16;                    // 16-key steps over the stair keys
+      // HM: dense staircase products into [NB, NB + 16 nks) (over item ng - 2's dQ / dK columns:
+      // S waits for that item's epilogue instead of the dQ / dK / dV MMAs)
+      const uint32_t idSt = tc::idesc_bf16(128, 16 * nks, 0, 0);
+      (void)idSt;
       int ns = 0, ndp = 0, ng = 0;
       while (ng < nme) {
         // dQ / dK / dV (ng) overwrite the accumulators of item ng - 2: they wait for its epilogue
@@ -587,8 +596,9 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t m = tc::mbar_test4(tc::smem_u32(&dsfull[ng & 1]), (ng >> 1) & 1,
                                           tc::smem_u32(&xfree[ndp & 1]), (ndp >> 1) & 1,
                                           tc::smem_u32(&full[ns & 1]), (ns >> 1) & 1,
-                                          tc::smem_u32(&tfree[ng & 1]), ((ng + 2) >> 1) & 1);
-        if (ng < ndp && (m & 1) && (ng < 2 || (m & 8))) {   // dQ, dK_stair, dV_stair of item ng
+                                          HM ? tc::smem_u32(&tfree[ns & 1]) : tc::smem_u32(&tfree[ng & 1]),
+                                          HM ? ((ns + 2) >> 1) & 1 : ((ng + 2) >> 1) & 1);
+        if (ng < ndp && (m & 1) && (HM || ng < 2 || (m & 8))) {   // dQ, dK_stair, dV_stair of item ng
           tc::tc_fence_after();
           const int b = ng & 1;
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
@@ -623,11 +633,18 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(vb + 32 * j), idS,
                          j > 0);
+          if constexpr (HM) {
+            const uint32_t vs = vb + Cf::KBB + Cf::SB;
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(tbase + b * 256 + NB, tc::desc_kmajor_sw128(dO + 32 * j), tc::desc_kmajor_sw128(vs + 32 * j),
+                           idSt, j > 0);
+          }
           tc::mma_commit(&dpfull[b]);
           ++ndp;
           continue;
         }
-        if (ns < nme && ns < ng + 2 && (m & 4)) {   // S_band of item ns
+        if (ns < nme && ns < ng + 2 && (m & 4) && (!HM || ns < 2 || (m & 8))) {   // S_band of item ns
           tc::tc_fence_after();
           const int b = ns & 1;
           const uint32_t sb = tc::smem_u32(stage0 + b * Cf::STAGE);
@@ -636,6 +653,13 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kb + 32 * j), idS,
                          j > 0);
+          if constexpr (HM) {
+            const uint32_t ks = kb + 2 * Cf::KBB;
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(tbase + b * 256 + NB, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(ks + 32 * j),
+                           idSt, j > 0);
+          }
           tc::mma_commit(&sfull[b]);
           ++ns;
           continue;
@@ -647,8 +671,27 @@ __global__ void __launch_bounds__(320, 1)
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lanes = uint32_t(32 * q4) << 16;
-    const int c = r / HZ, i = r - c * HZ;                  // output channel / horizon offset of row r
-    const bool in_item = c < C;
+    // output channel / horizon offset of row r (HM: r = i C + c; else r = c HZ + i)
+    const int c = HM ? r % C : r / HZ, i = HM ? r / C : r - (r / HZ) * HZ;
+    const bool in_item = HM ? i < HZ : c < C;
+    // HM: the RM staircase columns of row r are [i RM, i RM + RM) of the stair block; a warp's 32
+    // rows span at most KH horizons, read as one warp-uniform window from its first horizon i_lo
+    constexpr int KH = 31 / (RM + 1) + 2;
+    const int i_lo = HM ? (32 * q4) / C : 0;
+    auto stair_cols = [&](uint32_t xcol, float* out) {   // out[c'] = column xcol + i RM + c'
+      float v[KH * RM];
+#pragma unroll
+      for (int j = 0; j < KH * RM / 8; ++j) tc::tmem_ld8(xcol + i_lo * RM + 8 * j, v + 8 * j);
+      tc::tmem_ld_wait();
+      const int kq = i - i_lo;
+#pragma unroll
+      for (int cp = 0; cp < RM; ++cp) out[cp] = v[cp];
+#pragma unroll
+      for (int kk = 1; kk < KH; ++kk)
+#pragma unroll
+        for (int cp = 0; cp < RM; ++cp) out[cp] = kq == kk ? v[kk * RM + cp] : out[cp];
+    };
+    (void)stair_cols; (void)i_lo;
     const uint32_t xdsa = tc::smem_u32(xds), xpsa = tc::smem_u32(xps);
     // this row's LSE of item k (loaded one item ahead: the global load's latency is off the chain)
     auto lse_of = [&](int k) -> float {
@@ -676,7 +719,9 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_wait(&full[b], use & 1);
       LTR(1);
       float sst[RM], dst[RM];
-      if constexpr (Cf::SMMA) {
+      if constexpr (HM) {
+        // staircase S / dP come from TMEM with the band's (below)
+      } else if constexpr (Cf::SMMA) {
         // ---- staircase on mma.sync: horizon ih's blocks S = Q_ih K_ih^T, then dP = dO_ih V_ih^T
         //      (rows c: Q rows c HZ + ih; cols c': stair rows c' HZ + ih; ceil(C/16) x RM/8 blocks of
         //      16 x 8), two horizons per warp iteration, scattered to the scratch rows r = c HZ + ih
@@ -810,6 +855,15 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_after();
       float p[NB];
       const uint32_t x = tbase + lanes + b * 256;
+      if constexpr (HM) {   // P of the staircase slots (h - c', c'), c' < R (= RM)
+        stair_cols(x + NB, sst);
+#pragma unroll
+        for (int cp = 0; cp < RM; ++cp) {
+          const int f = h - cp;
+          const bool ok = row_ok && f >= 0 && f < T;
+          sst[cp] = ok ? tc::ex2(fmaf(sst[cp], a.scale_log2, -lse2)) : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NB / 8; ++j) tc::tmem_ld8(x + 8 * j, p + 8 * j);
       tc::tmem_ld_wait();
@@ -828,6 +882,7 @@ __global__ void __launch_bounds__(320, 1)
       LTR(5);
       __syncwarp();
       tc::tc_fence_after();
+      if constexpr (HM) stair_cols(x + NB, dst);   // staircase dP
       // dP is read from TMEM twice (delta, then dS) instead of being held next to P
       float delta = 0.f;
 #pragma unroll
@@ -857,6 +912,20 @@ __global__ void __launch_bounds__(320, 1)
       // read them (one buffer shared by both warpgroups)
       if (k >= 1) tc::mbar_wait(xsfree, (k - 1) & 1);
       if (in_item) {
+        if constexpr (HM) {   // the row's RM staircase entries: 16-byte chunks at column i RM
+#pragma unroll
+          for (int q8 = 0; q8 < RM / 8; ++q8) {
+            float d8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d8[e] = sst[8 * q8 + e] * (dst[8 * q8 + e] - delta);
+            const int col = i * RM + 8 * q8;
+            tc::st_shared_v4(xs_addr(xdsa, r, col), make_uint4(pack_bf16(d8[0], d8[1]), pack_bf16(d8[2], d8[3]),
+                                                              pack_bf16(d8[4], d8[5]), pack_bf16(d8[6], d8[7])));
+            const float* p8 = sst + 8 * q8;
+            tc::st_shared_v4(xs_addr(xpsa, r, col), make_uint4(pack_bf16(p8[0], p8[1]), pack_bf16(p8[2], p8[3]),
+                                                              pack_bf16(p8[4], p8[5]), pack_bf16(p8[6], p8[7])));
+          }
+        } else {
 #pragma unroll
         for (int cp = 0; cp < RM; ++cp) {
           if (cp < R) {
@@ -864,6 +933,7 @@ __global__ void __launch_bounds__(320, 1)
             tc::st_shared_u16(xs_addr(xdsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(ds)));
             tc::st_shared_u16(xs_addr(xpsa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
           }
+        }
         }
       }
       
@@ -894,8 +964,9 @@ __global__ void __launch_bounds__(320, 1)
       // TMA stores; edge items: direct row stores (a skewed box there would cross into the
       // neighbouring channel planes).  The stage is released once the stores have read it.
       const bool tma_out = h0 >= R && h0 + HZ <= T;
-      const int cq = r / HZ, iq = r - cq * HZ, u = h0 + iq - cq;
-      const bool key_ok = cq < R && u >= 0 && u < T;
+      // staircase key of accumulator row r: (u, cq), u = h0 + iq - cq (HM: r = iq RM + cq)
+      const int cq = HM ? r % RM : r / HZ, iq = HM ? r / RM : r - (r / HZ) * HZ, u = h0 + iq - cq;
+      const bool key_ok = (HM ? iq < HZ : cq < R) && u >= 0 && u < T;
       const long long krow = ((long long)cq * a.BH + bh) * T + u;
       uint8_t* qst = const_cast<uint8_t*>(sbp);
       uint8_t* kst = qst + 2 * Cf::QB + 2 * Cf::KBB;
@@ -916,9 +987,9 @@ __global__ void __launch_bounds__(320, 1)
       tc::named_bar(1 + wg, 128);
       if (r == 0) {
         if (tma_out) {
-          tc::tma_store_4d(&tmdQ, qst, 0, h0, 0, bh);
-          tc::tma_store_4d(&tmdK, kst, 0, h0, 0, bh);
-          tc::tma_store_4d(&tmdV, vst, 0, h0, 0, bh);
+          tc::tma_store_4d(&tmdQ, qst, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+          tc::tma_store_4d(&tmdK, kst, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+          tc::tma_store_4d(&tmdV, vst, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
           tc::bulk_commit();
           tc::bulk_wait_read0();
         }
@@ -1304,6 +1375,16 @@ bool map_skew(CUtensorMap* m, const void* base, int T, int BH, int C, int R, int
   return tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) == CUDA_SUCCESS;
 }
 
+// the skewed map with the channel as the faster box dimension: box (64, nch, rows) lands rows
+// i nch + c (horizon-major) instead of c rows + i; element (c, h) is frame h - c of channel c
+bool map_hm(CUtensorMap* m, const void* base, int T, int BH, int C, int R, int rows, int nch) {
+  if ((long long)BH * T - 1 < (long long)T + R) return false;
+  cuuint64_t dims[4] = {64, (cuuint64_t)C, (cuuint64_t)(T + R), (cuuint64_t)BH};
+  cuuint64_t strides[3] = {((cuuint64_t)BH * T - 1) * 128, 128, (cuuint64_t)T * 128};
+  cuuint32_t box[4] = {64, (cuuint32_t)nch, (cuuint32_t)rows, 1};
+  return tmap_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) == CUDA_SUCCESS;
+}
+
 template <int NB>
 sattn_status launch(const AttnArgs& a, cudaStream_t st) {
   using Cf = LCfg<NB>;
@@ -1358,17 +1439,18 @@ int fused_hz(int L, int R) {
   return hz;
 }
 
-template <int NB, int RM>
+template <int NB, int RM, bool HM = false>
 sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* ws_l2, int ws_flat, cudaStream_t st,
                                const ItemSub* sub) {
-  using Cf = LBCfg<NB, RM>;
+  using Cf = LBCfg<NB, RM, HM>;
   const int R = a.R, C = R + 1;
+  auto mskew = HM ? map_hm : map_skew;
   CUtensorMap mq, mdo, mkb, mvb, mks, mvs, mdq, mdk, mdv;
-  if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map_skew(&mdo, a.dO, a.T, a.BH, C, R, HZ, C) ||
+  if (!mskew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !mskew(&mdo, a.dO, a.T, a.BH, C, R, HZ, C) ||
       !map4(&mkb, a.K, a.T, a.BH, C, NB) || !map4(&mvb, a.V, a.T, a.BH, C, NB) ||
-      !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) || !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) ||
-      !map_skew(&mdq, a.dQ, a.T, a.BH, C, R, HZ, C) || !map_skew(&mdk, a.dK, a.T, a.BH, C, R, HZ, R) ||
-      !map_skew(&mdv, a.dV, a.T, a.BH, C, R, HZ, R)) {
+      !mskew(&mks, a.K, a.T, a.BH, C, R, HZ, R) || !mskew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) ||
+      !mskew(&mdq, a.dQ, a.T, a.BH, C, R, HZ, C) || !mskew(&mdk, a.dK, a.T, a.BH, C, R, HZ, R) ||
+      !mskew(&mdv, a.dV, a.T, a.BH, C, R, HZ, R)) {
     g_err = "tensor maps of the fused LLSA backward";
     return SATTN_ECUDA;
   }
@@ -1387,7 +1469,7 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   const int items = la.sub.nit_l * a.BH;
   if (items == 0) return SATTN_OK;
   const int grid = items < num_sms() ? items : num_sms();
-  set_smem(llsa_bwd_fused_tc<NB, RM>, Cf::SMEM);
+  set_smem(llsa_bwd_fused_tc<NB, RM, HM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);
@@ -1398,7 +1480,7 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM>, mq, mdo, mkb, mvb, mks, mvs, mdq, mdk,
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_bwd_fused_tc<NB, RM, HM>, mq, mdo, mkb, mvb, mks, mvs, mdq, mdk,
                                            mdv, la);
   if (e != cudaSuccess) {
     g_err = std::string("fused LLSA backward launch: ") + cudaGetErrorString(e);
@@ -1531,6 +1613,13 @@ sattn_status tc_llsa_bwd_fused(const AttnArgs& a, float* ws_del, float* ws_l2, i
   const int HZ = fused_hz(a.L, a.R);
   const int nb = (HZ + a.L + 15) / 16 * 16;
   const bool r16 = a.R > 8;
+  // horizon-major items with the staircase on tcgen05 when R fills the RM staircase columns
+  if ((a.R == 8 || a.R == 16) && (HZ * a.R) % 16 == 0 && (nb == 48 || nb == 64)) {
+    if (nb == 48) return r16 ? bwd_fused_launch<48, 16, true>(a, HZ, ws_del, ws_l2, ws_flat, st, sub)
+                             : bwd_fused_launch<48, 8, true>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
+    return r16 ? bwd_fused_launch<64, 16, true>(a, HZ, ws_del, ws_l2, ws_flat, st, sub)
+               : bwd_fused_launch<64, 8, true>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
+  }
   switch (nb) {
     case 16:
     case 32: return r16 ? bwd_fused_launch<32, 16>(a, HZ, ws_del, ws_l2, ws_flat, st, sub) : bwd_fused_launch<32, 8>(a, HZ, ws_del, ws_l2, ws_flat, st, sub);
