@@ -1026,26 +1026,29 @@ struct LlsaFwdArgs {
   bf16* O;                       // [C][BH][T][64]
 };
 
-template <int NB, int RM> struct LFCfg {
+template <int NB, int RM, bool HM = false> struct LFCfg {
   static constexpr int QB = 128 * 128;
   static constexpr int KBB = NB * 128;
   static constexpr int SB = 112 * 128;
   static constexpr int STAGE = QB + 2 * KBB + 2 * SB;      // Q | Kb | Vb | Ks | Vs
   static constexpr int XB = 2 * 128 * 128;                 // PS (shared by the warpgroups, see below)
-  static constexpr int SCR = 128 * RM * 4;                 // stair scores per warpgroup
+  static constexpr int SCR = HM ? 0 : 128 * RM * 4;       // stair scores per warpgroup (mma.sync path)
   // three stages where they fit (the warpgroups otherwise wait on the TMA loads)
   static constexpr int NSTG = 1024 + 3 * STAGE + XB + 2 * SCR + 128 + 256 <= 232448 ? 3 : 2;
   static constexpr int SMEM = 1024 + NSTG * STAGE + XB + 2 * SCR + 128 + 256;
   static_assert(NB + 64 <= 256 && SMEM <= 232448, "TMEM / shared memory");
 };
 
-template <int NB, int RM>
+template <int NB, int RM, bool HM>
 __global__ void __launch_bounds__(320, 1)
     llsa_fwd_item_tc(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKb,
                      const __grid_constant__ CUtensorMap tmVb, const __grid_constant__ CUtensorMap tmKs,
                      const __grid_constant__ CUtensorMap tmVs, const __grid_constant__ CUtensorMap tmO,
                      LlsaFwdArgs a) {
-  using Cf = LFCfg<NB, RM>;
+  // HM (R == RM): horizon-major item rows i C + c and staircase keys i' RM + c' (reordered skewed
+  // boxes), the staircase scores as one dense tcgen05 product Q Ks^T into TMEM [NB + 64, NB + 64 +
+  // HZ RM) (each row's RM entries are its horizon's contiguous columns), as the fused backward
+  using Cf = LFCfg<NB, RM, HM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage0 = smem;
@@ -1092,11 +1095,11 @@ __global__ void __launch_bounds__(320, 1)
     if (k >= nme) return;
     const int g = blockIdx.x + k * gridDim.x;
     const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
-    tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmQ, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
     tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
     tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
-    tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
-    tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+    tc::tma_prefetch_4d(&tmKs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+    tc::tma_prefetch_4d(&tmVs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
   };
   if (tid == 0)
     for (int k = 0; k < 2; ++k) prefetch_l2(k);
@@ -1109,11 +1112,11 @@ __global__ void __launch_bounds__(320, 1)
         if (k >= nme) return;
         const int g = blockIdx.x + k * gridDim.x;
         const int bh = g / nit, h0 = item_j(g % nit, a.sub) * HZ;
-        tc::tma_prefetch_4d(&tmQ, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmQ, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
         tc::tma_prefetch_4d(&tmKb, 0, h0 - R - L, bh, R);
         tc::tma_prefetch_4d(&tmVb, 0, h0 - R - L, bh, R);
-        tc::tma_prefetch_4d(&tmKs, 0, h0, 0, bh);
-        tc::tma_prefetch_4d(&tmVs, 0, h0, 0, bh);
+        tc::tma_prefetch_4d(&tmKs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+        tc::tma_prefetch_4d(&tmVs, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
       };
       for (int k = 0; k < nme; ++k) {
         const int g = blockIdx.x + k * gridDim.x;
@@ -1123,11 +1126,11 @@ __global__ void __launch_bounds__(320, 1)
         if (k >= NSTG) tc::mbar_wait(&empty[s], ((k - NSTG) / NSTG) & 1);
         uint8_t* sb = stage0 + s * Cf::STAGE;
         tc::mbar_expect_tx(&full[s], qbytes + 2 * Cf::KBB + 2 * sbytes);
-        tc::tma_load_4d(sb, &tmQ, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb, &tmQ, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);
         tc::tma_load_4d(sb + Cf::QB, &tmKb, &full[s], 0, h0 - R - L, bh, R);
         tc::tma_load_4d(sb + Cf::QB + Cf::KBB, &tmVb, &full[s], 0, h0 - R - L, bh, R);
-        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, h0, 0, bh);
-        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, h0, 0, bh);
+        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB, &tmKs, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);
+        tc::tma_load_4d(sb + Cf::QB + 2 * Cf::KBB + Cf::SB, &tmVs, &full[s], 0, HM ? 0 : h0, HM ? h0 : 0, bh);
       }
     }
   } else if (warp == 1) {
@@ -1135,6 +1138,8 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idS = tc::idesc_bf16(128, NB, 0, 0);
       constexpr uint32_t idO = tc::idesc_bf16(128, kD, 0, 1);
       const int nks = (R * HZ + 15) / 16;
+      const uint32_t idSt = tc::idesc_bf16(128, 16 * nks, 0, 0);
+      (void)idSt;
       int ns = 0, no = 0;
       while (no < nme) {
         // O(no) overwrites the O columns of item no - 2: it waits for that item's epilogue (tfree);
@@ -1170,6 +1175,13 @@ __global__ void __launch_bounds__(320, 1)
           for (int j = 0; j < kD / 16; ++j)
             tc::mma_bf16(tbase + b * 256, tc::desc_kmajor_sw128(q + 32 * j), tc::desc_kmajor_sw128(kb + 32 * j), idS,
                          j > 0);
+          if constexpr (HM) {   // staircase scores, dense: columns [NB + 64, NB + 64 + 16 nks) (beside O)
+            const uint32_t ks = kb + 2 * Cf::KBB;
+#pragma unroll
+            for (int j = 0; j < kD / 16; ++j)
+              tc::mma_bf16(tbase + b * 256 + NB + 64, tc::desc_kmajor_sw128(q + 32 * j),
+                           tc::desc_kmajor_sw128(ks + 32 * j), idSt, j > 0);
+          }
           tc::mma_commit(&sfull[b]);
           ++ns;
           continue;
@@ -1181,8 +1193,10 @@ __global__ void __launch_bounds__(320, 1)
     const int q4 = warp & 3;
     const int r = 32 * q4 + lane;
     const uint32_t lanes = uint32_t(32 * q4) << 16;
-    const int c = r / HZ, i = r - c * HZ;
-    const bool in_item = c < C;
+    const int c = HM ? r % C : r / HZ, i = HM ? r / C : r - (r / HZ) * HZ;
+    const bool in_item = HM ? i < HZ : c < C;
+    constexpr int KH = 31 / (RM + 1) + 2;                   // horizons a warp's 32 rows span (HM)
+    const int i_lo = HM ? (32 * q4) / C : 0;
     const int wq = warp & 3;
     const uint32_t psa = tc::smem_u32(xps0), sca = tc::smem_u32(scr0 + wg * Cf::SCR);
     const uint32_t za = tc::smem_u32(zrow);
@@ -1198,7 +1212,8 @@ __global__ void __launch_bounds__(320, 1)
       tc::mbar_wait(&full[st], (k / NSTG) & 1);
       // ---- staircase scores S[c][c'] = q_(h-c, c) . k_(h-c', c') on mma.sync: per horizon ceil(C/16)
       //      x RM/8 blocks of 16 x 8 (two horizons per iteration), through the scratch [128][RM]
-      {
+      //      (HM: from TMEM below)
+      if constexpr (!HM) {
         const uint32_t qt = sb, ks = sb + Cf::QB + 2 * Cf::KBB;
         const int gq = lane >> 2, t4 = lane & 3;
         const int nmb = (C + 15) / 16;
@@ -1239,9 +1254,9 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
-      tc::named_bar(1 + wg, 128);
       float sst[RM];
-      {
+      if constexpr (!HM) {
+        tc::named_bar(1 + wg, 128);
         const uint32_t o = sca + (uint32_t)r * RM * 4;
 #pragma unroll
         for (int q = 0; q < RM / 4; ++q) {
@@ -1253,14 +1268,32 @@ __global__ void __launch_bounds__(320, 1)
             sst[cp] = (row_ok && cp < R && f >= 0 && f < T) ? __uint_as_float(sv[e]) : neg_inf();
           }
         }
+        tc::named_bar(1 + wg, 128);   // scratch rewritten by this warpgroup's next item
       }
-      tc::named_bar(1 + wg, 128);   // scratch rewritten by this warpgroup's next item
       // ---- band strip + joint softmax
       tc::mbar_wait(&sfull[b], use & 1);
       __syncwarp();
       tc::tc_fence_after();
       float s[NB];
       const uint32_t x = tbase + lanes + b * 256;
+      if constexpr (HM) {   // the row's staircase columns: one warp-uniform window of KH horizons + selects
+        float v[KH * RM];
+#pragma unroll
+        for (int j = 0; j < KH * RM / 8; ++j) tc::tmem_ld8(x + NB + 64 + i_lo * RM + 8 * j, v + 8 * j);
+        tc::tmem_ld_wait();
+        const int kq = i - i_lo;
+#pragma unroll
+        for (int cp = 0; cp < RM; ++cp) sst[cp] = v[cp];
+#pragma unroll
+        for (int kk = 1; kk < KH; ++kk)
+#pragma unroll
+          for (int cp = 0; cp < RM; ++cp) sst[cp] = kq == kk ? v[kk * RM + cp] : sst[cp];
+#pragma unroll
+        for (int cp = 0; cp < RM; ++cp) {
+          const int f = h - cp;
+          sst[cp] = (row_ok && f >= 0 && f < T) ? sst[cp] : neg_inf();
+        }
+      }
 #pragma unroll
       for (int j = 0; j < NB / 8; ++j) tc::tmem_ld8(x + 8 * j, s + 8 * j);
       tc::tmem_ld_wait();
@@ -1295,9 +1328,18 @@ __global__ void __launch_bounds__(320, 1)
       // have read it (every item writes the same positions; the rest stays zero)
       if (k > 0) tc::mbar_wait(&ofull[(k - 1) & 1], ((k - 1) >> 1) & 1);
       if (in_item) {
+        if constexpr (HM) {
+#pragma unroll
+          for (int q8 = 0; q8 < RM / 8; ++q8) {
+            const float* p8 = sst + 8 * q8;
+            tc::st_shared_v4(xs_addr(psa, r, i * RM + 8 * q8), make_uint4(pack_bf16(p8[0], p8[1]), pack_bf16(p8[2], p8[3]),
+                                                                       pack_bf16(p8[4], p8[5]), pack_bf16(p8[6], p8[7])));
+          }
+        } else {
 #pragma unroll
         for (int cp = 0; cp < RM; ++cp)
           if (cp < R) tc::st_shared_u16(xs_addr(psa, r, cp * HZ + i), __bfloat16_as_ushort(__float2bfloat16_rn(sst[cp])));
+        }
       }
       tc::tmem_st_wait();
       tc::fence_proxy_async_smem();
@@ -1321,7 +1363,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::named_bar(1 + wg, 128);
       if (r == 0) {
         if (tma_out) {
-          tc::tma_store_4d(&tmO, sbp, 0, h0, 0, bh);
+          tc::tma_store_4d(&tmO, sbp, 0, HM ? 0 : h0, HM ? h0 : 0, bh);
           tc::bulk_commit();
           tc::bulk_wait_read0();
         }
@@ -1491,14 +1533,15 @@ sattn_status bwd_fused_launch(const AttnArgs& a, int HZ, float* ws_del, float* w
 
 }  // namespace
 
-template <int NB, int RM>
+template <int NB, int RM, bool HM = false>
 sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st, const ItemSub* sub = nullptr) {
-  using Cf = LFCfg<NB, RM>;
+  using Cf = LFCfg<NB, RM, HM>;
   const int R = a.R, C = R + 1;
+  auto mskew = HM ? map_hm : map_skew;
   CUtensorMap mq, mkb, mvb, mks, mvs, mo;
-  if (!map_skew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map4(&mkb, a.K, a.T, a.BH, C, NB) ||
-      !map4(&mvb, a.V, a.T, a.BH, C, NB) || !map_skew(&mks, a.K, a.T, a.BH, C, R, HZ, R) ||
-      !map_skew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) || !map_skew(&mo, a.Out, a.T, a.BH, C, R, HZ, C)) {
+  if (!mskew(&mq, a.Q, a.T, a.BH, C, R, HZ, C) || !map4(&mkb, a.K, a.T, a.BH, C, NB) ||
+      !map4(&mvb, a.V, a.T, a.BH, C, NB) || !mskew(&mks, a.K, a.T, a.BH, C, R, HZ, R) ||
+      !mskew(&mvs, a.V, a.T, a.BH, C, R, HZ, R) || !mskew(&mo, a.Out, a.T, a.BH, C, R, HZ, C)) {
     g_err = "tensor maps of the item-form LLSA forward";
     return SATTN_ECUDA;
   }
@@ -1511,7 +1554,7 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st, const I
   const int items = la.sub.nit_l * a.BH;
   if (items == 0) return SATTN_OK;
   const int grid = items < num_sms() ? items : num_sms();
-  set_smem(llsa_fwd_item_tc<NB, RM>, Cf::SMEM);
+  set_smem(llsa_fwd_item_tc<NB, RM, HM>, Cf::SMEM);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(320);
@@ -1522,7 +1565,7 @@ sattn_status fwd_item_launch(const AttnArgs& a, int HZ, cudaStream_t st, const I
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_fwd_item_tc<NB, RM>, mq, mkb, mvb, mks, mvs, mo, la);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, llsa_fwd_item_tc<NB, RM, HM>, mq, mkb, mvb, mks, mvs, mo, la);
   if (e != cudaSuccess) {
     g_err = std::string("item-form LLSA forward launch: ") + cudaGetErrorString(e);
     return SATTN_ECUDA;
@@ -1544,6 +1587,25 @@ bool tc_llsa_supported(int dtype, int D, int L, int R) {
   return dtype == SATTN_BF16 && D == 64 && R >= 4 && R <= kRmax && L >= 1 && L + 32 <= 64;
 }
 
+// item-form forward: horizon-major items with the staircase on tcgen05 when R fills the RM
+// staircase columns (R = 8, 16), else the mma.sync staircase
+sattn_status fwd_item_dispatch(const AttnArgs& a, int hz, cudaStream_t st, const ItemSub* su) {
+  const bool r16 = a.R > 8;
+  const int nb = (hz + a.L + 15) / 16 * 16;
+  if ((a.R == 8 || a.R == 16) && (hz * a.R) % 16 == 0 && (nb == 48 || nb == 64)) {
+    if (nb == 48) return r16 ? fwd_item_launch<48, 16, true>(a, hz, st, su) : fwd_item_launch<48, 8, true>(a, hz, st, su);
+    return r16 ? fwd_item_launch<64, 16, true>(a, hz, st, su) : fwd_item_launch<64, 8, true>(a, hz, st, su);
+  }
+  switch (nb) {
+    case 16:
+    case 32: return r16 ? fwd_item_launch<32, 16>(a, hz, st, su) : fwd_item_launch<32, 8>(a, hz, st, su);
+    case 48: return r16 ? fwd_item_launch<48, 16>(a, hz, st, su) : fwd_item_launch<48, 8>(a, hz, st, su);
+    case 64: return r16 ? fwd_item_launch<64, 16>(a, hz, st, su) : fwd_item_launch<64, 8>(a, hz, st, su);
+  }
+  g_err = "band too wide for the item-form LLSA forward";
+  return SATTN_EUNSUPPORTED;
+}
+
 // item-form forward over an item subset (sub4 = it0, nit_l, it_split, it_jump per (b, h)); 0 when
 // the item form does not apply
 int tc_llsa_item_hz(const AttnArgs& a) {
@@ -1558,28 +1620,11 @@ sattn_status tc_llsa_forward_items(const AttnArgs& a, const int* sub4, cudaStrea
     return SATTN_EUNSUPPORTED;
   }
   const ItemSub su{sub4[0], sub4[1], sub4[2], sub4[3]};
-  const bool r16 = a.R > 8;
-  switch ((hz + a.L + 15) / 16 * 16) {
-    case 16:
-    case 32: return r16 ? fwd_item_launch<32, 16>(a, hz, st, &su) : fwd_item_launch<32, 8>(a, hz, st, &su);
-    case 48: return r16 ? fwd_item_launch<48, 16>(a, hz, st, &su) : fwd_item_launch<48, 8>(a, hz, st, &su);
-    case 64: return r16 ? fwd_item_launch<64, 16>(a, hz, st, &su) : fwd_item_launch<64, 8>(a, hz, st, &su);
-  }
-  g_err = "band too wide for the item-form LLSA forward";
-  return SATTN_EUNSUPPORTED;
+  return fwd_item_dispatch(a, hz, st, &su);
 }
 
 sattn_status tc_llsa_forward(const AttnArgs& a, cudaStream_t st) {
-  if (fwd_item_ok(a)) {
-    const int hz = fused_hz(a.L, a.R);
-    const bool r16 = a.R > 8;
-    switch ((hz + a.L + 15) / 16 * 16) {
-      case 16:
-      case 32: return r16 ? fwd_item_launch<32, 16>(a, hz, st) : fwd_item_launch<32, 8>(a, hz, st);
-      case 48: return r16 ? fwd_item_launch<48, 16>(a, hz, st) : fwd_item_launch<48, 8>(a, hz, st);
-      case 64: return r16 ? fwd_item_launch<64, 16>(a, hz, st) : fwd_item_launch<64, 8>(a, hz, st);
-    }
-  }
+  if (fwd_item_ok(a)) return fwd_item_dispatch(a, fused_hz(a.L, a.R), st, nullptr);
   const int nb = (32 + a.L + 15) / 16 * 16;
   switch (nb) {
     case 48: return launch<48>(a, st);
