@@ -123,6 +123,9 @@ LLSA_CASES = [
     ("bf16", (1, 2, 400, 64), 48, 16), ("bf16", (2, 2, 513, 64), 20, 12),
     # packed kv tiles over the flattened B*H*T axis: heads shorter than a key tile
     ("bf16", (2, 3, 60, 64), 32, 8), ("bf16", (3, 2, 20, 64), 16, 4),
+    # horizon-major items (R = 8, 16: staircase on tcgen05) with fewer frames than an item's
+    # horizons, and L = 0
+    ("bf16", (2, 2, 10, 64), 32, 8), ("bf16", (1, 3, 25, 64), 8, 16), ("bf16", (2, 1, 200, 64), 0, 8),
 ]
 
 
