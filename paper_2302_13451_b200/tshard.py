@@ -60,13 +60,16 @@ def exchange_halo(x: torch.Tensor, left: int, right: int, group=None):
     return torch.cat(parts, dim=-2), (left if recv_l is not None else 0)
 
 
-def _halo(width: int, align: int, T_loc: int, group) -> int:
-    """`width` rounded up to `align` if every shard can supply it (agreed across ranks)."""
-    t = torch.tensor([T_loc], dtype=torch.int64)
-    if dist.get_backend(group) == "nccl":
-        t = t.cuda()
-    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
-    min_T = int(t.item())
+def _halo(width: int, align: int, T_loc: int, group, min_T: int | None = None) -> int:
+    """`width` rounded up to `align` if every shard can supply it (agreed across ranks).  `min_T`,
+    the smallest shard's frames, when the caller knows it (e.g. from shard_bounds): then no
+    collective and no host synchronisation; else a MIN all-reduce of T_loc."""
+    if min_T is None:
+        t = torch.tensor([T_loc], dtype=torch.int64)
+        if dist.get_backend(group) == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        min_T = int(t.item())
     if width > min_T:
         raise ValueError(f"shards of {min_T} frames cannot supply a {width}-frame halo: use fewer ranks")
     r = _round_up(width, align) if width else 0
@@ -95,25 +98,25 @@ def _stack_bwd_default(x, dy, L, R, n, mode):
 
 
 def stack_forward_tsharded(x, L: int, R: int, n_layers: int, mode: int = 0, group=None, align: int = 128,
-                           stack_fwd=None):
+                           stack_fwd=None, min_T: int | None = None):
     """x: this rank's slab [B, H, T_loc, D].  Returns this rank's rows of the n-layer stack
     output (SA: [B, H, T_loc, D]; LLSA mode 1: [C, B, H, T_loc, D])."""
     stack_fwd = stack_fwd or _stack_fwd_default
     T_loc = x.shape[-2]
     back = n_layers * (L + R) if mode == 1 else n_layers * L
-    hl, hr = _halo(back, align, T_loc, group), _halo(n_layers * R, align, T_loc, group)
+    hl, hr = _halo(back, align, T_loc, group, min_T), _halo(n_layers * R, align, T_loc, group, min_T)
     x_e, nl = exchange_halo(x, hl, hr, group)
     y = stack_fwd(x_e, L, R, n_layers, mode)
     return y[..., nl:nl + T_loc, :].contiguous()
 
 
 def stack_backward_tsharded(x, dy, L: int, R: int, n_layers: int, mode: int = 0, group=None, align: int = 128,
-                            stack_bwd=None):
+                            stack_bwd=None, min_T: int | None = None):
     """x: this rank's input slab [B, H, T_loc, D]; dy: its rows of dL/dY (SA [B, H, T_loc, D],
     LLSA [C, B, H, T_loc, D]).  Returns this rank's rows of dL/dX_0."""
     stack_bwd = stack_bwd or _stack_bwd_default
     T_loc = x.shape[-2]
-    h = _halo(2 * n_layers * (L + R), align, T_loc, group)
+    h = _halo(2 * n_layers * (L + R), align, T_loc, group, min_T)
     x_e, nl = exchange_halo(x, h, h, group)
     dy_e, _ = exchange_halo(dy, h, h, group)
     dx = stack_bwd(x_e, dy_e, L, R, n_layers, mode)

@@ -50,6 +50,11 @@ def _stack_worker(rank, world, port, T, L, R, n, mode, out):
     dyl = torch.from_numpy(dy[..., t0:t1, :].copy())
     y = tshard.stack_forward_tsharded(xl, L, R, n, mode, align=1, stack_fwd=fwd)
     dx = tshard.stack_backward_tsharded(xl, dyl, L, R, n, mode, align=1, stack_bwd=bwd)
+    # the smallest shard known from the partition: no agreeing all-reduce, the same halos
+    min_T = min(b - a for a, b in (tshard.shard_bounds(T, world, r, 1) for r in range(world)))
+    y2 = tshard.stack_forward_tsharded(xl, L, R, n, mode, align=1, stack_fwd=fwd, min_T=min_T)
+    dx2 = tshard.stack_backward_tsharded(xl, dyl, L, R, n, mode, align=1, stack_bwd=bwd, min_T=min_T)
+    assert torch.equal(y, y2) and torch.equal(dx, dx2)
     Y = ostack.stack_forward(x, L, R, n, mname)[0]
     DX = ostack.stack_backward(x, dy, L, R, n, mname)
     out[rank] = max(float(np.abs(y.numpy() - Y[..., t0:t1, :]).max()),
